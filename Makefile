@@ -1,0 +1,28 @@
+# Build every native artefact in-tree (the .so files travel to the GPU box).
+#   gen/libpfacgen.so                 seeded input generators (inputs only)
+#   oracle/liboracle.so               CPU oracle (test infrastructure only)
+#   paper_1702_03657_b200/libpfac.so  the product: host builder + sm_100a kernels + C ABI
+NVCC    ?= /usr/local/cuda/bin/nvcc
+CC      ?= gcc
+CFLAGS  := -O2 -g -fPIC -Wall -Wextra -std=gnu11
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC,-Wall -Iinclude --expt-relaxed-constexpr
+PKG     := paper_1702_03657_b200
+CSRC    := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cpp)
+CHDR    := $(wildcard $(PKG)/csrc/*.h) $(wildcard $(PKG)/csrc/*.cuh) include/pfac.h
+
+all: gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so
+
+gen/libpfacgen.so: gen/pfac_gen.c gen/pfac_gen.h
+	$(CC) $(CFLAGS) -shared -o $@ gen/pfac_gen.c -lm -lpthread
+
+oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
+	$(CC) $(CFLAGS) -shared -o $@ oracle/oracle.c -lpthread
+
+$(PKG)/libpfac.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) -lcudart
+
+clean:
+	rm -f gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so
+
+.PHONY: all clean
