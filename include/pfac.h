@@ -1,0 +1,158 @@
+/*
+ * pfac.h -- C ABI of the B200-native PFAC scan (arXiv 1702.03657).
+ *
+ * The operation (§II-B "searching for a pattern P in a text T";
+ * PAPER.md:76 §II-C parallel failure-less Aho-Corasick: "Each thread is
+ * assigned to a single letter in the text T. If a match is recorded, the
+ * thread continues the matching process until a mismatch."): given patterns
+ * P_0..P_{m-1} (byte strings, |P_k| >= 1, pid k = input index) and text T,
+ *
+ *     M = { (i, k) : i + |P_k| <= L  and  T[i .. i+|P_k|) == P_k }
+ *
+ * listed in ascending (pos, pid) order (BASELINE.json north_star; SURVEY.md
+ * §8(c) ledger L1-L3).  The trie is built on the host (PAPER.md:80 steps I-II,
+ * breadth-first, row-major), compressed to a CSR image
+ * and scanned by sm_100a kernels; no step runs on the CPU at match time and
+ * there is no CPU fallback: without a usable CUDA device the match calls
+ * return PFAC_ERR_CUDA.
+ *
+ * Conventions:
+ *  - Every entry point returns pfac_status (or void for the free functions);
+ *    nothing aborts, exits or throws across this boundary.  On failure
+ *    pfac_last_error() returns thread-local detail text.
+ *  - Handles are immutable after pfac_build/pfac_attach; a const handle may be
+ *    used by any number of host threads concurrently (the lazy per-device
+ *    upload is internally locked).
+ *  - Sizes are bytes unless stated.  Positions are u64, pattern ids u32.
+ */
+#ifndef PFAC_H
+#define PFAC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pfac_trie pfac_trie;   /* opaque */
+typedef struct CUstream_st *pfac_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    PFAC_OK = 0,
+    PFAC_ERR_INVALID_ARG = 1,  /* NULL pointer, n_patterns == 0, zero-length pattern, length > 65535, bad enum, bad image */
+    PFAC_ERR_LIMIT = 2,        /* trie exceeds 2^31-1 nodes or 2^32-1 pattern-id-list entries */
+    PFAC_ERR_NOMEM = 3,        /* host or device allocation failed */
+    PFAC_ERR_CUDA = 4,         /* no usable device / CUDA runtime error (detail in pfac_last_error) */
+    PFAC_ERR_CAPACITY = 5      /* (pfac_match only, never device path) internal retry failed */
+} pfac_status;
+
+typedef enum {
+    PFAC_BYTES_DEVICE_IMAGE = 0,  /* the whole device image: CSR trie + terminal tables + scan filter + root table */
+    PFAC_BYTES_UNCOMPRESSED = 1,  /* the paper's original trie: 36 B per node (256-bit bitmap + u32 offset) */
+    PFAC_BYTES_DENSE_STT = 2,     /* Lin et al. PFAC state table: 256 x u32 per node */
+    PFAC_BYTES_PAPER_CRS = 3,     /* paper CRS of the N x 9 word matrix: (2 nnz + n + 1) x 4 B */
+    PFAC_BYTES_CSR_CORE = 4       /* the CSR trie alone: row_ptr|terminal flag (4 B/node) + labels (1 B/edge) */
+} pfac_bytes_kind;
+
+typedef struct {
+    uint64_t nodes;       /* 1 + number of distinct non-empty pattern prefixes */
+    uint64_t edges;       /* nodes - 1 */
+    uint64_t terminals;   /* nodes where at least one pattern ends */
+    uint32_t n_patterns;
+    uint32_t max_len;     /* longest pattern; (max_len - 1) is the halo a shard must read */
+    uint32_t min_len;
+    uint32_t filter_gram; /* d of the d-gram first-stage filter (<= min(4, min_len)) */
+    uint32_t filter_log2_bits;
+    uint32_t reserved;
+} pfac_stats;
+
+/* Host-side result of pfac_match: library-allocated, free with pfac_matches_free.
+ * count == 0 => pos == pid == NULL. */
+typedef struct {
+    uint64_t count;
+    uint64_t *pos;
+    uint32_t *pid;
+} pfac_matches;
+
+/* ---------------------------------------------------------------- build */
+
+/* Builds the trie of `n_patterns` patterns.  patterns[k] points at lengths[k]
+ * bytes (not NUL-terminated, may contain 0x00); they are copied, so the caller
+ * may free them on return.  Duplicates are accepted and each id is reported.
+ * Errors: INVALID_ARG (see enum), LIMIT, NOMEM.  *out is NULL on error. */
+pfac_status pfac_build(const uint8_t *const *patterns, const uint32_t *lengths, uint32_t n_patterns,
+                       pfac_trie **out);
+
+/* Same, patterns concatenated in `data` (offset of k = sum of lengths[0..k)). */
+pfac_status pfac_build_concat(const uint8_t *data, const uint32_t *lengths, uint32_t n_patterns,
+                              pfac_trie **out);
+
+/* Frees the host image and every device copy.  NULL-safe. */
+void pfac_free(pfac_trie *t);
+
+/* Byte accounting of the trie (PAPER.md:134 36 B/node; PAPER.md:101 CRS cost). */
+pfac_status pfac_trie_bytes(const pfac_trie *t, pfac_bytes_kind kind, uint64_t *out_bytes);
+
+pfac_status pfac_trie_stats(const pfac_trie *t, pfac_stats *out);
+
+/* The serialised device image (host memory owned by t, valid until pfac_free).
+ * This is what a multi-GPU driver broadcasts (NCCL) before pfac_attach. */
+pfac_status pfac_image(const pfac_trie *t, const void **host_bytes, uint64_t *size);
+
+/* Creates a handle from an image produced by pfac_image, which may live in
+ * host memory or in device memory of `device` (detected with
+ * cudaPointerGetAttributes).  The image is copied; it is validated (magic,
+ * version, section bounds) and INVALID_ARG is returned for a bad image. */
+pfac_status pfac_attach(const void *image, uint64_t size, int device, pfac_trie **out);
+
+/* ------------------------------------------------------------ match, host */
+
+/* Matches `text` (HOST memory, len bytes) on the current CUDA device:
+ * H2D copy, scan, D2H of the sorted (pos, pid) rows.  Synchronous.
+ * len == 0 gives count 0.  Returns CUDA on any device failure. */
+pfac_status pfac_match(const pfac_trie *t, const uint8_t *text, uint64_t len, pfac_matches *out);
+
+void pfac_matches_free(pfac_matches *m);
+
+/* --------------------------------------------------------- match, device */
+
+/* Workspace bytes pfac_match_device needs for n_starts start positions. */
+pfac_status pfac_workspace_bytes(const pfac_trie *t, uint64_t n_starts, uint64_t *out);
+
+/* Stream-ordered scan on `device` (which must be the current device), all
+ * pointers device memory:
+ *   d_text[0 .. readable_len)   text; bytes [n_starts, readable_len) are the
+ *                               read-only halo (a shard's successor bytes):
+ *                               readable, never a start.  n_starts <= readable_len.
+ *   result: { (pos_base + i, k) : i < n_starts, i + |P_k| <= readable_len,
+ *             T[i .. i+|P_k|) == P_k } sorted by (pos, pid), written to
+ *             d_pos[0..min(count, capacity)) / d_pid[...]; *d_count (u64,
+ *             device) always receives the true count.  If count > capacity
+ *             nothing past capacity is written: re-run with larger buffers.
+ *   d_workspace: >= pfac_workspace_bytes(t, n_starts) bytes, 256-B aligned,
+ *             ZERO-FILLED BEFORE ITS FIRST USE; the kernels leave it ready for
+ *             the next call.  One workspace must not be used by two calls
+ *             that can run concurrently.
+ * No host synchronisation inside; kernel faults surface at the caller's next
+ * sync.  Launch errors return PFAC_ERR_CUDA.  The device copy of the trie is
+ * uploaded on first use per device (synchronously, once). */
+pfac_status pfac_match_device(const pfac_trie *t, int device, const uint8_t *d_text,
+                              uint64_t readable_len, uint64_t n_starts, uint64_t pos_base,
+                              uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+                              uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
+                              pfac_stream stream);
+
+/* Number of kernel launches one pfac_match_device call makes (for the bench's
+ * gpu_launches count). */
+uint32_t pfac_launches_per_call(void);
+
+/* ------------------------------------------------------------------ misc */
+const char *pfac_status_string(pfac_status s);
+const char *pfac_last_error(void);
+/* Version string, e.g. "pfac-b200 0.1 sm_100a". */
+const char *pfac_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFAC_H */

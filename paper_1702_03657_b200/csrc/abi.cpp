@@ -1,0 +1,324 @@
+// abi.cpp -- extern "C" entry points of libpfac.so (declared in include/pfac.h).
+// No exception crosses this boundary; errors set a thread-local message.
+#include "pfac.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace pfac;
+
+struct pfac_trie {
+    std::vector<uint8_t> image;
+    ImageHeader hdr;
+    std::mutex mu;                  // guards dev (lazy per-device upload)
+    std::map<int, void *> dev;      // device ordinal -> device copy of the image
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+pfac_status fail(int st, const std::string &msg) {
+    g_err = msg;
+    return (pfac_status)st;
+}
+
+pfac_status cuda_fail(const char *what, cudaError_t e) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return PFAC_ERR_CUDA;
+}
+
+pfac_status finish_handle(std::vector<uint8_t> &&img, pfac_trie **out) {
+    pfac_trie *t = new (std::nothrow) pfac_trie();
+    if (!t) return fail(kStatusNomem, "out of host memory");
+    t->image = std::move(img);
+    std::memcpy(&t->hdr, t->image.data(), sizeof(ImageHeader));
+    *out = t;
+    return PFAC_OK;
+}
+
+// Device copy of the image on `device` (uploaded on first use).
+pfac_status device_image(const pfac_trie *tc, int device, const uint8_t **d_img) {
+    pfac_trie *t = const_cast<pfac_trie *>(tc);
+    std::lock_guard<std::mutex> lk(t->mu);
+    auto it = t->dev.find(device);
+    if (it != t->dev.end()) {
+        *d_img = static_cast<const uint8_t *>(it->second);
+        return PFAC_OK;
+    }
+    int prev = -1;
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return cuda_fail("cudaGetDevice", e);
+    if (prev != device && (e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail("cudaSetDevice", e);
+    void *p = nullptr;
+    e = cudaMalloc(&p, t->image.size());
+    if (e == cudaSuccess) e = cudaMemcpy(p, t->image.data(), t->image.size(), cudaMemcpyHostToDevice);
+    if (prev != device) cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        if (p) cudaFree(p);
+        return cuda_fail("uploading the trie image", e);
+    }
+    t->dev[device] = p;
+    *d_img = static_cast<const uint8_t *>(p);
+    return PFAC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pfac_status pfac_build(const uint8_t *const *patterns, const uint32_t *lengths, uint32_t n_patterns,
+                       pfac_trie **out) {
+    if (!out) return fail(kStatusInvalid, "pfac_build: out is NULL");
+    *out = nullptr;
+    try {
+        std::vector<uint8_t> img;
+        std::string err;
+        int st = build_image(patterns, lengths, n_patterns, img, err);
+        if (st != kStatusOk) return fail(st, err);
+        return finish_handle(std::move(img), out);
+    } catch (const std::bad_alloc &) {
+        return fail(kStatusNomem, "pfac_build: out of host memory");
+    } catch (...) {
+        return fail(kStatusInvalid, "pfac_build: unexpected error");
+    }
+}
+
+pfac_status pfac_build_concat(const uint8_t *data, const uint32_t *lengths, uint32_t n_patterns, pfac_trie **out) {
+    if (!out) return fail(kStatusInvalid, "pfac_build_concat: out is NULL");
+    *out = nullptr;
+    if (!lengths || n_patterns == 0) return fail(kStatusInvalid, "pfac_build_concat: no patterns");
+    try {
+        std::vector<const uint8_t *> ptrs(n_patterns);
+        uint64_t off = 0;
+        for (uint32_t k = 0; k < n_patterns; k++) {
+            ptrs[k] = data ? data + off : nullptr;
+            off += lengths[k];
+        }
+        return pfac_build(ptrs.data(), lengths, n_patterns, out);
+    } catch (...) {
+        return fail(kStatusNomem, "pfac_build_concat: out of host memory");
+    }
+}
+
+void pfac_free(pfac_trie *t) {
+    if (!t) return;
+    for (auto &kv : t->dev) {
+        int prev = -1;
+        if (cudaGetDevice(&prev) == cudaSuccess) {
+            cudaSetDevice(kv.first);
+            cudaFree(kv.second);
+            cudaSetDevice(prev);
+        }
+    }
+    delete t;
+}
+
+pfac_status pfac_trie_bytes(const pfac_trie *t, pfac_bytes_kind kind, uint64_t *out) {
+    if (!t || !out) return fail(kStatusInvalid, "pfac_trie_bytes: NULL argument");
+    switch (kind) {
+    case PFAC_BYTES_DEVICE_IMAGE: *out = t->hdr.image_bytes; break;
+    case PFAC_BYTES_UNCOMPRESSED: *out = t->hdr.bytes_uncompressed; break;
+    case PFAC_BYTES_DENSE_STT: *out = t->hdr.bytes_dense_stt; break;
+    case PFAC_BYTES_PAPER_CRS: *out = t->hdr.bytes_paper_crs; break;
+    case PFAC_BYTES_CSR_CORE: *out = t->hdr.bytes_csr_core; break;
+    default: return fail(kStatusInvalid, "pfac_trie_bytes: bad kind");
+    }
+    return PFAC_OK;
+}
+
+pfac_status pfac_trie_stats(const pfac_trie *t, pfac_stats *o) {
+    if (!t || !o) return fail(kStatusInvalid, "pfac_trie_stats: NULL argument");
+    std::memset(o, 0, sizeof *o);
+    o->nodes = t->hdr.n_nodes;
+    o->edges = t->hdr.n_edges;
+    o->terminals = t->hdr.n_terminals;
+    o->n_patterns = t->hdr.n_patterns;
+    o->max_len = t->hdr.max_len;
+    o->min_len = t->hdr.min_len;
+    o->filter_gram = t->hdr.filter_gram;
+    o->filter_log2_bits = t->hdr.filter_log2_bits;
+    return PFAC_OK;
+}
+
+pfac_status pfac_image(const pfac_trie *t, const void **host_bytes, uint64_t *size) {
+    if (!t || !host_bytes || !size) return fail(kStatusInvalid, "pfac_image: NULL argument");
+    *host_bytes = t->image.data();
+    *size = t->image.size();
+    return PFAC_OK;
+}
+
+pfac_status pfac_attach(const void *image, uint64_t size, int device, pfac_trie **out) {
+    if (!out || !image) return fail(kStatusInvalid, "pfac_attach: NULL argument");
+    *out = nullptr;
+    try {
+        std::vector<uint8_t> img(size);
+        cudaPointerAttributes attr;
+        cudaError_t e = cudaPointerGetAttributes(&attr, image);
+        if (e != cudaSuccess) cudaGetLastError();  // plain host pointer on older runtimes
+        if (e == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+            e = cudaMemcpy(img.data(), image, size, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return cuda_fail("pfac_attach: copying the device image", e);
+        } else {
+            std::memcpy(img.data(), image, size);
+        }
+        std::string err;
+        int st = validate_image(img.data(), size, err);
+        if (st != kStatusOk) return fail(st, err);
+        pfac_status s = finish_handle(std::move(img), out);
+        if (s != PFAC_OK) return s;
+        const uint8_t *d = nullptr;
+        if (device >= 0) {
+            s = device_image(*out, device, &d);
+            if (s != PFAC_OK) {
+                pfac_free(*out);
+                *out = nullptr;
+                return s;
+            }
+        }
+        return PFAC_OK;
+    } catch (const std::bad_alloc &) {
+        return fail(kStatusNomem, "pfac_attach: out of host memory");
+    }
+}
+
+pfac_status pfac_workspace_bytes(const pfac_trie *t, uint64_t n_starts, uint64_t *out) {
+    if (!t || !out) return fail(kStatusInvalid, "pfac_workspace_bytes: NULL argument");
+    *out = workspace_bytes_for(n_starts);
+    return PFAC_OK;
+}
+
+pfac_status pfac_match_device(const pfac_trie *t, int device, const uint8_t *d_text, uint64_t readable_len,
+                              uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                              uint64_t capacity, uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
+                              pfac_stream stream) {
+    if (!t || !d_count || (n_starts && !d_text) || (capacity && (!d_pos || !d_pid)))
+        return fail(kStatusInvalid, "pfac_match_device: NULL argument");
+    if (n_starts > readable_len) return fail(kStatusInvalid, "pfac_match_device: n_starts > readable_len");
+    const uint8_t *d_img = nullptr;
+    pfac_status s = device_image(t, device, &d_img);
+    if (s != PFAC_OK) return s;
+    DevTrie dt = make_dev_trie(t->hdr, d_img);
+    std::string err;
+    int st = launch_scan(dt, device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
+                         d_workspace, workspace_bytes, reinterpret_cast<CUstream_st *>(stream), err);
+    if (st != kStatusOk) return fail(st, err);
+    return PFAC_OK;
+}
+
+pfac_status pfac_match(const pfac_trie *t, const uint8_t *text, uint64_t len, pfac_matches *out) {
+    if (!t || !out || (len && !text)) return fail(kStatusInvalid, "pfac_match: NULL argument");
+    out->count = 0;
+    out->pos = nullptr;
+    out->pid = nullptr;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail("pfac_match: no CUDA device", e);
+    if (len == 0) {
+        const uint8_t *d_img = nullptr;
+        return device_image(t, dev, &d_img);  // still requires a working device
+    }
+    uint64_t ws_bytes = workspace_bytes_for(len);
+    uint64_t cap = len / 256 + 4096;
+    uint8_t *d_text = nullptr;
+    void *d_ws = nullptr;
+    uint64_t *d_pos = nullptr, *d_count = nullptr;
+    uint32_t *d_pid = nullptr;
+    cudaStream_t st = nullptr;
+    pfac_status rs = PFAC_OK;
+    uint64_t count = 0;
+    auto cleanup = [&]() {
+        cudaFree(d_text); cudaFree(d_ws); cudaFree(d_pos); cudaFree(d_pid); cudaFree(d_count);
+        if (st) cudaStreamDestroy(st);
+    };
+    if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaMalloc(&d_text, len)) != cudaSuccess || (e = cudaMalloc(&d_ws, ws_bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&d_count, 8)) != cudaSuccess || (e = cudaMalloc(&d_pos, cap * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&d_pid, cap * 4)) != cudaSuccess) {
+        cleanup();
+        return cuda_fail("pfac_match: device allocation", e);
+    }
+    if ((e = cudaMemcpyAsync(d_text, text, len, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemsetAsync(d_ws, 0, ws_bytes, st)) != cudaSuccess) {
+        cleanup();
+        return cuda_fail("pfac_match: H2D", e);
+    }
+    for (int attempt = 0; attempt < 2; attempt++) {
+        rs = pfac_match_device(t, dev, d_text, len, len, 0, d_pos, d_pid, cap, d_count, d_ws, ws_bytes,
+                               reinterpret_cast<pfac_stream>(st));
+        if (rs != PFAC_OK) break;
+        if ((e = cudaMemcpyAsync(&count, d_count, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+            rs = cuda_fail("pfac_match: scan", e);
+            break;
+        }
+        if (count <= cap) break;
+        // count-and-retry with exact capacity
+        cudaFree(d_pos); cudaFree(d_pid);
+        d_pos = nullptr; d_pid = nullptr;
+        cap = count;
+        if ((e = cudaMalloc(&d_pos, cap * 8)) != cudaSuccess || (e = cudaMalloc(&d_pid, cap * 4)) != cudaSuccess) {
+            rs = cuda_fail("pfac_match: device allocation", e);
+            break;
+        }
+        if (attempt == 1) rs = fail(kStatusCapacity, "pfac_match: capacity retry failed");
+    }
+    if (rs == PFAC_OK && count > 0) {
+        out->pos = static_cast<uint64_t *>(std::malloc(count * 8));
+        out->pid = static_cast<uint32_t *>(std::malloc(count * 4));
+        if (!out->pos || !out->pid) {
+            std::free(out->pos); std::free(out->pid);
+            out->pos = nullptr; out->pid = nullptr;
+            rs = fail(kStatusNomem, "pfac_match: out of host memory");
+        } else if ((e = cudaMemcpyAsync(out->pos, d_pos, count * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+                   (e = cudaMemcpyAsync(out->pid, d_pid, count * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+                   (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+            std::free(out->pos); std::free(out->pid);
+            out->pos = nullptr; out->pid = nullptr;
+            rs = cuda_fail("pfac_match: D2H", e);
+        } else {
+            out->count = count;
+        }
+    }
+    cleanup();
+    return rs;
+}
+
+void pfac_matches_free(pfac_matches *m) {
+    if (!m) return;
+    std::free(m->pos);
+    std::free(m->pid);
+    m->pos = nullptr;
+    m->pid = nullptr;
+    m->count = 0;
+}
+
+uint32_t pfac_launches_per_call(void) { return launches_per_call(); }
+
+const char *pfac_status_string(pfac_status s) {
+    switch (s) {
+    case PFAC_OK: return "PFAC_OK";
+    case PFAC_ERR_INVALID_ARG: return "PFAC_ERR_INVALID_ARG";
+    case PFAC_ERR_LIMIT: return "PFAC_ERR_LIMIT";
+    case PFAC_ERR_NOMEM: return "PFAC_ERR_NOMEM";
+    case PFAC_ERR_CUDA: return "PFAC_ERR_CUDA";
+    case PFAC_ERR_CAPACITY: return "PFAC_ERR_CAPACITY";
+    }
+    return "PFAC_ERR_UNKNOWN";
+}
+
+const char *pfac_last_error(void) { return g_err.c_str(); }
+
+const char *pfac_version(void) { return "pfac-b200 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+// builder.cpp -- host trie builder: patterns -> breadth-first CSR device image.
+//
+// PAPER.md:80 step I ("constructed in a breadth-first approach, level by
+// level") and step II ("stored in a row major ordered array"), then the CRS
+// step of PAPER.md:89/:101 in label form (see image.h).  Steps III-V
+// (truncation, suffix/end-node merging) are NOT applied: the scan must report
+// exact (position, pattern-id) rows, which a truncated or merged trie cannot
+// (they are §8(f) NEXT-1/2).
+//
+// Construction: sort the pattern ids lexicographically (ties by id); every
+// trie node is then a contiguous range of that order sharing a prefix of
+// length `depth`.  Expanding ranges in FIFO order numbers the nodes in BFS
+// order with children in ascending byte order -- exactly the row-major layout
+// whose child through edge e is node e+1.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "image.h"
+#include "internal.h"
+
+namespace pfac {
+
+namespace {
+
+struct Range {
+    uint32_t lo, hi;    // [lo, hi) of the sorted order
+    uint32_t depth;     // prefix length shared by the range
+    uint32_t anc_term;  // index of the nearest terminal ancestor (kNone = none)
+};
+
+inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+}  // namespace
+
+int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, std::vector<uint8_t> &image,
+                std::string &err) {
+    if (!pats || !lens || m == 0) {
+        err = "pfac_build: NULL argument or n_patterns == 0";
+        return kStatusInvalid;
+    }
+    uint32_t max_len = 0, min_len = kNone;
+    for (uint32_t k = 0; k < m; k++) {
+        if (lens[k] == 0 || lens[k] > kMaxPatternLen) {
+            err = "pfac_build: pattern " + std::to_string(k) + " has length " + std::to_string(lens[k]) +
+                  " (must be 1.." + std::to_string(kMaxPatternLen) + ")";
+            return kStatusInvalid;
+        }
+        if (!pats[k]) {
+            err = "pfac_build: pattern pointer " + std::to_string(k) + " is NULL";
+            return kStatusInvalid;
+        }
+        max_len = std::max(max_len, lens[k]);
+        min_len = std::min(min_len, lens[k]);
+    }
+
+    // ---- sort ids lexicographically (a proper prefix sorts first), ties by id
+    std::vector<uint32_t> ord(m);
+    std::iota(ord.begin(), ord.end(), 0u);
+    std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) {
+        uint32_t l = std::min(lens[a], lens[b]);
+        int c = std::memcmp(pats[a], pats[b], l);
+        if (c != 0) return c < 0;
+        if (lens[a] != lens[b]) return lens[a] < lens[b];
+        return a < b;
+    });
+
+    // ---- step I/II: FIFO expansion of ranges == BFS numbering
+    std::vector<uint32_t> node_word;   // row_ptr | terminal bit, per node
+    std::vector<uint8_t> label;        // label of edge e (child e+1)
+    std::vector<uint32_t> term_node, out_ptr{0}, out_pid;
+    uint64_t paper_nnz = 0;
+
+    std::vector<Range> q;
+    q.reserve(1024);
+    q.push_back({0, m, 0, kNone});
+    std::vector<uint32_t> own;
+    for (size_t head = 0; head < q.size(); head++) {
+        if (q.size() > (size_t)kEdgeMask) {
+            err = "pfac_build: trie exceeds 2^31-1 nodes";
+            return kStatusLimit;
+        }
+        const Range r = q[head];
+        uint32_t v = (uint32_t)head;
+        // patterns ending exactly here sort first in the range
+        uint32_t lo = r.lo;
+        own.clear();
+        while (lo < r.hi && lens[ord[lo]] == r.depth) own.push_back(ord[lo++]);
+        uint32_t anc = r.anc_term;
+        bool terminal = !own.empty();
+        // row_ptr[v] = number of nodes numbered before v's first child, minus the root
+        uint32_t first_edge = (uint32_t)(q.size() - 1);
+        node_word.push_back(first_edge | (terminal ? kTermBit : 0u));
+        if (terminal) {
+            // union list = (ancestor's union) merged with own ids (both ascending)
+            std::sort(own.begin(), own.end());
+            std::vector<uint32_t> merged;
+            if (anc != kNone) {
+                merged.assign(out_pid.begin() + out_ptr[anc], out_pid.begin() + out_ptr[anc + 1]);
+            }
+            std::vector<uint32_t> u(merged.size() + own.size());
+            std::merge(merged.begin(), merged.end(), own.begin(), own.end(), u.begin());
+            if ((uint64_t)out_pid.size() + u.size() > 0xFFFFFFFEull) {
+                err = "pfac_build: pattern-id lists exceed 2^32-2 entries";
+                return kStatusLimit;
+            }
+            out_pid.insert(out_pid.end(), u.begin(), u.end());
+            term_node.push_back(v);
+            out_ptr.push_back((uint32_t)out_pid.size());
+            anc = (uint32_t)(term_node.size() - 1);
+        }
+        // children: partition [lo, hi) by the byte at position depth
+        int last_word = -1;
+        uint32_t i = lo;
+        if (i < r.hi) paper_nnz += 1;  // the non-zero offset column (P:101 matrix view)
+        while (i < r.hi) {
+            uint8_t c = pats[ord[i]][r.depth];
+            uint32_t j = i + 1;
+            while (j < r.hi && pats[ord[j]][r.depth] == c) j++;
+            label.push_back(c);
+            if ((int)(c >> 5) != last_word) {  // distinct non-zero bitmap word
+                paper_nnz += 1;
+                last_word = c >> 5;
+            }
+            q.push_back({i, j, r.depth + 1, anc});
+            i = j;
+        }
+    }
+    const uint64_t N = q.size(), E = N - 1, T = term_node.size();
+    node_word.push_back((uint32_t)E);  // row_ptr[N]
+
+    // ---- derived tables: level-1 direct table and first-stage d-gram filter
+    std::vector<uint32_t> root(256, 0);
+    {
+        uint32_t s = node_word[0] & kEdgeMask, e = node_word[1] & kEdgeMask;
+        for (uint32_t k = s; k < e; k++) root[label[k]] = k + 1;
+    }
+    const uint32_t gram = std::min<uint32_t>(4, min_len);
+    uint32_t exact = gram <= 2 ? 1u : 0u;
+    uint32_t log2_bits;
+    if (exact) {
+        log2_bits = 8 * gram;
+    } else {
+        // distinct d-grams -> ~32 filter bits per key (false-positive rate
+        // ~3%), between 2^10 and 2^19 bits (64 KiB, the shared-memory budget)
+        std::vector<uint32_t> keys(m);
+        for (uint32_t k = 0; k < m; k++) {
+            uint32_t x = 0;
+            for (uint32_t b = 0; b < gram; b++) x |= (uint32_t)pats[k][b] << (8 * b);
+            keys[k] = x;
+        }
+        std::sort(keys.begin(), keys.end());
+        uint64_t distinct = std::unique(keys.begin(), keys.end()) - keys.begin();
+        log2_bits = 10;
+        while (log2_bits < 19 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+    }
+    std::vector<uint32_t> filter((size_t)1 << (log2_bits - 5 > 0 ? log2_bits - 5 : 0), 0u);
+    if (filter.empty()) filter.resize(1);
+    for (uint32_t k = 0; k < m; k++) {
+        uint32_t x = 0;
+        for (uint32_t b = 0; b < gram; b++) x |= (uint32_t)pats[k][b] << (8 * b);
+        uint32_t h = filter_index(x, log2_bits, exact);
+        filter[h >> 5] |= 1u << (h & 31);
+    }
+
+    // ---- assemble the image
+    ImageHeader h;
+    std::memset(&h, 0, sizeof h);
+    std::memcpy(h.magic, "PFACIMG1", 8);
+    h.version = kVersion;
+    h.header_bytes = sizeof(ImageHeader);
+    h.n_nodes = N;
+    h.n_edges = E;
+    h.n_terminals = T;
+    h.n_out = out_pid.size();
+    h.n_patterns = m;
+    h.max_len = max_len;
+    h.min_len = min_len;
+    h.filter_gram = gram;
+    h.filter_log2_bits = log2_bits;
+    h.filter_exact = exact;
+    h.filter_mul = kFilterMul;
+    uint64_t o = align256(sizeof(ImageHeader));
+    h.off_node = o;      o = align256(o + 4 * (N + 1));
+    h.off_label = o;     o = align256(o + E + 16);
+    h.off_term_node = o; o = align256(o + 4 * T);
+    h.off_out_ptr = o;   o = align256(o + 4 * (T + 1));
+    h.off_out_pid = o;   o = align256(o + 4 * out_pid.size());
+    h.off_root = o;      o = align256(o + 4 * 256);
+    h.off_filter = o;    o = align256(o + 4 * filter.size());
+    h.image_bytes = o;
+    h.bytes_uncompressed = 36 * N;
+    h.bytes_dense_stt = 1024 * N;                      // 256 x u32 per state
+    h.bytes_paper_crs = 4 * (2 * paper_nnz + N + 1);   // PAPER.md:101, N x 9 words
+    h.bytes_csr_core = 4 * (N + 1) + E;
+
+    try {
+        image.assign(o, 0);
+    } catch (...) {
+        err = "pfac_build: out of host memory for the image";
+        return kStatusNomem;
+    }
+    uint8_t *p = image.data();
+    std::memcpy(p, &h, sizeof h);
+    std::memcpy(p + h.off_node, node_word.data(), 4 * (N + 1));
+    if (E) std::memcpy(p + h.off_label, label.data(), E);
+    if (T) std::memcpy(p + h.off_term_node, term_node.data(), 4 * T);
+    std::memcpy(p + h.off_out_ptr, out_ptr.data(), 4 * (T + 1));
+    if (!out_pid.empty()) std::memcpy(p + h.off_out_pid, out_pid.data(), 4 * out_pid.size());
+    std::memcpy(p + h.off_root, root.data(), 4 * 256);
+    std::memcpy(p + h.off_filter, filter.data(), 4 * filter.size());
+    return kStatusOk;
+}
+
+int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
+    if (!p || size < sizeof(ImageHeader)) {
+        err = "pfac_attach: image too small";
+        return kStatusInvalid;
+    }
+    ImageHeader h;
+    std::memcpy(&h, p, sizeof h);
+    if (std::memcmp(h.magic, "PFACIMG1", 8) != 0 || h.version != kVersion ||
+        h.header_bytes != sizeof(ImageHeader) || h.image_bytes != size) {
+        err = "pfac_attach: bad magic/version/size";
+        return kStatusInvalid;
+    }
+    const uint64_t N = h.n_nodes, E = h.n_edges, T = h.n_terminals;
+    auto in = [&](uint64_t off, uint64_t bytes) { return off >= sizeof(ImageHeader) && off + bytes <= size; };
+    bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
+              in(h.off_term_node, 4 * T) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
+              in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
+              in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && h.filter_gram <= 4 &&
+              h.filter_gram <= h.min_len && h.min_len <= h.max_len && h.max_len <= kMaxPatternLen &&
+              h.filter_mul == kFilterMul;
+    if (ok) {
+        const uint32_t *node = reinterpret_cast<const uint32_t *>(p + h.off_node);
+        const uint32_t *out_ptr = reinterpret_cast<const uint32_t *>(p + h.off_out_ptr);
+        ok = (node[0] & kEdgeMask) == 0 && (node[N] & kEdgeMask) == E && out_ptr[0] == 0 && out_ptr[T] == h.n_out;
+        for (uint64_t v = 0; ok && v < N; v++) ok = (node[v] & kEdgeMask) <= (node[v + 1] & kEdgeMask);
+    }
+    if (!ok) {
+        err = "pfac_attach: inconsistent image sections";
+        return kStatusInvalid;
+    }
+    return kStatusOk;
+}
+
+}  // namespace pfac

@@ -1,0 +1,62 @@
+// image.h -- layout of the PFAC device image (internal to the product library).
+//
+// One contiguous blob, built on the host by builder.cpp, copied verbatim to
+// every device (and broadcast between GPUs by the multi-GPU driver).  All
+// sections are 256-byte aligned offsets from the image start.
+//
+//   node   u32[N+1]   CSR row pointer of the breadth-first row-major trie
+//                     (PAPER.md:80 steps I-II; CRS row_ptr):
+//                     bits 0..30 = index of the node's first outgoing edge,
+//                     bit 31 = "a pattern ends at this node".  Children of a
+//                     node are consecutive and in ascending byte order, so the
+//                     child reached through edge e is node e+1 (implicit
+//                     col_ind: the BFS numbering makes it redundant).
+//   label  u8[E]      edge labels (CRS val, one byte per edge).
+//   term_node u32[T]  ascending ids of terminal nodes.
+//   out_ptr u32[T+1]  offsets into out_pid.
+//   out_pid u32[..]   per terminal t, the ascending union of the pattern ids
+//                     ending on the root->t path.  A walk passes every ancestor
+//                     of the deepest node it reaches, so the matches of one
+//                     start position are exactly this list for the deepest
+//                     terminal passed (prefix closure).
+//   root   u32[256]   child of the root per byte (0 = none): level 1 direct.
+//   filter u32[2^F/32] first-stage filter: bit h(x) set for the first d bytes
+//                     x of every pattern (d = min(4, shortest pattern)).  A
+//                     start whose d-gram bit is clear cannot match.
+#pragma once
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define PFAC_HD __host__ __device__
+#else
+#define PFAC_HD
+#endif
+
+namespace pfac {
+
+constexpr uint32_t kVersion = 1;
+constexpr uint32_t kTermBit = 0x80000000u;
+constexpr uint32_t kEdgeMask = 0x7FFFFFFFu;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kFilterMul = 0x9E3779B1u;  // Fibonacci hashing multiplier (odd)
+
+struct ImageHeader {
+    char magic[8];  // "PFACIMG1"
+    uint32_t version;
+    uint32_t header_bytes;
+    uint64_t image_bytes;
+    uint64_t n_nodes, n_edges, n_terminals, n_out;
+    uint32_t n_patterns, max_len, min_len, filter_gram;
+    uint32_t filter_log2_bits, filter_exact, filter_mul, reserved0;
+    uint64_t off_node, off_label, off_term_node, off_out_ptr, off_out_pid, off_root, off_filter;
+    uint64_t bytes_uncompressed, bytes_dense_stt, bytes_paper_crs, bytes_csr_core;
+    uint8_t pad[256 - 8 - 8 - 8 - 32 - 16 - 16 - 56 - 32];
+};
+static_assert(sizeof(ImageHeader) == 256, "header must be 256 bytes");
+
+// Filter index of a little-endian packed d-gram key (d bytes, zero-extended).
+PFAC_HD inline uint32_t filter_index(uint32_t key, uint32_t log2_bits, uint32_t exact) {
+    return exact ? key : (key * kFilterMul) >> (32u - log2_bits);
+}
+
+}  // namespace pfac

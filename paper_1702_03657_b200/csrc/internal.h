@@ -1,0 +1,58 @@
+// internal.h -- declarations shared by the product's translation units
+// (builder.cpp, abi.cpp, scan.cu).  Not part of the public ABI (include/pfac.h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "image.h"
+
+struct CUstream_st;
+
+namespace pfac {
+
+// mirrors pfac_status in include/pfac.h
+enum : int {
+    kStatusOk = 0,
+    kStatusInvalid = 1,
+    kStatusLimit = 2,
+    kStatusNomem = 3,
+    kStatusCuda = 4,
+    kStatusCapacity = 5,
+};
+
+constexpr uint32_t kMaxPatternLen = 65535;
+
+int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, std::vector<uint8_t> &image,
+                std::string &err);
+int validate_image(const uint8_t *p, uint64_t size, std::string &err);
+
+// Device-side view of an uploaded image (pointers into device memory).
+struct DevTrie {
+    const uint32_t *node;
+    const uint8_t *label;
+    const uint32_t *term_node;
+    const uint32_t *out_ptr;
+    const uint32_t *out_pid;
+    const uint32_t *root;
+    const uint32_t *filter;
+    uint32_t n_terminals;
+    uint32_t max_len;
+    uint32_t gram;
+    uint32_t log2_bits;
+    uint32_t exact;
+};
+
+DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d_image);
+
+// Workspace (device, caller-owned, zero-filled before first use).
+uint64_t workspace_bytes_for(uint64_t n_starts);
+
+// Launches the scan; returns kStatusOk or kStatusCuda (err filled).
+int launch_scan(const DevTrie &t, int device, const uint8_t *d_text, uint64_t readable_len, uint64_t n_starts,
+                uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity, uint64_t *d_count,
+                void *d_ws, uint64_t ws_bytes, CUstream_st *stream, std::string &err);
+
+uint32_t launches_per_call();
+
+}  // namespace pfac

@@ -1,0 +1,159 @@
+"""C-ABI boundary and host logic, no GPU: the library loads and exports every
+symbol include/pfac.h declares; the host builder's trie and byte accounting
+agree with the oracle; the exported image, interpreted on the CPU
+(tests/image_walker.py), reaches the oracle's result; error codes."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_1702_03657_b200 as pf
+from tests import image_walker
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "pfac.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pfac_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 15
+    lib = C.CDLL(pf.lib_path)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert pf._lib().pfac_version().decode().endswith("sm_100a")
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {pf.lib_path} 2>&1").read()
+    assert "sm_100a" in out, out
+
+
+def test_build_errors():
+    with pytest.raises(pf.PfacError) as e:
+        pf.Trie([])
+    assert e.value.status == 1
+    with pytest.raises(pf.PfacError) as e:
+        pf.Trie([b"ok", b""])
+    assert e.value.status == 1
+    with pytest.raises(pf.PfacError) as e:
+        pf.Trie([b"x" * 65536])
+    assert e.value.status == 1
+    pf.Trie([b"x" * 65535])  # library limit is inclusive
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 5])
+def test_stats_and_bytes_match_oracle(cid):
+    ps = gen.patterns(cid)
+    t = pf.Trie(ps)
+    o = oracle.Trie(ps)
+    st, ost = t.stats(), o.stats()
+    for k in ["nodes", "edges", "terminals", "n_patterns", "max_len", "min_len"]:
+        assert st[k] == ost[k], k
+    assert t.nbytes("uncompressed") == o.bytes("uncompressed") == 36 * st["nodes"]
+    assert t.nbytes("dense_stt") == o.bytes("dense_stt")
+    assert t.nbytes("paper_crs") == o.bytes("paper_crs")
+    assert t.nbytes("csr_core") == 4 * (st["nodes"] + 1) + st["edges"]
+    assert t.nbytes("device_image") < t.nbytes("uncompressed") or cid == 1
+    assert t.nbytes("device_image") == len(t.image())
+
+
+def test_image_interpreter_toy(golden):
+    ex = golden("examples.json")["matches"]
+    for e in ex:
+        t = pf.Trie([p.encode() for p in e["patterns"]])
+        h = image_walker.parse(t.image())
+        assert image_walker.match(h, e["text"].encode()) == [tuple(r) for r in e["expect"]], e["cite"]
+
+
+def test_image_layout_toy(golden):
+    g = golden("toy_trie.json")
+    h = image_walker.parse(pf.Trie([p.encode() for p in g["patterns"]]).image())
+    row_ptr = [int(x) & image_walker.MASK for x in h["node"]]
+    assert row_ptr == g["csr_row_ptr"]
+    assert bytes(h["label"]) == g["csr_labels"].encode()
+    terms = [v for v in range(g["nodes"]) if h["node"][v] & image_walker.TERM]
+    assert terms == sorted(int(k) for k in g["terminals"])
+    assert list(h["term_node"]) == terms
+    assert h["filter_gram"] == 2 and h["filter_exact"] == 1
+
+
+def test_image_interpreter_random_vs_oracle():
+    rng = np.random.default_rng(11)
+    for trial in range(150):
+        sigma = int(rng.choice([2, 4, 256]))
+        alpha = rng.choice(256, size=sigma, replace=False)
+        m = int(rng.integers(1, 30))
+        pats = [bytes(alpha[rng.integers(0, sigma, int(rng.integers(1, 9)))].astype(np.uint8)) for _ in range(m)]
+        if trial % 3 == 0:
+            pats.append(pats[0])
+        n = int(rng.integers(0, 600))
+        text = bytes(alpha[rng.integers(0, sigma, n)].astype(np.uint8))
+        h = image_walker.parse(pf.Trie(pats).image())
+        L = int(rng.integers(0, n + 1))
+        ns = int(rng.integers(0, L + 1))
+        want = oracle.Trie(pats).match_list(text, readable_len=L, lo=0, hi=ns)
+        assert image_walker.match(h, text, readable=L, n_starts=ns) == want, trial
+
+
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_image_interpreter_configs(cid):
+    ps = gen.patterns(cid)
+    t = pf.Trie(ps)
+    h = image_walker.parse(t.image())
+    text = gen.text(cid, 0, 40000).tobytes()
+    want = oracle.Trie(ps).match_list(text)
+    assert image_walker.match(h, text) == want
+
+
+def test_filter_is_complete():
+    """Every pattern's d-gram bit is set (a clear bit must imply no match)."""
+    for cid in [2, 3, 4, 5]:
+        ps = gen.patterns(cid)
+        h = image_walker.parse(pf.Trie(ps).image())
+        d = h["filter_gram"]
+        for k in range(len(ps)):
+            b = image_walker.filter_index(h, int.from_bytes(ps[k][:d], "little"))
+            assert (int(h["filter"][b >> 5]) >> (b & 31)) & 1
+
+
+def test_attach_roundtrip_and_validation():
+    t = pf.Trie(gen.patterns(2))
+    img = t.image()
+    t2 = pf.Trie.attach(img, device=-1)  # host only, no device upload
+    assert t2.image() == img and t2.stats() == t.stats()
+    bad = bytearray(img)
+    bad[0] ^= 0xFF
+    with pytest.raises(pf.PfacError):
+        pf.Trie.attach(bytes(bad), device=-1)
+    bad = bytearray(img)
+    bad[256 + 4 * 3] = 0xFF  # corrupt row_ptr monotonicity
+    with pytest.raises(pf.PfacError):
+        pf.Trie.attach(bytes(bad), device=-1)
+    with pytest.raises(pf.PfacError):
+        pf.Trie.attach(img[:-256], device=-1)
+
+
+def test_workspace_bytes_monotone():
+    t = pf.Trie([b"abc"])
+    a, b = t.workspace_bytes(1), t.workspace_bytes(1 << 30)
+    assert 256 < a < b
+
+
+def test_no_cpu_fallback():
+    """Without a usable device the product path fails loudly."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    t = pf.Trie([b"he", b"she"])
+    with pytest.raises(pf.PfacError) as e:
+        t.match_host(b"ushers")
+    assert e.value.status == 4

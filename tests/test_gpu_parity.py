@@ -1,0 +1,237 @@
+"""GPU parity: the sm_100a scan (through the C ABI) against the CPU oracle,
+element by element (bit-exact: this path is integer/byte/index work).
+
+Small cases compare full outputs; full BASELINE.json sizes (C2..C5, in the
+launch configuration bench.py times) compare every row's soundness, exact
+rows on oracle-computed sample windows, completeness on planted occurrences,
+and global (pos, pid) order."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_1702_03657_b200 as pf
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def gpu_rows(trie, text_np, readable=None, n_starts=None, pos_base=0, offset=0):
+    """Scan via the C ABI; `offset` shifts the text start inside the buffer
+    to exercise unaligned device pointers."""
+    buf = torch.zeros(len(text_np) + offset + 16, dtype=torch.uint8)
+    buf[offset:offset + len(text_np)] = torch.from_numpy(np.asarray(text_np, np.uint8))
+    d = buf.to(DEV)[offset:offset + len(text_np)]
+    pos, pid = trie.match(d, readable_len=readable, n_starts=n_starts, pos_base=pos_base)
+    return pos.cpu().numpy().astype(np.uint64), pid.cpu().numpy().astype(np.uint32)
+
+
+def assert_same(a, b, what=""):
+    (p1, q1), (p2, q2) = a, b
+    if len(p1) != len(p2) or not np.array_equal(p1, p2) or not np.array_equal(q1, q2):
+        n = min(len(p1), len(p2))
+        diff = np.nonzero((p1[:n] != p2[:n]) | (q1[:n] != q2[:n]))[0]
+        first = int(diff[0]) if len(diff) else n
+        raise AssertionError(f"{what}: counts {len(p1)} vs {len(p2)}, first difference at row {first}")
+
+
+def test_worked_examples(golden):
+    for ex in golden("examples.json")["matches"]:
+        t = pf.Trie([p.encode() for p in ex["patterns"]])
+        text = np.frombuffer(ex["text"].encode(), np.uint8)
+        if len(text) == 0:
+            continue
+        p, q = gpu_rows(t, text)
+        assert list(zip(p.tolist(), q.tolist())) == [tuple(r) for r in ex["expect"]], ex["cite"]
+
+
+def test_host_api_pfac_match(golden):
+    t = pf.Trie([b"he", b"she", b"his", b"hers"])
+    p, q = t.match_host(b"ushers")
+    assert list(zip(p.tolist(), q.tolist())) == [(1, 1), (2, 0), (2, 3)]
+    p, q = t.match_host(b"")
+    assert len(p) == 0
+
+
+def test_random_tiny_cases():
+    rng = np.random.default_rng(2024)
+    for trial in range(300):
+        sigma = int(rng.choice([2, 4, 256]))
+        alpha = rng.choice(256, size=sigma, replace=False)
+        m = int(rng.integers(1, 51))
+        pats = [bytes(alpha[rng.integers(0, sigma, int(rng.integers(1, 13)))].astype(np.uint8)) for _ in range(m)]
+        if trial % 4 == 0:
+            pats += [pats[0], pats[-1][:1]]
+        n = int(rng.choice([1, 3, 100, 4095, 4096, 4097, 9000, 70000]))
+        text = alpha[rng.integers(0, sigma, n)].astype(np.uint8)
+        for _ in range(min(20, n // 8)):
+            p = pats[int(rng.integers(len(pats)))]
+            if len(p) <= n:
+                o = int(rng.integers(0, n - len(p) + 1))
+                text[o:o + len(p)] = np.frombuffer(p, np.uint8)
+        want = oracle.Trie(pats).match(text)
+        got = gpu_rows(pf.Trie(pats), text, offset=int(rng.integers(0, 16)))
+        assert_same(got, want, f"trial {trial} sigma {sigma} n {n}")
+
+
+def test_halo_and_pos_base():
+    rng = np.random.default_rng(5)
+    pats = [b"ab", b"abab", b"b", b"bab", b"aaa", b"ba" * 20]
+    text = rng.choice(np.frombuffer(b"ab", np.uint8), size=50000).astype(np.uint8)
+    o = oracle.Trie(pats)
+    t = pf.Trie(pats)
+    for _ in range(20):
+        L = int(rng.integers(1, 50001))
+        ns = int(rng.integers(0, L + 1))
+        base = int(rng.integers(0, 1 << 40))
+        wp, wq = o.match(text, readable_len=L, lo=0, hi=ns)
+        gp, gq = gpu_rows(t, text, readable=L, n_starts=ns, pos_base=base)
+        assert_same((gp, gq), (wp + np.uint64(base), wq), f"L={L} ns={ns}")
+
+
+def test_sharded_equals_unsharded():
+    """Shards with a (max_len-1) halo, concatenated in order == one scan."""
+    ps = gen.patterns(2)
+    t = pf.Trie(ps)
+    text = gen.text(2, 0, 8 << 20)
+    full = gpu_rows(t, text)
+    halo = t.stats()["max_len"] - 1
+    rng = np.random.default_rng(9)
+    for G in [2, 3, 8]:
+        cuts = np.sort(rng.choice(np.arange(1, len(text)), size=G - 1, replace=False))
+        bounds = [0] + cuts.tolist() + [len(text)]
+        P, Q = [], []
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            e = min(len(text), b + halo)
+            p, q = gpu_rows(t, text[a:e], n_starts=b - a, pos_base=a)
+            P.append(p)
+            Q.append(q)
+        assert_same((np.concatenate(P), np.concatenate(Q)), full, f"G={G}")
+
+
+def test_capacity_overflow_and_count():
+    ps = [b"a", b"aa", b"aaa"]
+    t = pf.Trie(ps)
+    text = torch.full((10000,), ord("a"), dtype=torch.uint8, device=DEV)
+    sc = pf.Scanner(t, DEV, capacity=100)
+    sc.launch(text)
+    torch.cuda.synchronize()
+    n = int(sc.count.item())
+    assert n == 10000 + 9999 + 9998
+    want_p, want_q = oracle.Trie(ps).match(text.cpu().numpy())
+    assert np.array_equal(sc.pos[:100].cpu().numpy().astype(np.uint64), want_p[:100])
+    assert np.array_equal(sc.pid[:100].cpu().numpy().astype(np.uint32), want_q[:100])
+
+
+@pytest.mark.parametrize("kind", ["nested", "zero_bytes", "long", "len1", "len2", "dups"])
+def test_adversarial(kind):
+    rng = np.random.default_rng(["nested", "zero_bytes", "long", "len1", "len2", "dups"].index(kind))
+    if kind == "nested":
+        pats = [b"a" * k for k in range(1, 200)]
+        text = np.full(20000, ord("a"), np.uint8)
+        text[rng.integers(0, 20000, 50)] = ord("b")
+    elif kind == "zero_bytes":
+        pats = [b"\x00", b"\x00\x00\x01", b"\x01\x00", bytes(7)]
+        text = rng.integers(0, 2, 30000).astype(np.uint8)
+    elif kind == "long":
+        pats = [bytes(rng.integers(0, 256, 5000).astype(np.uint8)), b"xyz"]
+        text = rng.integers(0, 256, 100000).astype(np.uint8)
+        text[777:5777] = np.frombuffer(pats[0], np.uint8)
+        text[-3:] = np.frombuffer(b"xyz", np.uint8)
+    elif kind == "len1":
+        pats = [bytes([c]) for c in range(0, 256, 3)] + [b"\x03\x06"]
+        text = rng.integers(0, 256, 50000).astype(np.uint8)
+    elif kind == "len2":
+        pats = [bytes(rng.integers(0, 256, 2).astype(np.uint8)) for _ in range(500)] + [b"ab", b"abc"]
+        text = rng.integers(0, 256, 200000).astype(np.uint8)
+    else:
+        pats = [b"needle", b"needle", b"need", b"needle", b"le"]
+        text = np.frombuffer(b"xxneedlexxneedneedle" * 1000, np.uint8).copy()
+    want = oracle.Trie(pats).match(text)
+    assert_same(gpu_rows(pf.Trie(pats), text, offset=3), want, kind)
+
+
+def test_attach_from_device_image():
+    ps = gen.patterns(2)
+    t = pf.Trie(ps)
+    img = torch.frombuffer(bytearray(t.image()), dtype=torch.uint8).to(DEV)
+    t2 = pf.Trie.attach(img, device=0)
+    text = gen.text(2, 0, 1 << 20)
+    assert_same(gpu_rows(t2, text), gpu_rows(t, text), "attach")
+
+
+def test_repeated_calls_reuse_workspace():
+    """The workspace is left ready for the next call (no per-call reset by the caller)."""
+    ps = gen.patterns(2)
+    t = pf.Trie(ps)
+    sc = pf.Scanner(t, DEV, capacity=1 << 16)
+    texts = [torch.from_numpy(gen.text(2, k << 20, (k + 1) * 300000)).to(DEV) for k in range(3)]
+    ref = [oracle.Trie(ps).match(x.cpu().numpy()) for x in texts]
+    for rep in range(3):
+        for x, (wp, wq) in zip(texts, ref):
+            sc.launch(x)
+            torch.cuda.synchronize()
+            n = int(sc.count.item())
+            assert_same((sc.pos[:n].cpu().numpy().astype(np.uint64), sc.pid[:n].cpu().numpy().astype(np.uint32)),
+                        (wp, wq), f"rep {rep}")
+
+
+# ---------------------------------------------------------------- full sizes
+def _full_size_check(cid, n_bytes, windows=6, win=1 << 20):
+    ps = gen.patterns(cid)
+    pats = ps.to_list()
+    t = pf.Trie(ps)
+    host = torch.empty(n_bytes, dtype=torch.uint8, pin_memory=True)
+    gen.text(cid, 0, n_bytes, out=host.numpy())
+    d = host.to(DEV, non_blocking=True)
+    pos, pid = t.match(d)
+    pos = pos.cpu().numpy().astype(np.uint64)
+    pid = pid.cpu().numpy().astype(np.uint32)
+    text = host.numpy()
+    # sorted by (pos, pid), strictly
+    if len(pos) > 1:
+        dp = np.diff(pos.astype(np.int64))
+        assert np.all((dp > 0) | ((dp == 0) & (np.diff(pid.astype(np.int64)) > 0)))
+    # soundness of every row (vectorised memcmp per pattern length)
+    lens = ps.lens[pid].astype(np.int64)
+    for L in np.unique(lens):
+        sel = np.nonzero(lens == L)[0]
+        starts = pos[sel].astype(np.int64)
+        win_b = text[starts[:, None] + np.arange(L)[None, :]]
+        offs = ps.offs[pid[sel]].astype(np.int64)
+        pat_b = ps.data[offs[:, None] + np.arange(L)[None, :]]
+        assert np.array_equal(win_b, pat_b), f"unsound rows at length {L}"
+    # exact equality with the oracle on sampled windows (starts in [a, a+win))
+    o = oracle.Trie(ps)
+    rng = np.random.default_rng(cid)
+    halo = int(ps.lens.max()) - 1
+    for a in [0, n_bytes - win] + rng.integers(0, n_bytes - win, windows).tolist():
+        a = int(a)
+        e = min(n_bytes, a + win + halo)
+        wp, wq = o.match(text[a:e], readable_len=e - a, lo=0, hi=win)
+        sel = (pos >= a) & (pos < a + win)
+        assert_same((pos[sel] - np.uint64(a), pid[sel]), (wp, wq), f"C{cid} window @{a}")
+    # completeness on plants
+    pp, pq = gen.plants(cid, 0, (n_bytes + gen.CHUNK - 1) // gen.CHUNK)
+    keep = pp + ps.lens[pq] <= n_bytes
+    key = pos * np.uint64(1 << 20) + pid
+    want = pp[keep] * np.uint64(1 << 20) + pq[keep]
+    assert np.isin(want, key).all(), "a planted occurrence is missing"
+    return len(pos)
+
+
+def test_full_c2_exact():
+    ps = gen.patterns(2)
+    n = gen.config(2)["text_len"]
+    text = gen.text(2, 0, n)
+    want = oracle.Trie(ps).match(text)
+    got = gpu_rows(pf.Trie(ps), text)
+    assert_same(got, want, "C2 full 64 MiB")
+
+
+@pytest.mark.parametrize("cid", [3, 4, 5])
+def test_full_size_sampled(cid):
+    n = {3: 1 << 30, 4: 4 << 30, 5: 2 << 30}[cid]  # C5: the 1-GPU 2 GiB slice
+    assert _full_size_check(cid, n) > 0
