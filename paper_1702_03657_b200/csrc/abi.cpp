@@ -17,11 +17,27 @@
 
 using namespace pfac;
 
+// Device buffers pfac_match (host API) keeps between calls, per device.
+struct HostCtx {
+    std::mutex mu;  // one pfac_match at a time per handle and device
+    cudaStream_t st = nullptr;
+    uint8_t *d_text = nullptr;
+    uint64_t text_cap = 0;
+    void *d_ws = nullptr;
+    uint64_t ws_cap = 0;
+    uint64_t *d_pos = nullptr;
+    uint32_t *d_pid = nullptr;
+    uint64_t out_cap = 0;
+    uint64_t *d_count = nullptr;
+    uint64_t *h_count = nullptr;  // pinned
+};
+
 struct pfac_trie {
     std::vector<uint8_t> image;
     ImageHeader hdr;
-    std::mutex mu;                  // guards dev (lazy per-device upload)
+    std::mutex mu;                  // guards dev / ctx (lazy per-device state)
     std::map<int, void *> dev;      // device ordinal -> device copy of the image
+    std::map<int, std::unique_ptr<HostCtx>> ctx;
 };
 
 namespace {
@@ -113,14 +129,23 @@ pfac_status pfac_build_concat(const uint8_t *data, const uint32_t *lengths, uint
 
 void pfac_free(pfac_trie *t) {
     if (!t) return;
+    int prev = -1;
+    bool have = cudaGetDevice(&prev) == cudaSuccess;
     for (auto &kv : t->dev) {
-        int prev = -1;
-        if (cudaGetDevice(&prev) == cudaSuccess) {
-            cudaSetDevice(kv.first);
-            cudaFree(kv.second);
-            cudaSetDevice(prev);
-        }
+        if (!have) break;
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second);
     }
+    for (auto &kv : t->ctx) {
+        if (!have) break;
+        HostCtx &c = *kv.second;
+        cudaSetDevice(kv.first);
+        if (c.st) cudaStreamSynchronize(c.st);
+        cudaFree(c.d_text); cudaFree(c.d_ws); cudaFree(c.d_pos); cudaFree(c.d_pid); cudaFree(c.d_count);
+        cudaFreeHost(c.h_count);
+        if (c.st) cudaStreamDestroy(c.st);
+    }
+    if (have) cudaSetDevice(prev);
     delete t;
 }
 
@@ -194,7 +219,12 @@ pfac_status pfac_attach(const void *image, uint64_t size, int device, pfac_trie 
 
 pfac_status pfac_workspace_bytes(const pfac_trie *t, uint64_t n_starts, uint64_t *out) {
     if (!t || !out) return fail(kStatusInvalid, "pfac_workspace_bytes: NULL argument");
-    *out = workspace_bytes_for(n_starts);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail("pfac_workspace_bytes: no CUDA device", e);
+    std::string err;
+    int st = workspace_bytes_for(n_starts, dev, out, err);
+    if (st != kStatusOk) return fail(st, err);
     return PFAC_OK;
 }
 
@@ -210,7 +240,8 @@ pfac_status pfac_match_device(const pfac_trie *t, int device, const uint8_t *d_t
     if (s != PFAC_OK) return s;
     DevTrie dt = make_dev_trie(t->hdr, d_img);
     std::string err;
-    int st = launch_scan(dt, device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
+    const uint32_t *host_node = reinterpret_cast<const uint32_t *>(t->image.data() + t->hdr.off_node);
+    int st = launch_scan(dt, host_node, device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
                          d_workspace, workspace_bytes, reinterpret_cast<CUstream_st *>(stream), err);
     if (st != kStatusOk) return fail(st, err);
     return PFAC_OK;
@@ -224,74 +255,91 @@ pfac_status pfac_match(const pfac_trie *t, const uint8_t *text, uint64_t len, pf
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail("pfac_match: no CUDA device", e);
-    if (len == 0) {
-        const uint8_t *d_img = nullptr;
-        return device_image(t, dev, &d_img);  // still requires a working device
+    const uint8_t *d_img = nullptr;
+    pfac_status rs = device_image(t, dev, &d_img);
+    if (rs != PFAC_OK || len == 0) return rs;
+    HostCtx *cp;
+    {
+        pfac_trie *tm = const_cast<pfac_trie *>(t);
+        std::lock_guard<std::mutex> lk(tm->mu);
+        auto &slot = tm->ctx[dev];
+        if (!slot) slot.reset(new (std::nothrow) HostCtx());
+        if (!slot) return fail(kStatusNomem, "pfac_match: out of host memory");
+        cp = slot.get();
     }
-    uint64_t ws_bytes = workspace_bytes_for(len);
-    uint64_t cap = len / 256 + 4096;
-    uint8_t *d_text = nullptr;
-    void *d_ws = nullptr;
-    uint64_t *d_pos = nullptr, *d_count = nullptr;
-    uint32_t *d_pid = nullptr;
-    cudaStream_t st = nullptr;
-    pfac_status rs = PFAC_OK;
-    uint64_t count = 0;
-    auto cleanup = [&]() {
-        cudaFree(d_text); cudaFree(d_ws); cudaFree(d_pos); cudaFree(d_pid); cudaFree(d_count);
-        if (st) cudaStreamDestroy(st);
+    HostCtx &c = *cp;
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.st) {
+        if ((e = cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaMalloc(&c.d_count, 8)) != cudaSuccess || (e = cudaMallocHost(&c.h_count, 8)) != cudaSuccess)
+            return cuda_fail("pfac_match: stream/allocation", e);
+    }
+    // grow-only device buffers
+    if (len > c.text_cap) {
+        cudaFree(c.d_text);
+        c.d_text = nullptr;
+        c.text_cap = 0;
+        if ((e = cudaMalloc(&c.d_text, len)) != cudaSuccess) return cuda_fail("pfac_match: text buffer", e);
+        c.text_cap = len;
+    }
+    uint64_t ws_bytes = 0;
+    {
+        std::string err;
+        int st = workspace_bytes_for(len, dev, &ws_bytes, err);
+        if (st != kStatusOk) return fail(st, err);
+    }
+    if (ws_bytes > c.ws_cap) {
+        cudaFree(c.d_ws);
+        c.d_ws = nullptr;
+        c.ws_cap = 0;
+        if ((e = cudaMalloc(&c.d_ws, ws_bytes)) != cudaSuccess ||
+            (e = cudaMemsetAsync(c.d_ws, 0, ws_bytes, c.st)) != cudaSuccess)
+            return cuda_fail("pfac_match: workspace", e);
+        c.ws_cap = ws_bytes;
+    }
+    auto ensure_out = [&](uint64_t cap) -> cudaError_t {
+        if (cap <= c.out_cap) return cudaSuccess;
+        cudaFree(c.d_pos);
+        cudaFree(c.d_pid);
+        c.d_pos = nullptr;
+        c.d_pid = nullptr;
+        c.out_cap = 0;
+        cudaError_t r = cudaMalloc(&c.d_pos, cap * 8);
+        if (r == cudaSuccess) r = cudaMalloc(&c.d_pid, cap * 4);
+        if (r == cudaSuccess) c.out_cap = cap;
+        return r;
     };
-    if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaMalloc(&d_text, len)) != cudaSuccess || (e = cudaMalloc(&d_ws, ws_bytes)) != cudaSuccess ||
-        (e = cudaMalloc(&d_count, 8)) != cudaSuccess || (e = cudaMalloc(&d_pos, cap * 8)) != cudaSuccess ||
-        (e = cudaMalloc(&d_pid, cap * 4)) != cudaSuccess) {
-        cleanup();
-        return cuda_fail("pfac_match: device allocation", e);
-    }
-    if ((e = cudaMemcpyAsync(d_text, text, len, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-        (e = cudaMemsetAsync(d_ws, 0, ws_bytes, st)) != cudaSuccess) {
-        cleanup();
+    if ((e = ensure_out(len / 256 + 4096)) != cudaSuccess) return cuda_fail("pfac_match: output buffers", e);
+    if ((e = cudaMemcpyAsync(c.d_text, text, len, cudaMemcpyHostToDevice, c.st)) != cudaSuccess)
         return cuda_fail("pfac_match: H2D", e);
-    }
+    uint64_t count = 0;
     for (int attempt = 0; attempt < 2; attempt++) {
-        rs = pfac_match_device(t, dev, d_text, len, len, 0, d_pos, d_pid, cap, d_count, d_ws, ws_bytes,
-                               reinterpret_cast<pfac_stream>(st));
-        if (rs != PFAC_OK) break;
-        if ((e = cudaMemcpyAsync(&count, d_count, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-            (e = cudaStreamSynchronize(st)) != cudaSuccess) {
-            rs = cuda_fail("pfac_match: scan", e);
-            break;
-        }
-        if (count <= cap) break;
-        // count-and-retry with exact capacity
-        cudaFree(d_pos); cudaFree(d_pid);
-        d_pos = nullptr; d_pid = nullptr;
-        cap = count;
-        if ((e = cudaMalloc(&d_pos, cap * 8)) != cudaSuccess || (e = cudaMalloc(&d_pid, cap * 4)) != cudaSuccess) {
-            rs = cuda_fail("pfac_match: device allocation", e);
-            break;
-        }
-        if (attempt == 1) rs = fail(kStatusCapacity, "pfac_match: capacity retry failed");
+        rs = pfac_match_device(t, dev, c.d_text, len, len, 0, c.d_pos, c.d_pid, c.out_cap, c.d_count, c.d_ws,
+                               c.ws_cap, reinterpret_cast<pfac_stream>(c.st));
+        if (rs != PFAC_OK) return rs;
+        if ((e = cudaMemcpyAsync(c.h_count, c.d_count, 8, cudaMemcpyDeviceToHost, c.st)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(c.st)) != cudaSuccess)
+            return cuda_fail("pfac_match: scan", e);
+        count = *c.h_count;
+        if (count <= c.out_cap) break;
+        if (attempt == 1) return fail(kStatusCapacity, "pfac_match: capacity retry failed");
+        if ((e = ensure_out(count)) != cudaSuccess) return cuda_fail("pfac_match: output buffers", e);
     }
-    if (rs == PFAC_OK && count > 0) {
-        out->pos = static_cast<uint64_t *>(std::malloc(count * 8));
-        out->pid = static_cast<uint32_t *>(std::malloc(count * 4));
-        if (!out->pos || !out->pid) {
-            std::free(out->pos); std::free(out->pid);
-            out->pos = nullptr; out->pid = nullptr;
-            rs = fail(kStatusNomem, "pfac_match: out of host memory");
-        } else if ((e = cudaMemcpyAsync(out->pos, d_pos, count * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-                   (e = cudaMemcpyAsync(out->pid, d_pid, count * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-                   (e = cudaStreamSynchronize(st)) != cudaSuccess) {
-            std::free(out->pos); std::free(out->pid);
-            out->pos = nullptr; out->pid = nullptr;
-            rs = cuda_fail("pfac_match: D2H", e);
-        } else {
-            out->count = count;
-        }
+    if (count == 0) return PFAC_OK;
+    out->pos = static_cast<uint64_t *>(std::malloc(count * 8));
+    out->pid = static_cast<uint32_t *>(std::malloc(count * 4));
+    if (!out->pos || !out->pid) {
+        pfac_matches_free(out);
+        return fail(kStatusNomem, "pfac_match: out of host memory");
     }
-    cleanup();
-    return rs;
+    if ((e = cudaMemcpyAsync(out->pos, c.d_pos, count * 8, cudaMemcpyDeviceToHost, c.st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(out->pid, c.d_pid, count * 4, cudaMemcpyDeviceToHost, c.st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(c.st)) != cudaSuccess) {
+        pfac_matches_free(out);
+        return cuda_fail("pfac_match: D2H", e);
+    }
+    out->count = count;
+    return PFAC_OK;
 }
 
 void pfac_matches_free(pfac_matches *m) {

@@ -142,10 +142,17 @@ def test_attach_roundtrip_and_validation():
         pf.Trie.attach(img[:-256], device=-1)
 
 
-def test_workspace_bytes_monotone():
+def test_workspace_bytes_needs_device():
+    """Workspace size depends on the device's SM count (launch geometry)."""
+    import torch
     t = pf.Trie([b"abc"])
-    a, b = t.workspace_bytes(1), t.workspace_bytes(1 << 30)
-    assert 256 < a < b
+    if torch.cuda.is_available():
+        a, b = t.workspace_bytes(1), t.workspace_bytes(1 << 30)
+        assert 256 < a < b
+    else:
+        with pytest.raises(pf.PfacError) as e:
+            t.workspace_bytes(1)
+        assert e.value.status == 4
 
 
 def test_no_cpu_fallback():
