@@ -143,8 +143,9 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     if (exact) {
         log2_bits = 8 * gram;
     } else {
-        // distinct d-grams -> ~32 filter bits per key (false-positive rate
-        // ~3%), between 2^10 and 2^19 bits (64 KiB, the shared-memory budget)
+        // distinct d-grams -> ~32 filter bits per key (kind 0: ~3% false
+        // positives; kind 1, two bits per key in 64-bit blocks: ~0.5%),
+        // between 2^10 and 2^19 bits (64 KiB, the shared-memory budget)
         std::vector<uint32_t> keys(m);
         for (uint32_t k = 0; k < m; k++) {
             uint32_t x = 0;
@@ -158,11 +159,18 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     }
     std::vector<uint32_t> filter((size_t)1 << (log2_bits - 5 > 0 ? log2_bits - 5 : 0), 0u);
     if (filter.empty()) filter.resize(1);
+    const uint32_t kind = gram == 4 ? 1u : 0u;
     for (uint32_t k = 0; k < m; k++) {
         uint32_t x = 0;
         for (uint32_t b = 0; b < gram; b++) x |= (uint32_t)pats[k][b] << (8 * b);
-        uint32_t h = filter_index(x, log2_bits, exact);
-        filter[h >> 5] |= 1u << (h & 31);
+        if (kind == 1) {
+            const uint32_t b = filter4_block(x, log2_bits);
+            filter[2 * b] |= 1u << filter4_bit_lo(x);
+            filter[2 * b + 1] |= 1u << filter4_bit_hi(x);
+        } else {
+            uint32_t h = filter_index(x, log2_bits, exact);
+            filter[h >> 5] |= 1u << (h & 31);
+        }
     }
 
     // ---- assemble the image
@@ -182,6 +190,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     h.filter_log2_bits = log2_bits;
     h.filter_exact = exact;
     h.filter_mul = kFilterMul;
+    h.filter_kind = kind;
     uint64_t o = align256(sizeof(ImageHeader));
     h.off_node = o;      o = align256(o + 4 * (N + 1));
     h.off_label = o;     o = align256(o + E + 16);
@@ -233,7 +242,8 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
               in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && h.filter_gram <= 4 &&
               h.filter_gram <= h.min_len && h.min_len <= h.max_len && h.max_len <= kMaxPatternLen &&
-              h.filter_mul == kFilterMul;
+              h.filter_mul == kFilterMul && h.filter_kind == (h.filter_gram == 4 ? 1u : 0u) &&
+              (h.filter_kind == 0 || h.filter_log2_bits >= 10);
     if (ok) {
         const uint32_t *node = reinterpret_cast<const uint32_t *>(p + h.off_node);
         const uint32_t *out_ptr = reinterpret_cast<const uint32_t *>(p + h.off_out_ptr);

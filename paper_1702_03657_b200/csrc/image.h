@@ -20,9 +20,18 @@
 //                     start position are exactly this list for the deepest
 //                     terminal passed (prefix closure).
 //   root   u32[256]   child of the root per byte (0 = none): level 1 direct.
-//   filter u32[2^F/32] first-stage filter: bit h(x) set for the first d bytes
-//                     x of every pattern (d = min(4, shortest pattern)).  A
-//                     start whose d-gram bit is clear cannot match.
+//   filter u32[2^F/32] first-stage filter over the first d bytes of every
+//                     pattern (d = min(4, shortest pattern)); a start whose bit
+//                     is clear cannot match.  Two kinds:
+//                       kind 0 (d < 4): bit index filter_index(x) of the d-gram
+//                         x (little-endian), standard bit order;
+//                       kind 1 (d = 4): a blocked two-bit filter.  Block
+//                         (64 bits = words 2b, 2b+1) b = top (F-6) bits of
+//                         x * (kFilterMul << 8) (a hash of bytes 0..2); the
+//                         key sets bit 31-(byte3 & 31) of word 2b and bit
+//                         31-(byte2 & 31) of word 2b+1 (bit-reversed so the
+//                         kernel tests each with one rotate; scan.cu stage 1).
+//                         A start passes iff both bits are set.
 #pragma once
 #include <cstdint>
 
@@ -34,7 +43,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kEdgeMask = 0x7FFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
@@ -47,16 +56,23 @@ struct ImageHeader {
     uint64_t image_bytes;
     uint64_t n_nodes, n_edges, n_terminals, n_out;
     uint32_t n_patterns, max_len, min_len, filter_gram;
-    uint32_t filter_log2_bits, filter_exact, filter_mul, reserved0;
+    uint32_t filter_log2_bits, filter_exact, filter_mul, filter_kind;
     uint64_t off_node, off_label, off_term_node, off_out_ptr, off_out_pid, off_root, off_filter;
     uint64_t bytes_uncompressed, bytes_dense_stt, bytes_paper_crs, bytes_csr_core;
     uint8_t pad[256 - 8 - 8 - 8 - 32 - 16 - 16 - 56 - 32];
 };
 static_assert(sizeof(ImageHeader) == 256, "header must be 256 bytes");
 
-// Filter index of a little-endian packed d-gram key (d bytes, zero-extended).
+// Kind 0: filter bit index of a little-endian packed d-gram key (d < 4).
 PFAC_HD inline uint32_t filter_index(uint32_t key, uint32_t log2_bits, uint32_t exact) {
     return exact ? key : (key * kFilterMul) >> (32u - log2_bits);
 }
+// Kind 1 (d = 4): block index and the stored bit positions (word 2b, word
+// 2b+1) of the 4-gram x.
+PFAC_HD inline uint32_t filter4_block(uint32_t x, uint32_t log2_bits) {
+    return (x * (kFilterMul << 8)) >> (32u - (log2_bits - 6u));
+}
+PFAC_HD inline uint32_t filter4_bit_lo(uint32_t x) { return 31u - ((x >> 24) & 31u); }
+PFAC_HD inline uint32_t filter4_bit_hi(uint32_t x) { return 31u - ((x >> 16) & 31u); }
 
 }  // namespace pfac

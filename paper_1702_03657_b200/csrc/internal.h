@@ -41,6 +41,7 @@ struct DevTrie {
     uint32_t gram;
     uint32_t log2_bits;
     uint32_t exact;
+    uint32_t kind;       // filter kind (image.h)
     uint32_t n_nodes;
 };
 

@@ -9,21 +9,22 @@
 //
 // B200 mapping:
 //  * one persistent CTA per SM (kWarps warps).  Shared memory holds, once per
-//    SM, the first-stage d-gram filter (replicated per bank group so lanes
-//    rarely conflict), the level-1 table, and the top H nodes of the
-//    breadth-first CSR trie (BFS order = level order, so the first H nodes are
-//    the hot upper levels; PAPER.md:89 kept row_ptr on chip for the same
-//    reason).
-//  * phase 1 (scan): warp w owns a contiguous range of 512-start rounds.  A
-//    per-warp ring of kSlots 512-byte slots is filled by TMA bulk copies
+//    SM, the first-stage filter (replicated per bank group so lanes rarely
+//    conflict; at smem offset 0 so a byte offset is an address), the level-1
+//    table, the level-1 bitmapped nodes (Fig. 3), and the top H
+//    nodes of the breadth-first CSR trie (BFS order = level order, so the
+//    first H nodes are the hot upper levels; PAPER.md:89 kept row_ptr on chip
+//    for the same reason).
+//  * phase 1 (scan): warp w owns a contiguous range of 1024-start rounds.  A
+//    per-warp ring of kSlots 1 KiB slots is filled by TMA bulk copies
 //    (cp.async.bulk + mbarrier, evict-first in L2) kSlots-1 rounds ahead.
-//    Per round each lane tests its 16 consecutive starts against the d-gram
-//    filter (a clear bit means no pattern can start there: PFAC's early
-//    termination taken before the first trie access); survivors walk the trie
-//    to the first mismatch (shared memory for the top H nodes, L1/L2 below).
-//    A start that passed a terminal is appended, in position order, to the
-//    warp's hit list (its offset in the range; matches are rare, so phase 3
-//    walks these starts again instead of storing the terminal).
+//    Per round each lane tests its 32 consecutive starts against the filter
+//    (a clear bit means no pattern can start there: PFAC's early termination
+//    taken before the first trie access).  Survivors are compacted into a
+//    per-warp queue and walked with full warps to the first mismatch.  A
+//    start that passed a terminal is appended, in position order, to the
+//    warp's hit list (its offset; matches are rare, so phase 3 walks these
+//    starts again instead of storing the terminal).
 //  * phase 2 (offsets): per-warp match counts -> CTA scan -> one grid barrier
 //    -> exclusive prefix over CTA totals.  Ranges are contiguous and ordered,
 //    so the concatenation is globally sorted by (pos, pid).
@@ -41,13 +42,14 @@ namespace pfac {
 
 namespace {
 
-constexpr int kWarps = 32;
+constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
-constexpr int kPerLane = 16;           // consecutive starts per lane per round
-constexpr int kRound = 32 * kPerLane;  // 512 starts per warp round
+constexpr int kPerLane = 32;           // consecutive starts per lane per round
+constexpr int kRound = 32 * kPerLane;  // 1024 starts per warp round
 constexpr int kSlots = 4;              // text ring depth per warp
 constexpr int kSlotBytes = kRound;     // one round of text per slot
 constexpr int kMaxCtas = 1024;
+constexpr int kQueue = 64;             // per-warp survivor queue (u16 round offsets)
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
@@ -74,10 +76,11 @@ struct ScanArgs {
     uint32_t hit_cap;
     uint32_t parity;                // barrier counter used by this launch
     uint64_t rounds_per_warp;
-    // shared-memory layout (bytes from the dynamic smem base)
+    // shared-memory layout (bytes from the dynamic smem base; filter at 0)
     uint32_t filter_words;          // words of the (unreplicated) filter
-    uint32_t filter_rep;            // replication factor (power of two <= 32)
-    uint32_t off_filter, off_root, off_node, off_label, off_ring, off_bar, off_warp;
+    uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
+    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_queue;
+    uint32_t n_level1;              // B: the root's children are nodes [1, B]
     uint32_t hot_nodes;             // H: node words [0, H] resident
     uint32_t hot_edges;             // row_ptr[H]: labels [0, hot_edges) resident
     uint32_t aligned;               // text pointer is 16-byte aligned (bulk-copy path)
@@ -158,10 +161,11 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, int lane, uint32_
 
 // ------------------------------------------------------------ trie access
 struct Smem {
-    const uint32_t *filter;  // replicated, already offset by this lane's copy
-    const uint32_t *root;
-    const uint32_t *node;    // [0, H]
-    const uint8_t *label;    // [0, hot_edges)
+    uint32_t filter_base;    // smem byte address of the filter (0) | lane's copy
+    const uint32_t *root;    // level-1 table: child of the root per byte
+    const uint32_t *bm;      // level-1 bitmapped nodes, 10 words each (see below)
+    const uint32_t *node;    // node words [0, H]
+    const uint8_t *label;    // labels [0, hot_edges)
 };
 
 __device__ __forceinline__ uint32_t node_word(const ScanArgs &a, const Smem &s, uint32_t v) {
@@ -171,43 +175,69 @@ __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, u
     return e < a.hot_edges ? (uint32_t)s.label[e] : (uint32_t)__ldg(a.t.label + e);
 }
 
-// Text byte j: from the warp's ring when [lo, lo+len) covers it (slot0 then
-// slot1, contiguous in the stream), else from global memory.
-struct TextView {
-    const uint8_t *slot0;
-    const uint8_t *slot1;
-    uint64_t lo;
-    uint32_t len;
+// Text seen by a walk, addressed relative to a global position: from the
+// warp's ring when the offset lies in it, else from global memory.
+// `end` = readable bytes from that position (clamped to 32 bits).
+struct RingText {
+    const uint8_t *p0, *p1;  // current slot and the next slot of the stream
+    uint32_t span;           // contiguous ring bytes from p0 (1 or 2 slots)
+    uint32_t end;
+    const uint8_t *g;        // text + position of p0[0]
+    __device__ __forceinline__ uint32_t at(uint32_t r) const {
+        if (r < span) return r < (uint32_t)kSlotBytes ? p0[r] : p1[r - kSlotBytes];
+        return __ldg(g + r);
+    }
 };
-__device__ __forceinline__ uint32_t text_at(const ScanArgs &a, const TextView &tv, uint64_t j) {
-    const uint64_t r = j - tv.lo;
-    if (r < (uint64_t)tv.len) return r < (uint64_t)kSlotBytes ? tv.slot0[r] : tv.slot1[r - kSlotBytes];
-    return __ldg(a.text + j);
-}
+struct GlobalText {
+    const uint8_t *g;
+    uint32_t end;
+    __device__ __forceinline__ uint32_t at(uint32_t r) const { return __ldg(g + r); }
+};
 
-// Walk from start gi (whose first byte is c0) to the first mismatch; returns
-// the deepest terminal node passed, or kNone.
-__device__ uint32_t walk(const ScanArgs &a, const Smem &s, const TextView &tv, uint64_t gi, uint32_t c0) {
-    uint32_t v = s.root[c0];
+// Walk from the start at offset r0 to the first mismatch; returns the deepest
+// terminal node passed, or kNone.  Level 1 (the root's children, nodes
+// [1, B]) uses the paper's bitmapped node (Fig. 3: 256-bit child
+// bitmap + offset, child = offset + rank of c among the set bits); deeper
+// nodes use the CSR label list of the image.
+template <class Text>
+__device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0) {
+    uint32_t v = s.root[tx.at(r0)];
     if (v == 0) return kNone;
     uint32_t w = node_word(a, s, v);
     uint32_t last = (w & kTermBit) ? v : kNone;
-    for (uint64_t j = gi + 1; j < a.readable; ++j) {
+    uint32_t j = r0 + 1;
+    if (j >= tx.end) return last;
+    {   // level 1 -> 2 through the bitmap
+        const uint32_t c = tx.at(j);
+        const uint32_t *bm = s.bm + (v - 1) * 10;
+        const uint32_t word = bm[c >> 5];
+        if (!((word >> (c & 31)) & 1u)) return last;
+        const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
+        v = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
+        w = node_word(a, s, v);
+        if (w & kTermBit) last = v;
+        ++j;
+    }
+    for (; j < tx.end; ++j) {
         const uint32_t lo0 = w & kEdgeMask;
         const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
         if (lo0 == hi0) break;  // leaf
-        const uint32_t c = text_at(a, tv, j);
-        uint32_t lo = lo0, hi = hi0;  // labels[lo, hi) ascending
-        while (hi - lo > 4) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (label_at(a, s, mid) <= c) lo = mid; else hi = mid;
-        }
+        const uint32_t c = tx.at(j);
         uint32_t found = kNone;
-        for (uint32_t k = lo; k < hi; ++k) {
-            const uint32_t l = label_at(a, s, k);
-            if (l >= c) {
-                if (l == c) found = k;
-                break;
+        if (hi0 - lo0 == 1) {
+            if (label_at(a, s, lo0) == c) found = lo0;
+        } else {
+            uint32_t lo = lo0, hi = hi0;  // labels[lo, hi) ascending
+            while (hi - lo > 4) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (label_at(a, s, mid) <= c) lo = mid; else hi = mid;
+            }
+            for (uint32_t k = lo; k < hi; ++k) {
+                const uint32_t l = label_at(a, s, k);
+                if (l >= c) {
+                    if (l == c) found = k;
+                    break;
+                }
             }
         }
         if (found == kNone) break;  // mismatch: the thread terminates
@@ -218,6 +248,8 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const TextView &tv, u
     return last;
 }
 
+__device__ __forceinline__ uint32_t clamp32(uint64_t x) { return x > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)x; }
+
 __device__ __forceinline__ uint32_t term_index(const DevTrie &t, uint32_t v) {
     uint32_t lo = 0, hi = t.n_terminals;
     while (lo < hi) {
@@ -227,53 +259,129 @@ __device__ __forceinline__ uint32_t term_index(const DevTrie &t, uint32_t v) {
     return lo;
 }
 
-// Stage 1 over one lane's 16 starts: bit k set <=> start lbase+k may match.
-__device__ __forceinline__ uint32_t filter16(const ScanArgs &a, const Smem &s, const uint32_t wv[5], uint32_t kmask,
-                                             uint32_t nvalid) {
-    const uint32_t rep = a.filter_rep, log2_bits = a.t.log2_bits, exact = a.t.exact;
+// Stage 1 over one lane's 32 starts (text bytes wv[0..8] little-endian):
+// bit k set <=> start k may match.
+//  kind 1 (d = 4): word = hash of bytes k..k+2 (top bits of x*(M<<8)), bit =
+//    31 - (byte k+3 & 31): a rotate left by byte k+3 (the funnel shift takes
+//    its amount mod 32, so the 4-gram at k+3 serves as the amount) brings the
+//    tested bit to bit 31 and a funnel shift appends it to the mask.  Per
+//    start: IMAD (hash), SHF (word index), IMAD (address), LDS, 2x SHF.
+//  kind 0 (d < 4): generic d-gram bit index.
+__device__ __forceinline__ uint32_t lds_abs(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64_abs(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+template <int Kind>
+__device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[9], uint32_t sW, uint32_t stride,
+                                             uint32_t base_lane) {
     uint32_t surv = 0;
+    if (Kind == 1) {
+        constexpr uint32_t kMul = kFilterMul << 8;
+        uint32_t x[kPerLane + 3];
 #pragma unroll
-    for (int k = 0; k < kPerLane; ++k) {
-        const uint32_t x = __funnelshift_r(wv[k >> 2], wv[(k >> 2) + 1], 8 * (k & 3)) & kmask;
-        const uint32_t h = filter_index(x, log2_bits, exact);
-        const uint32_t word = s.filter[(h >> 5) * rep];
-        surv |= ((word >> (h & 31)) & 1u) << k;
+        for (int k = 0; k < kPerLane + 1; ++k)
+            x[k] = (k & 3) ? __funnelshift_r(wv[k >> 2], wv[(k >> 2) + 1], 8 * (k & 3)) : wv[k >> 2];
+        x[kPerLane + 1] = x[kPerLane - 1] >> 16;  // byte 33 in the low bits
+        x[kPerLane + 2] = x[kPerLane - 1] >> 24;  // byte 34
+#pragma unroll
+        for (int k = kPerLane - 1; k >= 0; --k) {
+            const uint32_t blk = (x[k] * kMul) >> sW;
+            const uint2 w2 = lds64_abs(blk * stride + base_lane);
+            // rotate by byte k+3 / byte k+2 (funnel amounts are mod 32): tested bits -> 31
+            const uint32_t r = __funnelshift_l(w2.x, w2.x, x[k + 3]) & __funnelshift_l(w2.y, w2.y, x[k + 2]);
+            surv = __funnelshift_l(r, surv, 1);  // surv << 1 | bit
+        }
+    } else {
+        const uint32_t gram = a.t.gram;
+        const uint32_t kmask = (1u << (8 * gram)) - 1u;
+#pragma unroll
+        for (int k = kPerLane - 1; k >= 0; --k) {
+            const uint32_t x = __funnelshift_r(wv[k >> 2], wv[(k >> 2) + 1], 8 * (k & 3)) & kmask;
+            const uint32_t h = filter_index(x, a.t.log2_bits, a.t.exact);
+            const uint32_t word = lds_abs((h >> 5) * stride + base_lane);
+            surv = (surv << 1) | ((word >> (h & 31)) & 1u);
+        }
     }
-    return surv & (nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u));
+    return surv;
 }
 
+template <int Kind>
 __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t *s_filter = reinterpret_cast<uint32_t *>(smem + a.off_filter);
+    uint32_t *s_filter = reinterpret_cast<uint32_t *>(smem);
     uint32_t *s_root = reinterpret_cast<uint32_t *>(smem + a.off_root);
     uint32_t *s_node = reinterpret_cast<uint32_t *>(smem + a.off_node);
     uint8_t *s_label = smem + a.off_label;
     uint8_t *ring = smem + a.off_ring + (uint32_t)warp * (kSlots * kSlotBytes);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.off_bar) + warp * kSlots;
     unsigned long long *s_wtot = reinterpret_cast<unsigned long long *>(smem + a.off_warp);  // [kWarps + 1]
+    uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
+    uint16_t *queue = reinterpret_cast<uint16_t *>(smem + a.off_queue) + warp * kQueue;
 
     // ---- one-time: clear the other barrier counter; stage tables in smem
     if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;
-    const uint32_t rep = a.filter_rep;
-    for (uint32_t i = tid; i < a.filter_words * rep; i += kThreads) s_filter[i] = __ldg(a.t.filter + i / rep);
+    const uint32_t rep = 1u << a.rep_log2;
+    if (Kind == 1) {  // interleave 8-byte blocks
+        for (uint32_t i = tid; i < (a.filter_words << a.rep_log2); i += kThreads)
+            s_filter[i] = __ldg(a.t.filter + (((i >> 1) >> a.rep_log2) << 1) + (i & 1));
+    } else {
+        for (uint32_t i = tid; i < (a.filter_words << a.rep_log2); i += kThreads)
+            s_filter[i] = __ldg(a.t.filter + (i >> a.rep_log2));
+    }
     for (uint32_t i = tid; i < 256; i += kThreads) s_root[i] = __ldg(a.t.root + i);
     for (uint32_t i = tid; i <= a.hot_nodes; i += kThreads) s_node[i] = __ldg(a.t.node + i);
     for (uint32_t i = tid; i < a.hot_edges; i += kThreads) s_label[i] = __ldg(a.t.label + i);
+    // level-1 bitmapped nodes: 8 bitmap words + 2 words of per-word prefix
+    // popcounts (bytes); built from the CSR labels of nodes [1, B]
+    for (uint32_t i = tid; i < a.n_level1 * 10; i += kThreads) s_bm[i] = 0u;
+    __syncthreads();
+    for (uint32_t v = 1 + warp; v <= a.n_level1; v += kWarps) {
+        const uint32_t e0 = __ldg(a.t.node + v) & kEdgeMask, e1 = __ldg(a.t.node + v + 1) & kEdgeMask;
+        uint32_t *o = s_bm + (v - 1) * 10;
+        for (uint32_t e = e0 + lane; e < e1; e += 32) {
+            const uint32_t c = __ldg(a.t.label + e);
+            atomicOr(&o[c >> 5], 1u << (c & 31));
+        }
+        __syncwarp();
+        if (lane == 0) {
+            uint32_t pre = 0, p0 = 0, p1 = 0;
+            for (int q = 0; q < 8; ++q) {
+                if (q < 4) p0 |= pre << (8 * q); else p1 |= pre << (8 * (q - 4));
+                pre += __popc(o[q]);
+            }
+            o[8] = p0;
+            o[9] = p1;
+        }
+    }
     if (lane < kSlots) mbar_init(&bars[lane], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
     Smem s;
-    s.filter = s_filter + (lane & (rep - 1));
+    s.filter_base = 0;
     s.root = s_root;
+    s.bm = s_bm;
     s.node = s_node;
     s.label = s_label;
+    // filter addressing: copies interleaved at the unit the kernel loads
+    // (kind 1: 8-byte block b of copy r at filter + 8*(b*rep + r); kind 0:
+    // word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
+    // so the lanes of a phase spread over the banks
+    const uint32_t unit = Kind == 1 ? 8u : 4u;
+    const uint32_t sW = 32u - (a.t.log2_bits - (Kind == 1 ? 6u : 5u));  // block index = hash >> sW
+    const uint32_t stride = rep * unit;
+    const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
 
-    const uint32_t gram = a.t.gram;
-    const uint32_t kmask = gram >= 4 ? 0xFFFFFFFFu : ((1u << (8 * gram)) - 1u);
     const uint64_t policy = evict_first_policy();
     // starts < lim are valid: inside [0, n_starts) and their d-gram fits
+    const uint32_t gram = a.t.gram;
     const uint64_t lim = (a.readable + 1 >= gram && a.readable + 1 - gram < a.n_starts) ? a.readable + 1 - gram
                                                                                         : a.n_starts;
     // ---- this warp's contiguous range of rounds
@@ -298,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             }
         } else {  // unaligned text or ragged tail: lanes copy, zero-fill past `readable`
             for (int k = 0; k < kPerLane; ++k) {
-                const uint32_t o = lane * kPerLane + k;
+                const uint32_t o = lane + 32 * k;
                 dst[o] = o < avail ? __ldg(a.text + lo + o) : (uint8_t)0;
             }
             __syncwarp();
@@ -309,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     // ================================================= phase 1: scan
     const uint64_t nr = r_end - r_begin;
     for (uint64_t i = 0; i < nr && i < kSlots - 1; ++i) issue(i);
-    uint64_t total = 0;   // pattern ids matched in this range (warp-uniform)
+    uint32_t c = 0;       // pattern ids matched by this lane's starts
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
     for (uint64_t i = 0; i < nr; ++i) {
         if (i + kSlots - 1 < nr) issue(i + kSlots - 1);  // refills the slot of round i-1
@@ -321,66 +429,90 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
         const uint8_t *p0 = ring + slot * kSlotBytes;
         const uint8_t *p1 = ring + slot1 * kSlotBytes;
         const uint64_t rbase = (r_begin + i) * kRound;
-        const TextView tv{p0, p1, rbase, has_next ? (uint32_t)(2 * kSlotBytes) : (uint32_t)kSlotBytes};
+        const RingText tx{p0, p1, has_next ? (uint32_t)(2 * kSlotBytes) : (uint32_t)kSlotBytes,
+                          clamp32(a.readable - rbase), a.text + rbase};
 
-        // ---- stage 1: d-gram filter over the lane's 16 starts
-        const uint4 q = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane);
-        uint32_t w4 = __shfl_down_sync(0xffffffffu, q.x, 1);
+        // ---- stage 1: filter over the lane's 32 starts
+        const uint4 q0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane);
+        const uint4 q1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16);
+        uint32_t w8 = __shfl_down_sync(0xffffffffu, q0.x, 1);
         if (lane == 31) {
             if (has_next) {
-                w4 = *reinterpret_cast<const uint32_t *>(p1);
+                w8 = *reinterpret_cast<const uint32_t *>(p1);
             } else {
-                w4 = 0;
+                w8 = 0;
                 const uint64_t j0 = rbase + kRound;
                 for (int b = 0; b < 4; ++b)
-                    if (j0 + b < a.readable) w4 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
+                    if (j0 + b < a.readable) w8 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
             }
         }
-        const uint32_t wv[5] = {q.x, q.y, q.z, q.w, w4};
+        const uint32_t wv[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, w8};
         const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
-        const uint32_t nvalid =
-            lbase >= lim ? 0u : (lim - lbase >= (uint64_t)kPerLane ? (uint32_t)kPerLane : (uint32_t)(lim - lbase));
-        const uint32_t surv = filter16(a, s, wv, kmask, nvalid);
+        uint32_t surv = filter32<Kind>(a, wv, sW, stride, base_lane);
+        if (lbase + kPerLane > lim) {
+            const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
+            surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
+        }
 
-        // ---- stage 2: survivors walk the trie
-        uint32_t c = 0, hm = 0;
-        for (uint32_t m = surv; m; m &= m - 1) {
-            const int k = __ffs(m) - 1;
-            const uint32_t tn = walk(a, s, tv, lbase + k, p0[lane * kPerLane + k]);
-            if (tn != kNone) {
-                const uint32_t ti = term_index(a.t, tn);
-                c += __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
-                hm |= 1u << k;
+        // ---- stage 2: compact survivors into the warp queue, walk with full warps
+        if (__any_sync(0xffffffffu, surv != 0)) {
+            const uint32_t ns = __popc(surv);
+            uint32_t stot;
+            const uint32_t sex = warp_excl_scan(ns, lane, &stot);
+            for (uint32_t qb = 0; qb < stot; qb += kQueue) {
+                if (ns && sex < qb + kQueue && sex + ns > qb) {
+                    uint32_t idx = sex;
+                    for (uint32_t m = surv; m; m &= m - 1, ++idx)
+                        if (idx >= qb && idx < qb + kQueue)
+                            queue[idx - qb] = (uint16_t)(lane * kPerLane + (__ffs(m) - 1));
+                }
+                __syncwarp();
+                const uint32_t n = stot - qb < (uint32_t)kQueue ? stot - qb : (uint32_t)kQueue;
+                for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    uint32_t off = 0;
+                    bool hit = false;
+                    if (j < n) {
+                        off = queue[j];
+                        const uint32_t tn = walk(a, s, tx, off);
+                        if (tn != kNone) {
+                            const uint32_t ti = term_index(a.t, tn);
+                            c += __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
+                            hit = true;
+                        }
+                    }
+                    // hits in queue order == position order
+                    const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+                    if (hit) {
+                        const uint32_t idx = n_hits + __popc(hb & ((1u << lane) - 1u));
+                        if (idx < a.hit_cap) hits[idx] = (uint32_t)(rbase - range_lo) + off;
+                    }
+                    n_hits += __popc(hb);
+                }
+                __syncwarp();
             }
         }
-        // ---- append hit offsets in position order (lane-major, then k)
-        uint32_t htot;
-        const uint32_t hex = warp_excl_scan((uint32_t)__popc(hm), lane, &htot);
-        if (htot) {
-            uint32_t idx = n_hits + hex;
-            const uint32_t off0 = (uint32_t)(lbase - range_lo);
-            for (uint32_t m = hm; m; m &= m - 1, ++idx)
-                if (idx < a.hit_cap) hits[idx] = off0 + (uint32_t)(__ffs(m) - 1);
-            n_hits += htot;
-        }
+        __syncwarp();
+    }
+    uint64_t total;
+    {
         uint32_t ct;
         warp_excl_scan(c, lane, &ct);
-        total += ct;
-        __syncwarp();
+        total = ct;
     }
 
     // ================================================= phase 2: offsets
     if (lane == 0) s_wtot[warp] = total;
     __syncthreads();
     if (warp == 0) {
-        unsigned long long v = s_wtot[lane];  // kWarps == 32
+        const unsigned long long v = lane < kWarps ? s_wtot[lane] : 0ull;
         unsigned long long incl = v;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += y;
         }
-        s_wtot[lane] = incl - v;  // exclusive within the CTA
+        if (lane < kWarps) s_wtot[lane] = incl - v;  // exclusive within the CTA
         if (lane == 31) a.cta_total[blockIdx.x] = incl;
     }
     grid_barrier(&a.ws->barrier[a.parity]);
@@ -406,7 +538,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
 
     // ================================================= phase 3: emit
     if (total == 0) return;
-    const TextView gv{nullptr, nullptr, 0, 0};
     if (n_hits <= a.hit_cap) {
         for (uint32_t b = 0; b < n_hits; b += 32) {
             const uint32_t i = b + lane;
@@ -414,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             uint64_t gi = 0;
             if (i < n_hits) {
                 gi = range_lo + hits[i];
-                const uint32_t tn = walk(a, s, gv, gi, __ldg(a.text + gi));
+                const uint32_t tn = walk(a, s, GlobalText{a.text + gi, clamp32(a.readable - gi)}, 0u);
                 ti = term_index(a.t, tn);
                 cnt = __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
             }
@@ -432,36 +563,39 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             off += ctot;
         }
     } else {
-        // hit list overflowed: scan the range again, writing rows directly
+        // hit list overflowed: scan the range again (text from global memory),
+        // writing rows directly in position order
         for (uint64_t i = 0; i < nr; ++i) {
             const uint64_t rbase = (r_begin + i) * kRound;
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
-            uint32_t wv[5] = {0, 0, 0, 0, 0};
-            for (int b = 0; b < 20; ++b)
+            uint32_t wv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            for (int b = 0; b < 36; ++b)
                 if (lbase + b < a.readable) wv[b >> 2] |= (uint32_t)__ldg(a.text + lbase + b) << (8 * (b & 3));
-            const uint32_t nvalid = lbase >= lim ? 0u
-                                                 : (lim - lbase >= (uint64_t)kPerLane ? (uint32_t)kPerLane
-                                                                                      : (uint32_t)(lim - lbase));
-            const uint32_t surv = filter16(a, s, wv, kmask, nvalid);
-            uint32_t c = 0, hm = 0;
+            uint32_t surv = filter32<Kind>(a, wv, sW, stride, base_lane);
+            if (lbase + kPerLane > lim) {
+                const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
+                surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
+            }
+            const GlobalText gt{a.text + lbase, clamp32(a.readable - lbase)};
+            uint32_t cc = 0, hm = 0;
             for (uint32_t m = surv; m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
-                const uint32_t tn = walk(a, s, gv, lbase + k, __ldg(a.text + lbase + k));
+                const uint32_t tn = walk(a, s, gt, (uint32_t)k);
                 if (tn != kNone) {
                     const uint32_t ti = term_index(a.t, tn);
-                    c += __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
+                    cc += __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
                     hm |= 1u << k;
                 }
             }
             uint32_t ctot;
-            uint64_t o = off + warp_excl_scan(c, lane, &ctot);
+            uint64_t o = off + warp_excl_scan(cc, lane, &ctot);
             for (uint32_t m = hm; m; m &= m - 1) {
-                const uint64_t gi = lbase + (uint64_t)(__ffs(m) - 1);
-                const uint32_t ti = term_index(a.t, walk(a, s, gv, gi, __ldg(a.text + gi)));
+                const uint32_t k = (uint32_t)(__ffs(m) - 1);
+                const uint32_t ti = term_index(a.t, walk(a, s, gt, k));
                 const uint32_t r0 = __ldg(a.t.out_ptr + ti), r1 = __ldg(a.t.out_ptr + ti + 1);
                 for (uint32_t e = r0; e < r1; ++e, ++o) {
                     if (o < a.capacity) {
-                        a.out_pos[o] = a.pos_base + gi;
+                        a.out_pos[o] = a.pos_base + lbase + k;
                         a.out_pid[o] = __ldg(a.t.out_pid + e);
                     }
                 }
@@ -492,7 +626,10 @@ int device_info(int device, DeviceInfo &out, std::string &err) {
         if (e == cudaSuccess)
             e = cudaDeviceGetAttribute(&di.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(pfac_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(pfac_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     di.max_smem_optin);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(pfac_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      di.max_smem_optin);
         if (e != cudaSuccess) {
             err = std::string("device query: ") + cudaGetErrorString(e);
@@ -543,6 +680,7 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.gram = h.filter_gram;
     t.log2_bits = h.filter_log2_bits;
     t.exact = h.filter_exact;
+    t.kind = h.filter_kind;
     t.n_nodes = (uint32_t)h.n_nodes;
     return t;
 }
@@ -584,18 +722,22 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
         err = "pfac_match_device: workspace too small or misaligned";
         return kStatusInvalid;
     }
-    // ---- shared-memory plan: ring + barriers + root + warp totals, then the
-    // filter (replicated while it fits half of the rest), then the hot trie.
+    // ---- shared-memory plan: filter at offset 0 (replicated while it fits
+    // half of what the fixed parts leave), ring, barriers, queues, root,
+    // level-1 bitmaps, warp totals, then the hot trie prefix.
     const uint32_t filter_words = (1u << t.log2_bits) >= 32 ? (1u << t.log2_bits) / 32 : 1u;
-    const uint32_t fixed = kWarps * kSlots * kSlotBytes + kWarps * kSlots * 8 + 1024 + 8 * (kWarps + 1) + 256;
+    const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
+    const uint32_t fixed = kWarps * kSlots * kSlotBytes + kWarps * kSlots * 8 + kWarps * kQueue * 2 + 1024 +
+                           40 * B + 8 * (kWarps + 1) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
         return kStatusLimit;
     }
     const uint32_t rest = (uint32_t)di.max_smem_optin - fixed;
-    uint32_t rep = 1;
-    while (rep < 32 && filter_words * 4 * (rep * 2) <= rest / 2) rep *= 2;
-    const uint32_t trie_budget = rest - filter_words * 4 * rep;
+    uint32_t rep_log2 = 0;
+    while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= rest / 2) rep_log2++;
+    const uint32_t filter_bytes = filter_words * 4 << rep_log2;
+    const uint32_t trie_budget = rest - filter_bytes;
     // H = largest node count whose words [0, H] and labels [0, row_ptr[H]) fit
     uint32_t lo = 0, hi = t.n_nodes - 1;
     while (lo < hi) {
@@ -609,14 +751,16 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     ScanArgs a;
     a.t = t;
     a.filter_words = filter_words;
-    a.filter_rep = rep;
-    uint32_t o = 0;
+    a.rep_log2 = rep_log2;
+    uint32_t o = filter_bytes;
+    o = align_up(o, 128);
     a.off_ring = o;   o += kWarps * kSlots * kSlotBytes;
     a.off_bar = o;    o += kWarps * kSlots * 8;
     a.off_warp = o;   o += 8 * (kWarps + 1);
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
-    a.off_filter = o; o += filter_words * 4 * rep;
+    a.off_queue = o;  o += kWarps * kQueue * 2;
+    a.off_bm = o;     o += 40 * B;
     a.off_node = o;   o = align_up(o + 4 * (H + 1), 16);
     a.off_label = o;  o = align_up(o + EH, 16);
     const size_t smem = o;
@@ -624,6 +768,7 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
         err = "pfac_match_device: internal shared-memory plan error";
         return kStatusLimit;
     }
+    a.n_level1 = B;
     a.hot_nodes = H;
     a.hot_edges = EH;
     uint32_t parity;
@@ -649,8 +794,8 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     a.rounds_per_warp = geo.rounds_per_warp;
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void *)pfac_scan_kernel, dim3((unsigned)geo.grid),
-                                                dim3(kThreads), args, smem, stream);
+    const void *fn = t.kind == 1 ? (const void *)pfac_scan_kernel<1> : (const void *)pfac_scan_kernel<0>;
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)geo.grid), dim3(kThreads), args, smem, stream);
     if (e != cudaSuccess) {
         {   // the kernel did not run: the barrier counter in use is unchanged
             std::lock_guard<std::mutex> lk(g_ws_mu);

@@ -16,7 +16,7 @@ def parse(image: bytes) -> dict:
     f = _HDR.unpack_from(image, 0)
     keys = ["magic", "version", "header_bytes", "image_bytes", "n_nodes", "n_edges", "n_terminals", "n_out",
             "n_patterns", "max_len", "min_len", "filter_gram", "filter_log2_bits", "filter_exact", "filter_mul",
-            "reserved0", "off_node", "off_label", "off_term_node", "off_out_ptr", "off_out_pid", "off_root",
+            "filter_kind", "off_node", "off_label", "off_term_node", "off_out_ptr", "off_out_pid", "off_root",
             "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
@@ -30,6 +30,19 @@ def parse(image: bytes) -> dict:
     nbits = 1 << h["filter_log2_bits"]
     h["filter"] = buf[h["off_filter"]:h["off_filter"] + max(4, nbits // 8)].view(np.uint32)
     return h
+
+
+def filter_bits(h, key):
+    """Bit indices (word * 32 + bit) of the filter entries a d-gram key tests
+    (all must be set for the start to survive)."""
+    if h["filter_kind"] == 1:  # d = 4: blocked two-bit filter (image.h)
+        b = ((key * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
+        return [2 * b * 32 + (31 - ((key >> 24) & 31)), (2 * b + 1) * 32 + (31 - ((key >> 16) & 31))]
+    return [filter_index(h, key)]
+
+
+def filter_pass(h, key):
+    return all((int(h["filter"][i >> 5]) >> (i & 31)) & 1 for i in filter_bits(h, key))
 
 
 def filter_index(h, key):
@@ -49,9 +62,7 @@ def match(h, text: bytes, readable=None, n_starts=None):
     for i in range(ns):
         if i + d > L:
             continue
-        key = int.from_bytes(text[i:i + d], "little")
-        b = filter_index(h, key)
-        if not (int(h["filter"][b >> 5]) >> (b & 31)) & 1:
+        if not filter_pass(h, int.from_bytes(text[i:i + d], "little")):
             continue
         v = int(h["root"][text[i]])
         if v == 0:
