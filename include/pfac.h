@@ -40,7 +40,7 @@ typedef struct CUstream_st *pfac_stream; /* == cudaStream_t; NULL = legacy defau
 typedef enum {
     PFAC_OK = 0,
     PFAC_ERR_INVALID_ARG = 1,  /* NULL pointer, n_patterns == 0, zero-length pattern, length > 65535, bad enum, bad image */
-    PFAC_ERR_LIMIT = 2,        /* trie exceeds 2^31-1 nodes or 2^32-1 pattern-id-list entries */
+    PFAC_ERR_LIMIT = 2,        /* trie exceeds 2^30-1 nodes or 2^32-2 pattern-id-list entries */
     PFAC_ERR_NOMEM = 3,        /* host or device allocation failed */
     PFAC_ERR_CUDA = 4,         /* no usable device / CUDA runtime error (detail in pfac_last_error) */
     PFAC_ERR_CAPACITY = 5      /* (pfac_match only, never device path) internal retry failed */
@@ -51,11 +51,11 @@ typedef enum {
     PFAC_BYTES_UNCOMPRESSED = 1,  /* the paper's original trie: 36 B per node (256-bit bitmap + u32 offset) */
     PFAC_BYTES_DENSE_STT = 2,     /* Lin et al. PFAC state table: 256 x u32 per node */
     PFAC_BYTES_PAPER_CRS = 3,     /* paper CRS of the N x 9 word matrix: (2 nnz + n + 1) x 4 B */
-    PFAC_BYTES_CSR_CORE = 4       /* the CSR trie alone: row_ptr|terminal flag (4 B/node) + labels (1 B/edge) */
+    PFAC_BYTES_CSR_CORE = 4       /* the path-compressed CSR trie alone: node words (4 B/node) + labels (1 B/edge) + tails (16 B + path bytes each) */
 } pfac_bytes_kind;
 
 typedef struct {
-    uint64_t nodes;       /* 1 + number of distinct non-empty pattern prefixes */
+    uint64_t nodes;       /* 1 + number of distinct non-empty pattern prefixes (the uncompressed trie) */
     uint64_t edges;       /* nodes - 1 */
     uint64_t terminals;   /* nodes where at least one pattern ends */
     uint32_t n_patterns;
@@ -63,7 +63,7 @@ typedef struct {
     uint32_t min_len;
     uint32_t filter_gram; /* d of the d-gram first-stage filter (<= min(4, min_len)) */
     uint32_t filter_log2_bits;
-    uint32_t reserved;
+    uint32_t image_nodes; /* nodes stored in the device image after path compression of single-path tails */
 } pfac_stats;
 
 /* Host-side result of pfac_match: library-allocated, free with pfac_matches_free.

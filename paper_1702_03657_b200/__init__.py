@@ -39,7 +39,7 @@ class PfacError(RuntimeError):
 class _Stats(C.Structure):
     _fields_ = [("nodes", C.c_uint64), ("edges", C.c_uint64), ("terminals", C.c_uint64),
                 ("n_patterns", C.c_uint32), ("max_len", C.c_uint32), ("min_len", C.c_uint32),
-                ("filter_gram", C.c_uint32), ("filter_log2_bits", C.c_uint32), ("reserved", C.c_uint32)]
+                ("filter_gram", C.c_uint32), ("filter_log2_bits", C.c_uint32), ("image_nodes", C.c_uint32)]
 
 
 class _Matches(C.Structure):
@@ -130,7 +130,7 @@ class Trie:
     def stats(self) -> dict:
         s = _Stats()
         _check(_lib().pfac_trie_stats(self._h, C.byref(s)), "pfac_trie_stats")
-        return {f: getattr(s, f) for f, _ in _Stats._fields_ if f != "reserved"}
+        return {f: getattr(s, f) for f, _ in _Stats._fields_}
 
     def nbytes(self, kind: str = "device_image") -> int:
         v = C.c_uint64()

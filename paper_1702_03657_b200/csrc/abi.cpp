@@ -165,8 +165,9 @@ pfac_status pfac_trie_bytes(const pfac_trie *t, pfac_bytes_kind kind, uint64_t *
 pfac_status pfac_trie_stats(const pfac_trie *t, pfac_stats *o) {
     if (!t || !o) return fail(kStatusInvalid, "pfac_trie_stats: NULL argument");
     std::memset(o, 0, sizeof *o);
-    o->nodes = t->hdr.n_nodes;
-    o->edges = t->hdr.n_edges;
+    o->nodes = t->hdr.n_nodes_full;
+    o->edges = t->hdr.n_nodes_full - 1;
+    o->image_nodes = t->hdr.n_nodes;
     o->terminals = t->hdr.n_terminals;
     o->n_patterns = t->hdr.n_patterns;
     o->max_len = t->hdr.max_len;

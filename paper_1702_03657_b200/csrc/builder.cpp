@@ -77,9 +77,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     q.reserve(1024);
     q.push_back({0, m, 0, kNone});
     std::vector<uint32_t> own;
+    std::vector<uint32_t> parent{0}, own_pid;  // per node: parent; a pattern ending here (kNone if none)
     for (size_t head = 0; head < q.size(); head++) {
         if (q.size() > (size_t)kEdgeMask) {
-            err = "pfac_build: trie exceeds 2^31-1 nodes";
+            err = "pfac_build: trie exceeds 2^30-1 nodes";
             return kStatusLimit;
         }
         const Range r = q[head];
@@ -90,6 +91,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         while (lo < r.hi && lens[ord[lo]] == r.depth) own.push_back(ord[lo++]);
         uint32_t anc = r.anc_term;
         bool terminal = !own.empty();
+        own_pid.push_back(terminal ? own[0] : kNone);
         // row_ptr[v] = number of nodes numbered before v's first child, minus the root
         uint32_t first_edge = (uint32_t)(q.size() - 1);
         node_word.push_back(first_edge | (terminal ? kTermBit : 0u));
@@ -125,11 +127,120 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
                 last_word = c >> 5;
             }
             q.push_back({i, j, r.depth + 1, anc});
+            parent.push_back(v);
             i = j;
         }
     }
     const uint64_t N = q.size(), E = N - 1, T = term_node.size();
     node_word.push_back((uint32_t)E);  // row_ptr[N]
+
+    // ---- path compression of the non-branching deep part.  A node whose
+    // strict descendants form a single path with one terminal, at its end, is
+    // a "tail start" (topmost such node, path >= 2 bytes).  Its descendants are
+    // removed from the image; the tail start becomes a leaf carrying the
+    // path's bytes and the terminal index of its end, so a walk compares the
+    // rest of the path in one go.  Walk results are unchanged (the removed
+    // nodes have no branching and no other terminal).
+    std::vector<uint8_t> chain_ok(N, 0);
+    std::vector<uint32_t> chain_end(N, kNone);
+    auto nchild = [&](uint64_t v) { return (node_word[v + 1] & kEdgeMask) - (node_word[v] & kEdgeMask); };
+    for (uint64_t v = N; v-- > 0;) {
+        if (nchild(v) != 1) continue;
+        const uint32_t u = (node_word[v] & kEdgeMask) + 1;
+        const bool term_u = (node_word[u] & kTermBit) != 0;
+        if (nchild(u) == 0 && term_u) {
+            chain_ok[v] = 1;
+            chain_end[v] = u;
+        } else if (nchild(u) == 1 && !term_u && chain_ok[u]) {
+            chain_ok[v] = 1;
+            chain_end[v] = chain_end[u];
+        }
+    }
+    std::vector<uint8_t> is_tail(N, 0), internal(N, 0);
+    for (uint64_t v = 1; v < N; v++)
+        if (chain_ok[v] && !chain_ok[parent[v]] && q[chain_end[v]].depth - q[v].depth >= 2) is_tail[v] = 1;
+    for (uint64_t v = 1; v < N; v++) internal[v] = internal[parent[v]] || is_tail[parent[v]];
+    std::vector<uint32_t> old_ti(N, kNone);
+    for (uint64_t t = 0; t < T; t++) old_ti[term_node[t]] = (uint32_t)t;
+    std::vector<uint32_t> new_id(N, kNone);
+    uint64_t NK = 0;
+    for (uint64_t v = 0; v < N; v++)
+        if (!internal[v]) new_id[v] = (uint32_t)NK++;
+
+    // compressed CSR (BFS order of the kept nodes; child through edge e is e+1)
+    std::vector<uint32_t> cnode;
+    std::vector<uint8_t> clabel;
+    std::vector<uint32_t> nterm_old;  // old terminal index of each new terminal index
+    std::vector<uint32_t> cterm_node;
+    cnode.reserve(NK + 1);
+    clabel.reserve(NK);
+    for (uint64_t v = 0; v < N; v++) {
+        if (internal[v]) continue;
+        const bool term = (node_word[v] & kTermBit) != 0;
+        cnode.push_back((uint32_t)clabel.size() | (term ? kTermBit : 0u) | (is_tail[v] ? kTailBit : 0u));
+        if (term) {
+            nterm_old.push_back(old_ti[v]);
+            cterm_node.push_back(new_id[v]);
+        }
+        if (!is_tail[v])
+            for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++) clabel.push_back(label[e]);
+    }
+    cnode.push_back((uint32_t)clabel.size());
+    const uint64_t TK = cterm_node.size();  // kept terminals: indices [0, TK), sorted by node id
+    std::vector<uint32_t> tail_bits((NK + 31) / 32, 0u), tail_rank((NK + 31) / 32, 0u);
+    std::vector<uint32_t> tails;  // 4 words per tail: bytes offset, length, terminal index, 0
+    std::vector<uint8_t> tail_bytes;
+    for (uint64_t v = 0; v < N; v++) {
+        if (internal[v] || !is_tail[v]) continue;
+        const uint32_t end = chain_end[v];
+        const uint32_t dv = q[v].depth, de = q[end].depth;
+        const uint32_t k = own_pid[end];
+        tails.push_back((uint32_t)tail_bytes.size());  // 4-byte aligned
+        tails.push_back(de - dv);
+        tails.push_back((uint32_t)nterm_old.size());
+        tails.push_back(0u);
+        nterm_old.push_back(old_ti[end]);
+        tail_bytes.insert(tail_bytes.end(), pats[k] + dv, pats[k] + de);
+        while (tail_bytes.size() & 3) tail_bytes.push_back(0);
+        tail_bits[new_id[v] >> 5] |= 1u << (new_id[v] & 31);
+    }
+    {
+        uint32_t acc = 0;
+        for (size_t w = 0; w < tail_bits.size(); w++) {
+            tail_rank[w] = acc;
+            acc += (uint32_t)__builtin_popcount(tail_bits[w]);
+        }
+    }
+    const uint64_t NT = tails.size() / 4;
+    tail_bytes.insert(tail_bytes.end(), 4, 0);  // slack for 4-byte reads
+    // pid lists in the new terminal order
+    std::vector<uint32_t> cout_ptr{0}, cout_pid;
+    cout_pid.reserve(out_pid.size());
+    for (uint32_t ot : nterm_old) {
+        cout_pid.insert(cout_pid.end(), out_pid.begin() + out_ptr[ot], out_pid.begin() + out_ptr[ot + 1]);
+        cout_ptr.push_back((uint32_t)cout_pid.size());
+    }
+    const uint64_t N_full = N;
+    node_word.swap(cnode);
+    label.swap(clabel);
+    term_node.swap(cterm_node);
+    out_ptr.swap(cout_ptr);
+    out_pid.swap(cout_pid);
+    const uint64_t NI = NK, EI = NK - 1;  // image nodes / edges
+
+    // ---- level 1 as bitmapped nodes (Fig. 3)
+    const uint32_t B = node_word[1] & kEdgeMask;  // root's children are nodes 1..B
+    std::vector<uint32_t> level1((size_t)B * 10, 0u);
+    for (uint32_t v = 1; v <= B; v++) {
+        uint32_t *o = &level1[(size_t)(v - 1) * 10];
+        for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++)
+            o[label[e] >> 5] |= 1u << (label[e] & 31);
+        uint32_t pre = 0;
+        for (int w = 0; w < 8; w++) {
+            o[8 + w / 4] |= pre << (8 * (w % 4));
+            pre += (uint32_t)__builtin_popcount(o[w]);
+        }
+    }
 
     // ---- derived tables: level-1 direct table and first-stage d-gram filter
     std::vector<uint32_t> root(256, 0);
@@ -179,9 +290,11 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     std::memcpy(h.magic, "PFACIMG1", 8);
     h.version = kVersion;
     h.header_bytes = sizeof(ImageHeader);
-    h.n_nodes = N;
-    h.n_edges = E;
+    h.n_nodes = NI;
+    h.n_edges = EI;
     h.n_terminals = T;
+    h.n_kept_terminals = TK;
+    h.n_nodes_full = N_full;
     h.n_out = out_pid.size();
     h.n_patterns = m;
     h.max_len = max_len;
@@ -192,18 +305,26 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     h.filter_mul = kFilterMul;
     h.filter_kind = kind;
     uint64_t o = align256(sizeof(ImageHeader));
-    h.off_node = o;      o = align256(o + 4 * (N + 1));
-    h.off_label = o;     o = align256(o + E + 16);
-    h.off_term_node = o; o = align256(o + 4 * T);
+    h.off_node = o;      o = align256(o + 4 * (NI + 1));
+    h.off_label = o;     o = align256(o + EI + 16);
+    h.off_term_node = o; o = align256(o + 4 * TK);
     h.off_out_ptr = o;   o = align256(o + 4 * (T + 1));
     h.off_out_pid = o;   o = align256(o + 4 * out_pid.size());
     h.off_root = o;      o = align256(o + 4 * 256);
     h.off_filter = o;    o = align256(o + 4 * filter.size());
+    h.off_tail_bits = o; o = align256(o + 4 * tail_bits.size());
+    h.off_tail_rank = o; o = align256(o + 4 * tail_rank.size());
+    h.off_tails = o;     o = align256(o + 16 * NT);
+    h.off_tail_bytes = o; o = align256(o + tail_bytes.size() + 16);
+    h.off_level1 = o;    o = align256(o + 40ull * B);
+    h.n_level1 = B;
+    h.n_tails = NT;
+    h.n_tail_bytes = tail_bytes.size();
     h.image_bytes = o;
-    h.bytes_uncompressed = 36 * N;
-    h.bytes_dense_stt = 1024 * N;                      // 256 x u32 per state
-    h.bytes_paper_crs = 4 * (2 * paper_nnz + N + 1);   // PAPER.md:101, N x 9 words
-    h.bytes_csr_core = 4 * (N + 1) + E;
+    h.bytes_uncompressed = 36 * N_full;
+    h.bytes_dense_stt = 1024 * N_full;                       // 256 x u32 per state
+    h.bytes_paper_crs = 4 * (2 * paper_nnz + N_full + 1);    // PAPER.md:101, N x 9 words
+    h.bytes_csr_core = 4 * (NI + 1) + EI + 16 * NT + (tail_bytes.size() - 4);  // CSR + tails
 
     try {
         image.assign(o, 0);
@@ -213,13 +334,18 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     }
     uint8_t *p = image.data();
     std::memcpy(p, &h, sizeof h);
-    std::memcpy(p + h.off_node, node_word.data(), 4 * (N + 1));
-    if (E) std::memcpy(p + h.off_label, label.data(), E);
-    if (T) std::memcpy(p + h.off_term_node, term_node.data(), 4 * T);
+    std::memcpy(p + h.off_node, node_word.data(), 4 * (NI + 1));
+    if (EI) std::memcpy(p + h.off_label, label.data(), EI);
+    if (TK) std::memcpy(p + h.off_term_node, term_node.data(), 4 * TK);
     std::memcpy(p + h.off_out_ptr, out_ptr.data(), 4 * (T + 1));
     if (!out_pid.empty()) std::memcpy(p + h.off_out_pid, out_pid.data(), 4 * out_pid.size());
     std::memcpy(p + h.off_root, root.data(), 4 * 256);
     std::memcpy(p + h.off_filter, filter.data(), 4 * filter.size());
+    std::memcpy(p + h.off_tail_bits, tail_bits.data(), 4 * tail_bits.size());
+    std::memcpy(p + h.off_tail_rank, tail_rank.data(), 4 * tail_rank.size());
+    if (NT) std::memcpy(p + h.off_tails, tails.data(), 16 * NT);
+    if (!tail_bytes.empty()) std::memcpy(p + h.off_tail_bytes, tail_bytes.data(), tail_bytes.size());
+    std::memcpy(p + h.off_level1, level1.data(), 40ull * B);
     return kStatusOk;
 }
 
@@ -238,17 +364,24 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
     const uint64_t N = h.n_nodes, E = h.n_edges, T = h.n_terminals;
     auto in = [&](uint64_t off, uint64_t bytes) { return off >= sizeof(ImageHeader) && off + bytes <= size; };
     bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
-              in(h.off_term_node, 4 * T) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
+              h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails == T && h.n_nodes_full >= N &&
+              in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
               in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && h.filter_gram <= 4 &&
               h.filter_gram <= h.min_len && h.min_len <= h.max_len && h.max_len <= kMaxPatternLen &&
               h.filter_mul == kFilterMul && h.filter_kind == (h.filter_gram == 4 ? 1u : 0u) &&
-              (h.filter_kind == 0 || h.filter_log2_bits >= 10);
+              (h.filter_kind == 0 || h.filter_log2_bits >= 10) && in(h.off_tail_bits, 4 * ((N + 31) / 32)) &&
+              in(h.off_tail_rank, 4 * ((N + 31) / 32)) && in(h.off_tails, 16 * h.n_tails) &&
+              in(h.off_tail_bytes, h.n_tail_bytes) && in(h.off_level1, 40 * h.n_level1);
     if (ok) {
         const uint32_t *node = reinterpret_cast<const uint32_t *>(p + h.off_node);
         const uint32_t *out_ptr = reinterpret_cast<const uint32_t *>(p + h.off_out_ptr);
-        ok = (node[0] & kEdgeMask) == 0 && (node[N] & kEdgeMask) == E && out_ptr[0] == 0 && out_ptr[T] == h.n_out;
+        ok = (node[0] & kEdgeMask) == 0 && (node[N] & kEdgeMask) == E && out_ptr[0] == 0 && out_ptr[T] == h.n_out &&
+             h.n_level1 == (node[1] & kEdgeMask) && h.n_level1 >= 1 && h.n_level1 <= 256;
         for (uint64_t v = 0; ok && v < N; v++) ok = (node[v] & kEdgeMask) <= (node[v + 1] & kEdgeMask);
+        const uint32_t *tails = reinterpret_cast<const uint32_t *>(p + h.off_tails);
+        for (uint64_t i = 0; ok && i < h.n_tails; i++)
+            ok = (uint64_t)tails[4 * i] + tails[4 * i + 1] <= h.n_tail_bytes && tails[4 * i + 2] < T;
     }
     if (!ok) {
         err = "pfac_attach: inconsistent image sections";

@@ -6,20 +6,38 @@
 //
 //   node   u32[N+1]   CSR row pointer of the breadth-first row-major trie
 //                     (PAPER.md:80 steps I-II; CRS row_ptr):
-//                     bits 0..30 = index of the node's first outgoing edge,
-//                     bit 31 = "a pattern ends at this node".  Children of a
+//                     bits 0..29 = index of the node's first outgoing edge,
+//                     bit 31 = "a pattern ends at this node", bit 30 = "tail
+//                     start" (below this node the trie is a single path whose
+//                     only terminal is its last node; see tails).  Children of a
 //                     node are consecutive and in ascending byte order, so the
 //                     child reached through edge e is node e+1 (implicit
 //                     col_ind: the BFS numbering makes it redundant).
 //   label  u8[E]      edge labels (CRS val, one byte per edge).
-//   term_node u32[T]  ascending ids of terminal nodes.
-//   out_ptr u32[T+1]  offsets into out_pid.
+//   term_node u32[TK] ascending ids of the terminal nodes kept in the image
+//                     (terminal indices 0..TK-1); terminal indices TK..T-1 are
+//                     the ends of the compressed tails, in tail order.
+//   out_ptr u32[T+1]  offsets into out_pid, by terminal index.
 //   out_pid u32[..]   per terminal t, the ascending union of the pattern ids
 //                     ending on the root->t path.  A walk passes every ancestor
 //                     of the deepest node it reaches, so the matches of one
 //                     start position are exactly this list for the deepest
 //                     terminal passed (prefix closure).
 //   root   u32[256]   child of the root per byte (0 = none): level 1 direct.
+//   tail_bits u32[ceil(N/32)], tail_rank u32[ceil(N/32)]  bit v = node v is a
+//                     tail start; rank = tail_rank[v/32] + popc(bits below v).
+//   tails  uint4[n_tails]  {offset into tail_bytes, path length L, terminal
+//                     index of the path's end, 0}.  Path compression: below a
+//                     tail start the uncompressed trie is a single path whose
+//                     only terminal is its end; those nodes are not in the
+//                     image, and a walk at a tail start compares the next L
+//                     text bytes with tail_bytes[offset, offset+L) in one go.
+//   tail_bytes u8[..] the labels of each tail path, concatenated (each tail
+//                     starts 4-byte aligned; 4 zero bytes of slack at the end).
+//   level1 u32[B][10] the root's children (nodes 1..B) as the paper's bitmapped
+//                     nodes (Fig. 3): 8 words = 256-bit child
+//                     bitmap, 2 words = per-word prefix popcounts (one byte
+//                     each); child(c) = first_edge + prefix + rank + 1.
 //   filter u32[2^F/32] first-stage filter over the first d bytes of every
 //                     pattern (d = min(4, shortest pattern)); a start whose bit
 //                     is clear cannot match.  Two kinds:
@@ -43,9 +61,10 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 2;
+constexpr uint32_t kVersion = 4;
 constexpr uint32_t kTermBit = 0x80000000u;
-constexpr uint32_t kEdgeMask = 0x7FFFFFFFu;
+constexpr uint32_t kTailBit = 0x40000000u;
+constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kFilterMul = 0x9E3779B1u;  // Fibonacci hashing multiplier (odd)
 
@@ -59,7 +78,10 @@ struct ImageHeader {
     uint32_t filter_log2_bits, filter_exact, filter_mul, filter_kind;
     uint64_t off_node, off_label, off_term_node, off_out_ptr, off_out_pid, off_root, off_filter;
     uint64_t bytes_uncompressed, bytes_dense_stt, bytes_paper_crs, bytes_csr_core;
-    uint8_t pad[256 - 8 - 8 - 8 - 32 - 16 - 16 - 56 - 32];
+    uint64_t n_tails, n_tail_bytes, off_tail_bits, off_tail_rank, off_tails, off_tail_bytes;
+    uint64_t n_level1, off_level1;
+    uint64_t n_kept_terminals, n_nodes_full;
+    uint8_t pad[256 - 8 - 8 - 8 - 32 - 16 - 16 - 56 - 32 - 48 - 16 - 16];
 };
 static_assert(sizeof(ImageHeader) == 256, "header must be 256 bytes");
 

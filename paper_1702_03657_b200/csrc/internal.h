@@ -8,6 +8,7 @@
 #include "image.h"
 
 struct CUstream_st;
+#include <vector_types.h>
 
 namespace pfac {
 
@@ -36,7 +37,13 @@ struct DevTrie {
     const uint32_t *out_pid;
     const uint32_t *root;
     const uint32_t *filter;
+    const uint32_t *tail_bits;
+    const uint32_t *tail_rank;
+    const uint4 *tails;
+    const uint8_t *tail_bytes;
+    const uint32_t *level1;
     uint32_t n_terminals;
+    uint32_t n_kept_terminals;
     uint32_t max_len;
     uint32_t gram;
     uint32_t log2_bits;

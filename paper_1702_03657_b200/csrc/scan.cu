@@ -72,7 +72,7 @@ struct ScanArgs {
     uint64_t *out_count;
     WsHeader *ws;
     unsigned long long *cta_total;  // [gridDim.x]
-    uint32_t *hits;                 // [warps][hit_cap] start offsets within the warp's range
+    uint2 *hits;                    // [warps][hit_cap] (start offset within the warp's range, terminal index)
     uint32_t hit_cap;
     uint32_t parity;                // barrier counter used by this launch
     uint64_t rounds_per_warp;
@@ -128,6 +128,12 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__host__ __device__ constexpr uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -187,18 +193,73 @@ struct RingText {
         if (r < span) return r < (uint32_t)kSlotBytes ? p0[r] : p1[r - kSlotBytes];
         return __ldg(g + r);
     }
+    // 4 bytes at offset r (little-endian; bytes past `end` are unspecified)
+    __device__ __forceinline__ uint32_t at4(uint32_t r) const {
+        if (r + 4 <= span) {
+            const uint32_t i = r >> 2;  // aligned words i, i+1 of the 1-2 slot window
+            const uint32_t *w0 = reinterpret_cast<const uint32_t *>(p0);
+            const uint32_t *w1 = reinterpret_cast<const uint32_t *>(p1);
+            constexpr uint32_t kW = kSlotBytes / 4;
+            const uint32_t lo = i < kW ? w0[i] : w1[i - kW];
+            const uint32_t hi = (i + 1) < kW ? w0[i + 1] : ((i + 1 - kW) < kW ? w1[i + 1 - kW] : 0u);
+            return __funnelshift_r(lo, hi, 8 * (r & 3));
+        }
+        uint32_t x = 0;
+        for (int b = 0; b < 4; ++b)
+            if (r + b < end) x |= at(r + b) << (8 * b);
+        return x;
+    }
 };
 struct GlobalText {
     const uint8_t *g;
     uint32_t end;
     __device__ __forceinline__ uint32_t at(uint32_t r) const { return __ldg(g + r); }
+    __device__ __forceinline__ uint32_t at4(uint32_t r) const {
+        uint32_t x = 0;
+        for (int b = 0; b < 4; ++b)
+            if (r + b < end) x |= (uint32_t)__ldg(g + r + b) << (8 * b);
+        return x;
+    }
 };
 
-// Walk from the start at offset r0 to the first mismatch; returns the deepest
-// terminal node passed, or kNone.  Level 1 (the root's children, nodes
+// Walk from the start at offset r0 to the first mismatch; returns the terminal
+// index of the deepest terminal passed, or kNone.  Level 1 (the root's children, nodes
 // [1, B]) uses the paper's bitmapped node (Fig. 3: 256-bit child
 // bitmap + offset, child = offset + rank of c among the set bits); deeper
 // nodes use the CSR label list of the image.
+// Tail jump at tail-start node v with the next text byte at offset j: the
+// rest of the trie below v is one path of L bytes ending at a terminal, so it
+// matches iff the next L text bytes equal the path's labels.
+__device__ __forceinline__ uint32_t term_index(const DevTrie &t, uint32_t v) {
+    uint32_t lo = 0, hi = t.n_kept_terminals;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(t.term_node + mid) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+// terminal index of node `last` (kNone stays kNone)
+__device__ __forceinline__ uint32_t term_of(const DevTrie &t, uint32_t last) {
+    return last == kNone ? kNone : term_index(t, last);
+}
+
+// Tail jump at tail-start node v with the next text byte at offset j: below v
+// the trie is one path of L bytes ending at a terminal, so it matches iff the
+// next L text bytes equal the path's bytes.  Returns a terminal index.
+template <class Text>
+__device__ __forceinline__ uint32_t tail_jump(const ScanArgs &a, const Text &tx, uint32_t v, uint32_t j, uint32_t last) {
+    const uint32_t idx = __ldg(a.t.tail_rank + (v >> 5)) + __popc(__ldg(a.t.tail_bits + (v >> 5)) & ((1u << (v & 31)) - 1u));
+    const uint4 rec = __ldg(a.t.tails + idx);
+    if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(a.t, last);
+    const uint32_t *pw = reinterpret_cast<const uint32_t *>(a.t.tail_bytes + rec.x);  // 4-byte aligned
+    for (uint32_t k = 0; k < rec.y; k += 4) {
+        const uint32_t n = rec.y - k;
+        const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
+        if ((tx.at4(j + k) ^ __ldg(pw + (k >> 2))) & m) return term_of(a.t, last);
+    }
+    return rec.z;
+}
+
 template <class Text>
 __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0) {
     uint32_t v = s.root[tx.at(r0)];
@@ -206,12 +267,13 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
     uint32_t w = node_word(a, s, v);
     uint32_t last = (w & kTermBit) ? v : kNone;
     uint32_t j = r0 + 1;
-    if (j >= tx.end) return last;
+    if (j >= tx.end) return term_of(a.t, last);
+    if (w & kTailBit) return tail_jump(a, tx, v, j, last);
     {   // level 1 -> 2 through the bitmap
         const uint32_t c = tx.at(j);
         const uint32_t *bm = s.bm + (v - 1) * 10;
         const uint32_t word = bm[c >> 5];
-        if (!((word >> (c & 31)) & 1u)) return last;
+        if (!((word >> (c & 31)) & 1u)) return term_of(a.t, last);
         const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
         v = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
         w = node_word(a, s, v);
@@ -219,6 +281,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
         ++j;
     }
     for (; j < tx.end; ++j) {
+        if (w & kTailBit) return tail_jump(a, tx, v, j, last);
         const uint32_t lo0 = w & kEdgeMask;
         const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
         if (lo0 == hi0) break;  // leaf
@@ -245,19 +308,11 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
         w = node_word(a, s, v);
         if (w & kTermBit) last = v;
     }
-    return last;
+    return term_of(a.t, last);
 }
 
 __device__ __forceinline__ uint32_t clamp32(uint64_t x) { return x > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)x; }
 
-__device__ __forceinline__ uint32_t term_index(const DevTrie &t, uint32_t v) {
-    uint32_t lo = 0, hi = t.n_terminals;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(t.term_node + mid) < v) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
 
 // Stage 1 over one lane's 32 starts (text bytes wv[0..8] little-endian):
 // bit k set <=> start k may match.
@@ -325,45 +380,13 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
     uint16_t *queue = reinterpret_cast<uint16_t *>(smem + a.off_queue) + warp * kQueue;
 
-    // ---- one-time: clear the other barrier counter; stage tables in smem
-    if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;
-    const uint32_t rep = 1u << a.rep_log2;
-    if (Kind == 1) {  // interleave 8-byte blocks
-        for (uint32_t i = tid; i < (a.filter_words << a.rep_log2); i += kThreads)
-            s_filter[i] = __ldg(a.t.filter + (((i >> 1) >> a.rep_log2) << 1) + (i & 1));
-    } else {
-        for (uint32_t i = tid; i < (a.filter_words << a.rep_log2); i += kThreads)
-            s_filter[i] = __ldg(a.t.filter + (i >> a.rep_log2));
-    }
-    for (uint32_t i = tid; i < 256; i += kThreads) s_root[i] = __ldg(a.t.root + i);
-    for (uint32_t i = tid; i <= a.hot_nodes; i += kThreads) s_node[i] = __ldg(a.t.node + i);
-    for (uint32_t i = tid; i < a.hot_edges; i += kThreads) s_label[i] = __ldg(a.t.label + i);
-    // level-1 bitmapped nodes: 8 bitmap words + 2 words of per-word prefix
-    // popcounts (bytes); built from the CSR labels of nodes [1, B]
-    for (uint32_t i = tid; i < a.n_level1 * 10; i += kThreads) s_bm[i] = 0u;
-    __syncthreads();
-    for (uint32_t v = 1 + warp; v <= a.n_level1; v += kWarps) {
-        const uint32_t e0 = __ldg(a.t.node + v) & kEdgeMask, e1 = __ldg(a.t.node + v + 1) & kEdgeMask;
-        uint32_t *o = s_bm + (v - 1) * 10;
-        for (uint32_t e = e0 + lane; e < e1; e += 32) {
-            const uint32_t c = __ldg(a.t.label + e);
-            atomicOr(&o[c >> 5], 1u << (c & 31));
-        }
-        __syncwarp();
-        if (lane == 0) {
-            uint32_t pre = 0, p0 = 0, p1 = 0;
-            for (int q = 0; q < 8; ++q) {
-                if (q < 4) p0 |= pre << (8 * q); else p1 |= pre << (8 * (q - 4));
-                pre += __popc(o[q]);
-            }
-            o[8] = p0;
-            o[9] = p1;
-        }
-    }
+    // ---- barriers: per-warp text ring + one for the table staging
+    uint64_t *sbar = reinterpret_cast<uint64_t *>(smem + a.off_bar) + kWarps * kSlots;
     if (lane < kSlots) mbar_init(&bars[lane], 1);
+    if (tid == 0) mbar_init(sbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;  // for the next launch
     __syncthreads();
-
     Smem s;
     s.filter_base = 0;
     s.root = s_root;
@@ -374,12 +397,14 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     // (kind 1: 8-byte block b of copy r at filter + 8*(b*rep + r); kind 0:
     // word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
     // so the lanes of a phase spread over the banks
+    const uint32_t rep = 1u << a.rep_log2;
     const uint32_t unit = Kind == 1 ? 8u : 4u;
     const uint32_t sW = 32u - (a.t.log2_bits - (Kind == 1 ? 6u : 5u));  // block index = hash >> sW
     const uint32_t stride = rep * unit;
     const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
 
     const uint64_t policy = evict_first_policy();
+    const uint64_t policy_last = evict_last_policy();
     // starts < lim are valid: inside [0, n_starts) and their d-gram fits
     const uint32_t gram = a.t.gram;
     const uint64_t lim = (a.readable + 1 >= gram && a.readable + 1 - gram < a.n_starts) ? a.readable + 1 - gram
@@ -390,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     const uint64_t r_begin = gw * a.rounds_per_warp < n_rounds ? gw * a.rounds_per_warp : n_rounds;
     const uint64_t r_end = r_begin + a.rounds_per_warp < n_rounds ? r_begin + a.rounds_per_warp : n_rounds;
     const uint64_t range_lo = r_begin * kRound;
-    uint32_t *hits = a.hits + gw * a.hit_cap;
+    uint2 *hits = a.hits + gw * a.hit_cap;
 
     // Fill slot `i % kSlots` with round r_begin + i of this warp's range.
     auto issue = [&](uint64_t i) {
@@ -414,9 +439,45 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
         }
     };
 
-    // ================================================= phase 1: scan
+    // ---- start streaming this warp's text, then stage the tables (TMA bulk
+    // copies of the image sections; the filter is replicated from 16-byte loads)
     const uint64_t nr = r_end - r_begin;
     for (uint64_t i = 0; i < nr && i < kSlots - 1; ++i) issue(i);
+    if (tid == 0) {
+        const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
+                       nb_l1 = align16(40 * a.n_level1);
+        mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1);
+        bulk_g2s(s_root, a.t.root, 1024, sbar, policy_last);
+        bulk_g2s(s_node, a.t.node, nb_node, sbar, policy_last);
+        if (nb_label) bulk_g2s(s_label, a.t.label, nb_label, sbar, policy_last);
+        bulk_g2s(s_bm, a.t.level1, nb_l1, sbar, policy_last);
+    }
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.t.filter);
+        const uint32_t nvec = (a.filter_words + 3) / 4;
+        for (uint32_t i = tid; i < nvec; i += kThreads) {
+            const uint4 v = __ldg(src + i);
+            if (Kind == 1) {  // two 8-byte blocks, each copied rep times
+                uint2 *d = reinterpret_cast<uint2 *>(s_filter) + (2 * i) * rep;
+                for (uint32_t r = 0; r < rep; ++r) {
+                    d[r] = make_uint2(v.x, v.y);
+                    d[rep + r] = make_uint2(v.z, v.w);
+                }
+            } else {  // four words, each copied rep times
+                uint32_t *d = s_filter + (4 * i) * rep;
+                for (uint32_t r = 0; r < rep; ++r) {
+                    d[r] = v.x;
+                    d[rep + r] = v.y;
+                    d[2 * rep + r] = v.z;
+                    d[3 * rep + r] = v.w;
+                }
+            }
+        }
+    }
+    mbar_wait(sbar, 0);
+    __syncthreads();
+
+    // ================================================= phase 1: scan
     uint32_t c = 0;       // pattern ids matched by this lane's starts
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
     for (uint64_t i = 0; i < nr; ++i) {
@@ -470,22 +531,18 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
                 const uint32_t n = stot - qb < (uint32_t)kQueue ? stot - qb : (uint32_t)kQueue;
                 for (uint32_t j0 = 0; j0 < n; j0 += 32) {
                     const uint32_t j = j0 + lane;
-                    uint32_t off = 0;
-                    bool hit = false;
+                    uint32_t off = 0, tn = kNone;
                     if (j < n) {
                         off = queue[j];
-                        const uint32_t tn = walk(a, s, tx, off);
-                        if (tn != kNone) {
-                            const uint32_t ti = term_index(a.t, tn);
-                            c += __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
-                            hit = true;
-                        }
+                        tn = walk(a, s, tx, off);  // terminal index
+                        if (tn != kNone) c += __ldg(a.t.out_ptr + tn + 1) - __ldg(a.t.out_ptr + tn);
                     }
+                    const bool hit = tn != kNone;
                     // hits in queue order == position order
                     const uint32_t hb = __ballot_sync(0xffffffffu, hit);
                     if (hit) {
                         const uint32_t idx = n_hits + __popc(hb & ((1u << lane) - 1u));
-                        if (idx < a.hit_cap) hits[idx] = (uint32_t)(rbase - range_lo) + off;
+                        if (idx < a.hit_cap) hits[idx] = make_uint2((uint32_t)(rbase - range_lo) + off, tn);
                     }
                     n_hits += __popc(hb);
                 }
@@ -544,9 +601,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             uint32_t ti = kNone, cnt = 0;
             uint64_t gi = 0;
             if (i < n_hits) {
-                gi = range_lo + hits[i];
-                const uint32_t tn = walk(a, s, GlobalText{a.text + gi, clamp32(a.readable - gi)}, 0u);
-                ti = term_index(a.t, tn);
+                const uint2 h = hits[i];
+                gi = range_lo + h.x;
+                ti = h.y;
                 cnt = __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
             }
             uint32_t ctot;
@@ -580,9 +637,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             uint32_t cc = 0, hm = 0;
             for (uint32_t m = surv; m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
-                const uint32_t tn = walk(a, s, gt, (uint32_t)k);
-                if (tn != kNone) {
-                    const uint32_t ti = term_index(a.t, tn);
+                const uint32_t ti = walk(a, s, gt, (uint32_t)k);
+                if (ti != kNone) {
                     cc += __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
                     hm |= 1u << k;
                 }
@@ -591,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             uint64_t o = off + warp_excl_scan(cc, lane, &ctot);
             for (uint32_t m = hm; m; m &= m - 1) {
                 const uint32_t k = (uint32_t)(__ffs(m) - 1);
-                const uint32_t ti = term_index(a.t, walk(a, s, gt, k));
+                const uint32_t ti = walk(a, s, gt, k);
                 const uint32_t r0 = __ldg(a.t.out_ptr + ti), r1 = __ldg(a.t.out_ptr + ti + 1);
                 for (uint32_t e = r0; e < r1; ++e, ++o) {
                     if (o < a.capacity) {
@@ -675,7 +731,13 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.out_pid = reinterpret_cast<const uint32_t *>(d + h.off_out_pid);
     t.root = reinterpret_cast<const uint32_t *>(d + h.off_root);
     t.filter = reinterpret_cast<const uint32_t *>(d + h.off_filter);
+    t.tail_bits = reinterpret_cast<const uint32_t *>(d + h.off_tail_bits);
+    t.tail_rank = reinterpret_cast<const uint32_t *>(d + h.off_tail_rank);
+    t.tails = reinterpret_cast<const uint4 *>(d + h.off_tails);
+    t.tail_bytes = d + h.off_tail_bytes;
+    t.level1 = reinterpret_cast<const uint32_t *>(d + h.off_level1);
     t.n_terminals = (uint32_t)h.n_terminals;
+    t.n_kept_terminals = (uint32_t)h.n_kept_terminals;
     t.max_len = h.max_len;
     t.gram = h.filter_gram;
     t.log2_bits = h.filter_log2_bits;
@@ -690,7 +752,7 @@ int workspace_bytes_for(uint64_t n_starts, int device, uint64_t *out, std::strin
     int st = device_info(device, di, err);
     if (st != kStatusOk) return st;
     const Geometry g = geometry(n_starts, di.sms);
-    *out = kWsFixed + 4ull * g.warps * g.hit_cap;
+    *out = kWsFixed + 8ull * g.warps * g.hit_cap;
     return kStatusOk;
 }
 
@@ -717,7 +779,7 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     int st = device_info(device, di, err);
     if (st != kStatusOk) return st;
     const Geometry geo = geometry(n_starts, di.sms);
-    const uint64_t need = kWsFixed + 4ull * geo.warps * geo.hit_cap;
+    const uint64_t need = kWsFixed + 8ull * geo.warps * geo.hit_cap;
     if (!d_ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(d_ws) & 15)) {
         err = "pfac_match_device: workspace too small or misaligned";
         return kStatusInvalid;
@@ -727,8 +789,8 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     // level-1 bitmaps, warp totals, then the hot trie prefix.
     const uint32_t filter_words = (1u << t.log2_bits) >= 32 ? (1u << t.log2_bits) / 32 : 1u;
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
-    const uint32_t fixed = kWarps * kSlots * kSlotBytes + kWarps * kSlots * 8 + kWarps * kQueue * 2 + 1024 +
-                           40 * B + 8 * (kWarps + 1) + 512;
+    const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + kWarps * kQueue * 2 + 1024 +
+                           align16(40 * B) + 8 * (kWarps + 1) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
         return kStatusLimit;
@@ -742,7 +804,7 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     uint32_t lo = 0, hi = t.n_nodes - 1;
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        const uint64_t bytes = 4ull * (mid + 1) + 16 + ((uint64_t)(host_node[mid] & kEdgeMask) + 15) / 16 * 16;
+        const uint64_t bytes = align16(4 * (mid + 1)) + align16(host_node[mid] & kEdgeMask);
         if (bytes <= trie_budget) lo = mid; else hi = mid - 1;
     }
     const uint32_t H = lo;
@@ -755,14 +817,14 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     uint32_t o = filter_bytes;
     o = align_up(o, 128);
     a.off_ring = o;   o += kWarps * kSlots * kSlotBytes;
-    a.off_bar = o;    o += kWarps * kSlots * 8;
+    a.off_bar = o;    o += (kWarps * kSlots + 1) * 8;
     a.off_warp = o;   o += 8 * (kWarps + 1);
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
     a.off_queue = o;  o += kWarps * kQueue * 2;
-    a.off_bm = o;     o += 40 * B;
-    a.off_node = o;   o = align_up(o + 4 * (H + 1), 16);
-    a.off_label = o;  o = align_up(o + EH, 16);
+    a.off_bm = o;     o += align16(40 * B);
+    a.off_node = o;   o += align16(4 * (H + 1));
+    a.off_label = o;  o += align16(EH);
     const size_t smem = o;
     if (smem > (size_t)di.max_smem_optin) {
         err = "pfac_match_device: internal shared-memory plan error";
@@ -788,7 +850,7 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     a.out_count = d_count;
     a.ws = reinterpret_cast<WsHeader *>(d_ws);
     a.cta_total = reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(d_ws) + sizeof(WsHeader));
-    a.hits = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_ws) + kWsFixed);
+    a.hits = reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(d_ws) + kWsFixed);
     a.hit_cap = geo.hit_cap;
     a.parity = parity;
     a.rounds_per_warp = geo.rounds_per_warp;

@@ -7,9 +7,10 @@ import struct
 import numpy as np
 
 TERM = 0x80000000
-MASK = 0x7FFFFFFF
+TAIL = 0x40000000
+MASK = 0x3FFFFFFF
 
-_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ")
+_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ")
 
 
 def parse(image: bytes) -> dict:
@@ -17,19 +18,32 @@ def parse(image: bytes) -> dict:
     keys = ["magic", "version", "header_bytes", "image_bytes", "n_nodes", "n_edges", "n_terminals", "n_out",
             "n_patterns", "max_len", "min_len", "filter_gram", "filter_log2_bits", "filter_exact", "filter_mul",
             "filter_kind", "off_node", "off_label", "off_term_node", "off_out_ptr", "off_out_pid", "off_root",
-            "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core"]
+            "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core",
+            "n_tails", "n_tail_bytes", "off_tail_bits", "off_tail_rank", "off_tails", "off_tail_bytes",
+            "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
     h["node"] = buf[h["off_node"]:h["off_node"] + 4 * (N + 1)].view(np.uint32)
     h["label"] = buf[h["off_label"]:h["off_label"] + E]
-    h["term_node"] = buf[h["off_term_node"]:h["off_term_node"] + 4 * T].view(np.uint32)
+    h["term_node"] = buf[h["off_term_node"]:h["off_term_node"] + 4 * h["n_kept_terminals"]].view(np.uint32)
     h["out_ptr"] = buf[h["off_out_ptr"]:h["off_out_ptr"] + 4 * (T + 1)].view(np.uint32)
     h["out_pid"] = buf[h["off_out_pid"]:h["off_out_pid"] + 4 * h["n_out"]].view(np.uint32)
     h["root"] = buf[h["off_root"]:h["off_root"] + 1024].view(np.uint32)
     nbits = 1 << h["filter_log2_bits"]
     h["filter"] = buf[h["off_filter"]:h["off_filter"] + max(4, nbits // 8)].view(np.uint32)
+    nw = (N + 31) // 32
+    h["tail_bits"] = buf[h["off_tail_bits"]:h["off_tail_bits"] + 4 * nw].view(np.uint32)
+    h["tail_rank"] = buf[h["off_tail_rank"]:h["off_tail_rank"] + 4 * nw].view(np.uint32)
+    h["tails"] = buf[h["off_tails"]:h["off_tails"] + 16 * h["n_tails"]].view(np.uint32).reshape(-1, 4)
+    h["tail_bytes"] = buf[h["off_tail_bytes"]:h["off_tail_bytes"] + h["n_tail_bytes"]]
+    h["level1"] = buf[h["off_level1"]:h["off_level1"] + 40 * h["n_level1"]].view(np.uint32).reshape(-1, 10)
     return h
+
+
+def tail_index(h, v):
+    w = int(h["tail_bits"][v >> 5])
+    return int(h["tail_rank"][v >> 5]) + bin(w & ((1 << (v & 31)) - 1)).count("1")
 
 
 def filter_bits(h, key):
@@ -51,12 +65,52 @@ def filter_index(h, key):
     return ((key * h["filter_mul"]) & 0xFFFFFFFF) >> (32 - h["filter_log2_bits"])
 
 
+def term_of(h, last):
+    if last is None:
+        return None
+    k = int(np.searchsorted(h["term_node"], last))
+    assert h["term_node"][k] == last
+    return k
+
+
+def walk(h, text, i, L):
+    """Terminal index of the deepest terminal passed by the walk from start i."""
+    node, label = h["node"], h["label"]
+    v = int(h["root"][text[i]])
+    if v == 0:
+        return None
+    last = v if node[v] & TERM else None
+    j = i + 1
+    while j < L:
+        if node[v] & TAIL:  # path-compressed tail: compare its bytes at once
+            off, ln, ti, _ = (int(x) for x in h["tails"][tail_index(h, v)])
+            if j + ln <= L and bytes(text[j:j + ln]) == h["tail_bytes"][off:off + ln].tobytes():
+                return ti
+            return term_of(h, last)
+        s, e = int(node[v]) & MASK, int(node[v + 1]) & MASK
+        if 1 <= v <= h["n_level1"]:  # level 1: the bitmapped node (PAPER.md:97)
+            bm = [int(x) for x in h["level1"][v - 1]]
+            c = text[j]
+            if not (bm[c >> 5] >> (c & 31)) & 1:
+                break
+            pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFF
+            v = s + pre + bin(bm[c >> 5] & ((1 << (c & 31)) - 1)).count("1") + 1
+        else:
+            labs = label[s:e]
+            k = np.searchsorted(labs, text[j])
+            if k >= len(labs) or labs[k] != text[j]:
+                break
+            v = s + int(k) + 1
+        if node[v] & TERM:
+            last = v
+        j += 1
+    return term_of(h, last)
+
+
 def match(h, text: bytes, readable=None, n_starts=None):
     """Rows (pos, pid) per the image: filter test, then walk to the deepest terminal."""
     L = len(text) if readable is None else readable
     ns = L if n_starts is None else n_starts
-    node, label = h["node"], h["label"]
-    term = {int(v): i for i, v in enumerate(h["term_node"])}
     d = h["filter_gram"]
     rows = []
     for i in range(ns):
@@ -64,23 +118,8 @@ def match(h, text: bytes, readable=None, n_starts=None):
             continue
         if not filter_pass(h, int.from_bytes(text[i:i + d], "little")):
             continue
-        v = int(h["root"][text[i]])
-        if v == 0:
-            continue
-        last = v if node[v] & TERM else None
-        j = i + 1
-        while j < L:
-            s, e = int(node[v]) & MASK, int(node[v + 1]) & MASK
-            labs = label[s:e]
-            k = np.searchsorted(labs, text[j])
-            if k >= len(labs) or labs[k] != text[j]:
-                break
-            v = s + int(k) + 1
-            if node[v] & TERM:
-                last = v
-            j += 1
-        if last is not None:
-            t = term[last]
-            for r in range(int(h["out_ptr"][t]), int(h["out_ptr"][t + 1])):
+        ti = walk(h, text, i, L)
+        if ti is not None:
+            for r in range(int(h["out_ptr"][ti]), int(h["out_ptr"][ti + 1])):
                 rows.append((i, int(h["out_pid"][r])))
     return rows

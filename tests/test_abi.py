@@ -61,7 +61,8 @@ def test_stats_and_bytes_match_oracle(cid):
     assert t.nbytes("uncompressed") == o.bytes("uncompressed") == 36 * st["nodes"]
     assert t.nbytes("dense_stt") == o.bytes("dense_stt")
     assert t.nbytes("paper_crs") == o.bytes("paper_crs")
-    assert t.nbytes("csr_core") == 4 * (st["nodes"] + 1) + st["edges"]
+    assert st["image_nodes"] <= st["nodes"]
+    assert t.nbytes("csr_core") <= 4 * (st["nodes"] + 1) + st["edges"] or cid == 1
     assert t.nbytes("device_image") < t.nbytes("uncompressed") or cid == 1
     assert t.nbytes("device_image") == len(t.image())
 
@@ -74,15 +75,23 @@ def test_image_interpreter_toy(golden):
         assert image_walker.match(h, e["text"].encode()) == [tuple(r) for r in e["expect"]], e["cite"]
 
 
-def test_image_layout_toy(golden):
-    g = golden("toy_trie.json")
-    h = image_walker.parse(pf.Trie([p.encode() for p in g["patterns"]]).image())
-    row_ptr = [int(x) & image_walker.MASK for x in h["node"]]
-    assert row_ptr == g["csr_row_ptr"]
-    assert bytes(h["label"]) == g["csr_labels"].encode()
-    terms = [v for v in range(g["nodes"]) if h["node"][v] & image_walker.TERM]
-    assert terms == sorted(int(k) for k in g["terminals"])
-    assert list(h["term_node"]) == terms
+def test_image_layout_toy():
+    """Path-compressed image of {he, she, his, hers}, derived by hand from the
+    layout documented in csrc/image.h: 's'->"he" and 'he'->"rs" are tails
+    (single paths of 2 bytes ending at one terminal); 'hi'->'s' (1 byte) is not."""
+    t = pf.Trie([b"he", b"she", b"his", b"hers"])
+    h = image_walker.parse(t.image())
+    M, TE, TA = image_walker.MASK, image_walker.TERM, image_walker.TAIL
+    assert t.stats()["nodes"] == 10 and t.stats()["image_nodes"] == 6
+    assert [int(x) & M for x in h["node"]] == [0, 2, 4, 4, 4, 5, 5]
+    assert bytes(h["label"]) == b"hseis"
+    flags = [(bool(int(x) & TE), bool(int(x) & TA)) for x in h["node"][:6]]
+    assert flags == [(False, False), (False, False), (False, True), (True, True), (False, False), (True, False)]
+    assert list(h["term_node"]) == [3, 5] and h["n_terminals"] == 4
+    assert [tuple(int(y) for y in x[:3]) for x in h["tails"]] == [(0, 2, 2), (4, 2, 3)]
+    assert h["tail_bytes"][:8].tobytes() == b"he\x00\x00rs\x00\x00"
+    outs = [h["out_pid"][h["out_ptr"][k]:h["out_ptr"][k + 1]].tolist() for k in range(4)]
+    assert outs == [[0], [2], [1], [0, 3]]  # he, his, she, hers (+ its prefix he)
     assert h["filter_gram"] == 2 and h["filter_exact"] == 1
 
 
