@@ -22,6 +22,10 @@ oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
 $(PKG)/libpfac.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) -lcudart
 
+# instrumented build for tools/timing.py (not used by tests or bench)
+$(PKG)/libpfac_timing.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -shared -o $@ $(CSRC) -lcudart
+
 clean:
 	rm -f gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so
 

@@ -22,7 +22,7 @@ import numpy as np
 __all__ = ["Trie", "Scanner", "PfacError", "BYTES_KINDS", "lib_path", "launches_per_call"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libpfac.so")
+lib_path = os.environ.get("PFAC_LIB") or os.path.join(_HERE, "libpfac.so")  # PFAC_LIB: instrumented build
 
 PFAC_OK = 0
 _STATUS = {0: "PFAC_OK", 1: "PFAC_ERR_INVALID_ARG", 2: "PFAC_ERR_LIMIT", 3: "PFAC_ERR_NOMEM",

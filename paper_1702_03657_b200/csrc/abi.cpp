@@ -241,8 +241,7 @@ pfac_status pfac_match_device(const pfac_trie *t, int device, const uint8_t *d_t
     if (s != PFAC_OK) return s;
     DevTrie dt = make_dev_trie(t->hdr, d_img);
     std::string err;
-    const uint32_t *host_node = reinterpret_cast<const uint32_t *>(t->image.data() + t->hdr.off_node);
-    int st = launch_scan(dt, host_node, device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
+    int st = launch_scan(dt, t->image.data(), device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
                          d_workspace, workspace_bytes, reinterpret_cast<CUstream_st *>(stream), err);
     if (st != kStatusOk) return fail(st, err);
     return PFAC_OK;
@@ -369,5 +368,10 @@ const char *pfac_status_string(pfac_status s) {
 const char *pfac_last_error(void) { return g_err.c_str(); }
 
 const char *pfac_version(void) { return "pfac-b200 0.1 sm_100a"; }
+
+#ifdef PFAC_TIMING
+// Instrumented build only: copy the per-warp stamps of the last launch.
+int pfac_debug_timing(unsigned long long *host, uint64_t n) { return pfac::debug_timing(host, n); }
+#endif
 
 }  // extern "C"

@@ -59,10 +59,13 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d_image);
 int workspace_bytes_for(uint64_t n_starts, int device, uint64_t *out, std::string &err);
 
 // Launches the scan; returns kStatusOk or kStatusCuda (err filled).
-int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const uint8_t *d_text, uint64_t readable_len, uint64_t n_starts,
+int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const uint8_t *d_text, uint64_t readable_len, uint64_t n_starts,
                 uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity, uint64_t *d_count,
                 void *d_ws, uint64_t ws_bytes, CUstream_st *stream, std::string &err);
 
 uint32_t launches_per_call();
+#ifdef PFAC_TIMING
+int debug_timing(unsigned long long *host, uint64_t n);
+#endif
 
 }  // namespace pfac

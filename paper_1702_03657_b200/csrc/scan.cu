@@ -46,8 +46,10 @@ constexpr int kWarps = 16;
 constexpr int kThreads = kWarps * 32;
 constexpr int kPerLane = 32;           // consecutive starts per lane per round
 constexpr int kRound = 32 * kPerLane;  // 1024 starts per warp round
-constexpr int kSlots = 4;              // text ring depth per warp
+constexpr int kSlots = 4;              // text ring depth per warp (power of two)
+constexpr int kGroup = 2;              // rounds per survivor-compaction/walk pass
 constexpr int kSlotBytes = kRound;     // one round of text per slot
+static_assert(kSlotBytes == 1024 && (kSlots & (kSlots - 1)) == 0, "ring indexing uses shifts");
 constexpr int kMaxCtas = 1024;
 constexpr int kQueue = 64;             // per-warp survivor queue (u16 round offsets)
 
@@ -80,6 +82,9 @@ struct ScanArgs {
     uint32_t filter_words;          // words of the (unreplicated) filter
     uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
     uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_queue;
+    uint32_t off_tbits, off_trank, off_tails, off_tbytes;
+    uint32_t hot_tails, hot_tail_bytes, hot_words;  // tails of nodes < H; bitmap words ceil(H/32)
+    uint32_t off_terms;             // out_ptr[T+1] + term_node[TK] in smem (0 = in global memory)
     uint32_t n_level1;              // B: the root's children are nodes [1, B]
     uint32_t hot_nodes;             // H: node words [0, H] resident
     uint32_t hot_edges;             // row_ptr[H]: labels [0, hot_edges) resident
@@ -143,13 +148,27 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int *p) {
     return v;
 }
 
+#ifdef PFAC_TIMING
+// Instrumented build only (tools/timing.py): per-warp %globaltimer stamps.
+__device__ unsigned long long g_pfac_timing[2048 * 8];
+__device__ __forceinline__ void stamp(int warp_global, int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if ((threadIdx.x & 31) == 0 && warp_global < 2048) g_pfac_timing[warp_global * 8 + k] = t;
+}
+#define STAMP(k) stamp((int)(blockIdx.x * kWarps + (threadIdx.x >> 5)), k)
+#else
+#define STAMP(k)
+#endif
+
 // One barrier across the (co-resident, cooperative-launch) grid.
 __device__ __forceinline__ void grid_barrier(unsigned int *ctr) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(ctr, 1u);
-        while (ld_acquire_u32(ctr) < gridDim.x) __nanosleep(64);
+        while (ld_acquire_u32(ctr) < gridDim.x) {
+        }
     }
     __syncthreads();
 }
@@ -167,11 +186,16 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, int lane, uint32_
 
 // ------------------------------------------------------------ trie access
 struct Smem {
-    uint32_t filter_base;    // smem byte address of the filter (0) | lane's copy
-    const uint32_t *root;    // level-1 table: child of the root per byte
-    const uint32_t *bm;      // level-1 bitmapped nodes, 10 words each (see below)
-    const uint32_t *node;    // node words [0, H]
-    const uint8_t *label;    // labels [0, hot_edges)
+    const uint32_t *root;       // level-1 table: child of the root per byte
+    const uint32_t *bm;         // level-1 bitmapped nodes, 10 words each (see below)
+    const uint32_t *node;       // node words [0, H]
+    const uint8_t *label;       // labels [0, hot_edges)
+    const uint32_t *tail_bits;  // tail-start bitmap / rank words for nodes [0, H)
+    const uint32_t *tail_rank;
+    const uint4 *tails;         // tail records [0, hot_tails)
+    const uint8_t *tail_bytes;  // their bytes [0, hot_tail_bytes)
+    const uint32_t *out_ptr;    // pid-list offsets by terminal index (smem or global)
+    const uint32_t *term_node;  // kept terminal node ids (smem or global)
 };
 
 __device__ __forceinline__ uint32_t node_word(const ScanArgs &a, const Smem &s, uint32_t v) {
@@ -185,25 +209,21 @@ __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, u
 // warp's ring when the offset lies in it, else from global memory.
 // `end` = readable bytes from that position (clamped to 32 bits).
 struct RingText {
-    const uint8_t *p0, *p1;  // current slot and the next slot of the stream
-    uint32_t span;           // contiguous ring bytes from p0 (1 or 2 slots)
-    uint32_t end;
-    const uint8_t *g;        // text + position of p0[0]
+    const uint8_t *ring;  // this warp's ring (kSlots slots of kSlotBytes)
+    uint32_t s0;          // slot holding the first round of the window
+    uint32_t span;        // resident bytes from the window start (whole rounds)
+    uint32_t end;         // readable bytes from the window start
+    const uint8_t *g;     // text + window start
     __device__ __forceinline__ uint32_t at(uint32_t r) const {
-        if (r < span) return r < (uint32_t)kSlotBytes ? p0[r] : p1[r - kSlotBytes];
+        if (r < span) return ring[(((s0 + (r >> 10)) & (kSlots - 1)) << 10) | (r & 1023u)];
         return __ldg(g + r);
+    }
+    __device__ __forceinline__ uint32_t word(uint32_t i) const {  // aligned word i of the window
+        return reinterpret_cast<const uint32_t *>(ring)[(((s0 + (i >> 8)) & (kSlots - 1)) << 8) | (i & 255u)];
     }
     // 4 bytes at offset r (little-endian; bytes past `end` are unspecified)
     __device__ __forceinline__ uint32_t at4(uint32_t r) const {
-        if (r + 4 <= span) {
-            const uint32_t i = r >> 2;  // aligned words i, i+1 of the 1-2 slot window
-            const uint32_t *w0 = reinterpret_cast<const uint32_t *>(p0);
-            const uint32_t *w1 = reinterpret_cast<const uint32_t *>(p1);
-            constexpr uint32_t kW = kSlotBytes / 4;
-            const uint32_t lo = i < kW ? w0[i] : w1[i - kW];
-            const uint32_t hi = (i + 1) < kW ? w0[i + 1] : ((i + 1 - kW) < kW ? w1[i + 1 - kW] : 0u);
-            return __funnelshift_r(lo, hi, 8 * (r & 3));
-        }
+        if (r + 4 <= span) return __funnelshift_r(word(r >> 2), word((r >> 2) + 1), 8 * (r & 3));
         uint32_t x = 0;
         for (int b = 0; b < 4; ++b)
             if (r + b < end) x |= at(r + b) << (8 * b);
@@ -227,35 +247,37 @@ struct GlobalText {
 // [1, B]) uses the paper's bitmapped node (Fig. 3: 256-bit child
 // bitmap + offset, child = offset + rank of c among the set bits); deeper
 // nodes use the CSR label list of the image.
-// Tail jump at tail-start node v with the next text byte at offset j: the
-// rest of the trie below v is one path of L bytes ending at a terminal, so it
-// matches iff the next L text bytes equal the path's labels.
-__device__ __forceinline__ uint32_t term_index(const DevTrie &t, uint32_t v) {
-    uint32_t lo = 0, hi = t.n_kept_terminals;
+// Terminal index of kept terminal node v: binary search in term_node (shared
+// memory when staged, else global; plain loads through a generic pointer).
+__device__ __forceinline__ uint32_t term_index(const uint32_t *term_node, uint32_t n, uint32_t v) {
+    uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(t.term_node + mid) < v) lo = mid + 1; else hi = mid;
+        if (term_node[mid] < v) lo = mid + 1; else hi = mid;
     }
     return lo;
 }
-// terminal index of node `last` (kNone stays kNone)
-__device__ __forceinline__ uint32_t term_of(const DevTrie &t, uint32_t last) {
-    return last == kNone ? kNone : term_index(t, last);
-}
+// terminal index of node `last` (kNone stays kNone); needs `a` and `s` in scope
+#define term_of(last_) ((last_) == kNone ? kNone : term_index(s.term_node, a.t.n_kept_terminals, (last_)))
 
 // Tail jump at tail-start node v with the next text byte at offset j: below v
 // the trie is one path of L bytes ending at a terminal, so it matches iff the
 // next L text bytes equal the path's bytes.  Returns a terminal index.
 template <class Text>
-__device__ __forceinline__ uint32_t tail_jump(const ScanArgs &a, const Text &tx, uint32_t v, uint32_t j, uint32_t last) {
-    const uint32_t idx = __ldg(a.t.tail_rank + (v >> 5)) + __popc(__ldg(a.t.tail_bits + (v >> 5)) & ((1u << (v & 31)) - 1u));
-    const uint4 rec = __ldg(a.t.tails + idx);
-    if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(a.t, last);
-    const uint32_t *pw = reinterpret_cast<const uint32_t *>(a.t.tail_bytes + rec.x);  // 4-byte aligned
+__device__ __forceinline__ uint32_t tail_jump(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t v, uint32_t j,
+                                              uint32_t last) {
+    const bool hot = v < a.hot_nodes;  // hot tails (records + bytes) are in shared memory
+    const uint32_t below = (1u << (v & 31)) - 1u;
+    const uint32_t idx = hot ? s.tail_rank[v >> 5] + __popc(s.tail_bits[v >> 5] & below)
+                             : __ldg(a.t.tail_rank + (v >> 5)) + __popc(__ldg(a.t.tail_bits + (v >> 5)) & below);
+    const uint4 rec = hot ? s.tails[idx] : __ldg(a.t.tails + idx);
+    if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(last);
+    const uint32_t *pw = reinterpret_cast<const uint32_t *>((hot ? s.tail_bytes : a.t.tail_bytes) + rec.x);
     for (uint32_t k = 0; k < rec.y; k += 4) {
         const uint32_t n = rec.y - k;
         const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
-        if ((tx.at4(j + k) ^ __ldg(pw + (k >> 2))) & m) return term_of(a.t, last);
+        const uint32_t pwk = hot ? pw[k >> 2] : __ldg(pw + (k >> 2));
+        if ((tx.at4(j + k) ^ pwk) & m) return term_of(last);
     }
     return rec.z;
 }
@@ -267,13 +289,13 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
     uint32_t w = node_word(a, s, v);
     uint32_t last = (w & kTermBit) ? v : kNone;
     uint32_t j = r0 + 1;
-    if (j >= tx.end) return term_of(a.t, last);
-    if (w & kTailBit) return tail_jump(a, tx, v, j, last);
+    if (j >= tx.end) return term_of(last);
+    if (w & kTailBit) return tail_jump(a, s, tx, v, j, last);
     {   // level 1 -> 2 through the bitmap
         const uint32_t c = tx.at(j);
         const uint32_t *bm = s.bm + (v - 1) * 10;
         const uint32_t word = bm[c >> 5];
-        if (!((word >> (c & 31)) & 1u)) return term_of(a.t, last);
+        if (!((word >> (c & 31)) & 1u)) return term_of(last);
         const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
         v = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
         w = node_word(a, s, v);
@@ -281,7 +303,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
         ++j;
     }
     for (; j < tx.end; ++j) {
-        if (w & kTailBit) return tail_jump(a, tx, v, j, last);
+        if (w & kTailBit) return tail_jump(a, s, tx, v, j, last);
         const uint32_t lo0 = w & kEdgeMask;
         const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
         if (lo0 == hi0) break;  // leaf
@@ -308,7 +330,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
         w = node_word(a, s, v);
         if (w & kTermBit) last = v;
     }
-    return term_of(a.t, last);
+    return term_of(last);
 }
 
 __device__ __forceinline__ uint32_t clamp32(uint64_t x) { return x > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)x; }
@@ -333,8 +355,8 @@ __device__ __forceinline__ uint2 lds64_abs(uint32_t addr) {
     return v;
 }
 template <int Kind>
-__device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[9], uint32_t sW, uint32_t stride,
-                                             uint32_t base_lane) {
+__device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[9], uint32_t sW, uint32_t sWmul,
+                                             uint32_t stride, uint32_t base_lane) {
     uint32_t surv = 0;
     if (Kind == 1) {
         constexpr uint32_t kMul = kFilterMul << 8;
@@ -344,14 +366,19 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
             x[k] = (k & 3) ? __funnelshift_r(wv[k >> 2], wv[(k >> 2) + 1], 8 * (k & 3)) : wv[k >> 2];
         x[kPerLane + 1] = x[kPerLane - 1] >> 16;  // byte 33 in the low bits
         x[kPerLane + 2] = x[kPerLane - 1] >> 24;  // byte 34
+        // four independent accumulation chains of 8 starts (short dependency
+        // chains); the block index uses IMAD.HI (a right shift on the FMA pipe,
+        // which the ALU-heavy bit test leaves idle): hi32(h * 2^(32-sW)) = h >> sW
+        uint32_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = kPerLane - 1; k >= 0; --k) {
-            const uint32_t blk = (x[k] * kMul) >> sW;
+            const uint32_t blk = __umulhi(x[k] * kMul, sWmul);
             const uint2 w2 = lds64_abs(blk * stride + base_lane);
             // rotate by byte k+3 / byte k+2 (funnel amounts are mod 32): tested bits -> 31
             const uint32_t r = __funnelshift_l(w2.x, w2.x, x[k + 3]) & __funnelshift_l(w2.y, w2.y, x[k + 2]);
-            surv = __funnelshift_l(r, surv, 1);  // surv << 1 | bit
+            acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);  // acc << 1 | bit
         }
+        surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
     } else {
         const uint32_t gram = a.t.gram;
         const uint32_t kmask = (1u << (8 * gram)) - 1u;
@@ -380,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
     uint16_t *queue = reinterpret_cast<uint16_t *>(smem + a.off_queue) + warp * kQueue;
 
+    STAMP(0);
     // ---- barriers: per-warp text ring + one for the table staging
     uint64_t *sbar = reinterpret_cast<uint64_t *>(smem + a.off_bar) + kWarps * kSlots;
     if (lane < kSlots) mbar_init(&bars[lane], 1);
@@ -388,11 +416,17 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;  // for the next launch
     __syncthreads();
     Smem s;
-    s.filter_base = 0;
+    // terminal tables: shared-memory copies when staged (generic pointers)
+    s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem + a.off_terms) : a.t.out_ptr;
+    s.term_node = a.off_terms ? s.out_ptr + a.t.n_terminals + 1 : a.t.term_node;
     s.root = s_root;
     s.bm = s_bm;
     s.node = s_node;
     s.label = s_label;
+    s.tail_bits = reinterpret_cast<const uint32_t *>(smem + a.off_tbits);
+    s.tail_rank = reinterpret_cast<const uint32_t *>(smem + a.off_trank);
+    s.tails = reinterpret_cast<const uint4 *>(smem + a.off_tails);
+    s.tail_bytes = smem + a.off_tbytes;
     // filter addressing: copies interleaved at the unit the kernel loads
     // (kind 1: 8-byte block b of copy r at filter + 8*(b*rep + r); kind 0:
     // word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
@@ -400,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     const uint32_t rep = 1u << a.rep_log2;
     const uint32_t unit = Kind == 1 ? 8u : 4u;
     const uint32_t sW = 32u - (a.t.log2_bits - (Kind == 1 ? 6u : 5u));  // block index = hash >> sW
+    const uint32_t sWmul = 1u << (32u - sW);                              // (hash * sWmul) >> 32 == hash >> sW
     const uint32_t stride = rep * unit;
     const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
 
@@ -442,90 +477,113 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     // ---- start streaming this warp's text, then stage the tables (TMA bulk
     // copies of the image sections; the filter is replicated from 16-byte loads)
     const uint64_t nr = r_end - r_begin;
-    for (uint64_t i = 0; i < nr && i < kSlots - 1; ++i) issue(i);
+    for (uint64_t i = 0; i < nr && i < kSlots - kGroup; ++i) issue(i);
     if (tid == 0) {
         const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
                        nb_l1 = align16(40 * a.n_level1);
-        mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1);
+        const uint32_t nb_w = align16(4 * a.hot_words), nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
+        mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1 + 2 * nb_w + nb_t + nb_tb);
         bulk_g2s(s_root, a.t.root, 1024, sbar, policy_last);
         bulk_g2s(s_node, a.t.node, nb_node, sbar, policy_last);
         if (nb_label) bulk_g2s(s_label, a.t.label, nb_label, sbar, policy_last);
         bulk_g2s(s_bm, a.t.level1, nb_l1, sbar, policy_last);
+        if (nb_w) {
+            bulk_g2s(smem + a.off_tbits, a.t.tail_bits, nb_w, sbar, policy_last);
+            bulk_g2s(smem + a.off_trank, a.t.tail_rank, nb_w, sbar, policy_last);
+        }
+        if (nb_t) bulk_g2s(smem + a.off_tails, a.t.tails, nb_t, sbar, policy_last);
+        if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, policy_last);
     }
-    {
-        const uint4 *src = reinterpret_cast<const uint4 *>(a.t.filter);
-        const uint32_t nvec = (a.filter_words + 3) / 4;
-        for (uint32_t i = tid; i < nvec; i += kThreads) {
-            const uint4 v = __ldg(src + i);
-            if (Kind == 1) {  // two 8-byte blocks, each copied rep times
-                uint2 *d = reinterpret_cast<uint2 *>(s_filter) + (2 * i) * rep;
-                for (uint32_t r = 0; r < rep; ++r) {
-                    d[r] = make_uint2(v.x, v.y);
-                    d[rep + r] = make_uint2(v.z, v.w);
-                }
-            } else {  // four words, each copied rep times
-                uint32_t *d = s_filter + (4 * i) * rep;
-                for (uint32_t r = 0; r < rep; ++r) {
-                    d[r] = v.x;
-                    d[rep + r] = v.y;
-                    d[2 * rep + r] = v.z;
-                    d[3 * rep + r] = v.w;
-                }
-            }
+    {   // replicate the filter: destination unit j holds source unit j >> rep_log2
+        // (consecutive threads write consecutive units: no bank conflicts)
+        const uint32_t nu = (Kind == 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
+        if (Kind == 1) {
+            const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
+            uint2 *d = reinterpret_cast<uint2 *>(s_filter);
+            for (uint32_t j = tid; j < nu; j += kThreads) d[j] = __ldg(src + (j >> a.rep_log2));
+        } else {
+            for (uint32_t j = tid; j < nu; j += kThreads) s_filter[j] = __ldg(a.t.filter + (j >> a.rep_log2));
+        }
+        // terminal tables (pid-list offsets, kept terminal ids) when small
+        if (a.off_terms) {
+            uint32_t *so = reinterpret_cast<uint32_t *>(smem + a.off_terms);
+            const uint32_t n_op = a.t.n_terminals + 1;
+            for (uint32_t j = tid; j < n_op; j += kThreads) so[j] = __ldg(a.t.out_ptr + j);
+            for (uint32_t j = tid; j < a.t.n_kept_terminals; j += kThreads) so[n_op + j] = __ldg(a.t.term_node + j);
         }
     }
     mbar_wait(sbar, 0);
     __syncthreads();
+    STAMP(1);
 
     // ================================================= phase 1: scan
+    // Groups of kGroup rounds: stage 1 on each round, then one compaction +
+    // walk pass for the group's survivors (amortises the pass overhead).  The
+    // ring keeps the group + one round of look-ahead resident while the rest
+    // of the ring is in flight.
     uint32_t c = 0;       // pattern ids matched by this lane's starts
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
-    for (uint64_t i = 0; i < nr; ++i) {
-        if (i + kSlots - 1 < nr) issue(i + kSlots - 1);  // refills the slot of round i-1
-        const uint32_t slot = (uint32_t)(i % kSlots);
-        mbar_wait(&bars[slot], (uint32_t)((i / kSlots) & 1));
-        const bool has_next = i + 1 < nr;
-        const uint32_t slot1 = (uint32_t)((i + 1) % kSlots);
-        if (has_next) mbar_wait(&bars[slot1], (uint32_t)(((i + 1) / kSlots) & 1));
-        const uint8_t *p0 = ring + slot * kSlotBytes;
-        const uint8_t *p1 = ring + slot1 * kSlotBytes;
-        const uint64_t rbase = (r_begin + i) * kRound;
-        const RingText tx{p0, p1, has_next ? (uint32_t)(2 * kSlotBytes) : (uint32_t)kSlotBytes,
-                          clamp32(a.readable - rbase), a.text + rbase};
+    for (uint64_t i = 0; i < nr; i += kGroup) {
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g)  // refill the slots of the previous group
+            if (i + kSlots - kGroup + g < nr) issue(i + kSlots - kGroup + g);
+        const uint32_t ng = nr - i < (uint64_t)kGroup ? (uint32_t)(nr - i) : (uint32_t)kGroup;
+        const uint32_t nres = nr - i < (uint64_t)(ng + 1) ? (uint32_t)(nr - i) : ng + 1;
+        for (uint32_t q = 0; q < nres; ++q) mbar_wait(&bars[(i + q) % kSlots], (uint32_t)(((i + q) / kSlots) & 1));
+        const uint64_t gbase = (r_begin + i) * kRound;
+        const RingText tx{ring, (uint32_t)(i % kSlots), nres * (uint32_t)kSlotBytes, clamp32(a.readable - gbase),
+                          a.text + gbase};
 
-        // ---- stage 1: filter over the lane's 32 starts
-        const uint4 q0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane);
-        const uint4 q1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16);
-        uint32_t w8 = __shfl_down_sync(0xffffffffu, q0.x, 1);
-        if (lane == 31) {
-            if (has_next) {
-                w8 = *reinterpret_cast<const uint32_t *>(p1);
-            } else {
-                w8 = 0;
-                const uint64_t j0 = rbase + kRound;
-                for (int b = 0; b < 4; ++b)
-                    if (j0 + b < a.readable) w8 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
+        // ---- stage 1: filter over the lane's 32 starts of each round
+        uint32_t surv[kGroup];
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+            surv[g] = 0;
+            if ((uint32_t)g < ng) {
+                const uint8_t *p0 = ring + ((i + g) % kSlots) * kSlotBytes;
+                const uint4 q0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane);
+                const uint4 q1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16);
+                uint32_t w8 = __shfl_down_sync(0xffffffffu, q0.x, 1);
+                const uint64_t rbase = gbase + (uint64_t)g * kRound;
+                if (lane == 31) {
+                    if ((uint32_t)g + 1 < nres) {
+                        w8 = *reinterpret_cast<const uint32_t *>(ring + ((i + g + 1) % kSlots) * kSlotBytes);
+                    } else {
+                        w8 = 0;
+                        const uint64_t j0 = rbase + kRound;
+                        for (int b = 0; b < 4; ++b)
+                            if (j0 + b < a.readable) w8 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
+                    }
+                }
+                const uint32_t wv[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, w8};
+                const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
+                surv[g] = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
+                if (lbase + kPerLane > lim) {
+                    const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
+                    surv[g] &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
+                }
             }
         }
-        const uint32_t wv[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, w8};
-        const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
-        uint32_t surv = filter32<Kind>(a, wv, sW, stride, base_lane);
-        if (lbase + kPerLane > lim) {
-            const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
-            surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
-        }
 
-        // ---- stage 2: compact survivors into the warp queue, walk with full warps
-        if (__any_sync(0xffffffffu, surv != 0)) {
-            const uint32_t ns = __popc(surv);
-            uint32_t stot;
-            const uint32_t sex = warp_excl_scan(ns, lane, &stot);
+        // ---- stage 2: compact survivors (position order: round, lane, start)
+        // into the warp queue, walk them with full warps
+        static_assert(kGroup == 2, "packed two-round scan below");
+        const uint32_t ns0 = __popc(surv[0]), ns1 = __popc(surv[1]);
+        if (__any_sync(0xffffffffu, (ns0 | ns1) != 0)) {
+            uint32_t tot;
+            const uint32_t ex = warp_excl_scan(ns0 | (ns1 << 16), lane, &tot);  // both rounds in one scan
+            const uint32_t t0 = tot & 0xFFFFu, stot = t0 + (tot >> 16);
+            const uint32_t st[2] = {ex & 0xFFFFu, t0 + (ex >> 16)};
             for (uint32_t qb = 0; qb < stot; qb += kQueue) {
-                if (ns && sex < qb + kQueue && sex + ns > qb) {
-                    uint32_t idx = sex;
-                    for (uint32_t m = surv; m; m &= m - 1, ++idx)
-                        if (idx >= qb && idx < qb + kQueue)
-                            queue[idx - qb] = (uint16_t)(lane * kPerLane + (__ffs(m) - 1));
+#pragma unroll
+                for (int g = 0; g < kGroup; ++g) {
+                    const uint32_t ns = g == 0 ? ns0 : ns1;
+                    if (ns && st[g] < qb + kQueue && st[g] + ns > qb) {
+                        uint32_t idx = st[g];
+                        for (uint32_t m = surv[g]; m; m &= m - 1, ++idx)
+                            if (idx >= qb && idx < qb + kQueue)
+                                queue[idx - qb] = (uint16_t)(g * kRound + lane * kPerLane + (__ffs(m) - 1));
+                    }
                 }
                 __syncwarp();
                 const uint32_t n = stot - qb < (uint32_t)kQueue ? stot - qb : (uint32_t)kQueue;
@@ -535,14 +593,14 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
                     if (j < n) {
                         off = queue[j];
                         tn = walk(a, s, tx, off);  // terminal index
-                        if (tn != kNone) c += __ldg(a.t.out_ptr + tn + 1) - __ldg(a.t.out_ptr + tn);
+                        if (tn != kNone) c += s.out_ptr[tn + 1] - s.out_ptr[tn];
                     }
                     const bool hit = tn != kNone;
                     // hits in queue order == position order
                     const uint32_t hb = __ballot_sync(0xffffffffu, hit);
                     if (hit) {
                         const uint32_t idx = n_hits + __popc(hb & ((1u << lane) - 1u));
-                        if (idx < a.hit_cap) hits[idx] = make_uint2((uint32_t)(rbase - range_lo) + off, tn);
+                        if (idx < a.hit_cap) hits[idx] = make_uint2((uint32_t)(gbase - range_lo) + off, tn);
                     }
                     n_hits += __popc(hb);
                 }
@@ -551,6 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
         }
         __syncwarp();
     }
+    STAMP(2);
     uint64_t total;
     {
         uint32_t ct;
@@ -592,9 +651,13 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     }
     __syncthreads();
     uint64_t off = s_wtot[kWarps] + s_wtot[warp];  // this warp's first output row
+    STAMP(3);
 
     // ================================================= phase 3: emit
-    if (total == 0) return;
+    if (total == 0) {
+        STAMP(4);
+        return;
+    }
     if (n_hits <= a.hit_cap) {
         for (uint32_t b = 0; b < n_hits; b += 32) {
             const uint32_t i = b + lane;
@@ -604,12 +667,12 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
                 const uint2 h = hits[i];
                 gi = range_lo + h.x;
                 ti = h.y;
-                cnt = __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
+                cnt = s.out_ptr[ti + 1] - s.out_ptr[ti];
             }
             uint32_t ctot;
             uint64_t o = off + warp_excl_scan(cnt, lane, &ctot);
             if (cnt) {
-                const uint32_t r0 = __ldg(a.t.out_ptr + ti);
+                const uint32_t r0 = s.out_ptr[ti];
                 for (uint32_t e = 0; e < cnt; ++e, ++o) {
                     if (o < a.capacity) {
                         a.out_pos[o] = a.pos_base + gi;
@@ -628,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             uint32_t wv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
             for (int b = 0; b < 36; ++b)
                 if (lbase + b < a.readable) wv[b >> 2] |= (uint32_t)__ldg(a.text + lbase + b) << (8 * (b & 3));
-            uint32_t surv = filter32<Kind>(a, wv, sW, stride, base_lane);
+            uint32_t surv = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
                 surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
@@ -639,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
                 const int k = __ffs(m) - 1;
                 const uint32_t ti = walk(a, s, gt, (uint32_t)k);
                 if (ti != kNone) {
-                    cc += __ldg(a.t.out_ptr + ti + 1) - __ldg(a.t.out_ptr + ti);
+                    cc += s.out_ptr[ti + 1] - s.out_ptr[ti];
                     hm |= 1u << k;
                 }
             }
@@ -648,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             for (uint32_t m = hm; m; m &= m - 1) {
                 const uint32_t k = (uint32_t)(__ffs(m) - 1);
                 const uint32_t ti = walk(a, s, gt, k);
-                const uint32_t r0 = __ldg(a.t.out_ptr + ti), r1 = __ldg(a.t.out_ptr + ti + 1);
+                const uint32_t r0 = s.out_ptr[ti], r1 = s.out_ptr[ti + 1];
                 for (uint32_t e = r0; e < r1; ++e, ++o) {
                     if (o < a.capacity) {
                         a.out_pos[o] = a.pos_base + lbase + k;
@@ -659,6 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
             off += ctot;
         }
     }
+    STAMP(4);
 }
 
 struct DeviceInfo {
@@ -758,7 +822,13 @@ int workspace_bytes_for(uint64_t n_starts, int device, uint64_t *out, std::strin
 
 uint32_t launches_per_call() { return 1; }  // the scan kernel
 
-int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const uint8_t *d_text,
+#ifdef PFAC_TIMING
+int debug_timing(unsigned long long *host, uint64_t n) {
+    return cudaMemcpyFromSymbol(host, g_pfac_timing, n * 8) == cudaSuccess ? 0 : -1;
+}
+#endif
+
+int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const uint8_t *d_text,
                 uint64_t readable_len, uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                 uint64_t capacity, uint64_t *d_count, void *d_ws, uint64_t ws_bytes, CUstream_st *stream_,
                 std::string &err) {
@@ -788,6 +858,8 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     // half of what the fixed parts leave), ring, barriers, queues, root,
     // level-1 bitmaps, warp totals, then the hot trie prefix.
     const uint32_t filter_words = (1u << t.log2_bits) >= 32 ? (1u << t.log2_bits) / 32 : 1u;
+    const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
+    const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + kWarps * kQueue * 2 + 1024 +
                            align16(40 * B) + 8 * (kWarps + 1) + 512;
@@ -797,18 +869,37 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     }
     const uint32_t rest = (uint32_t)di.max_smem_optin - fixed;
     uint32_t rep_log2 = 0;
-    while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= rest / 2) rep_log2++;
+    // the filter gets up to 64 KiB (replicas cut bank conflicts), the hot trie the rest
+    const uint32_t fcap = rest > 16384 + 65536 ? 65536u : (rest > 16384 ? rest - 16384 : rest / 2);
+    while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= fcap) rep_log2++;
     const uint32_t filter_bytes = filter_words * 4 << rep_log2;
     const uint32_t trie_budget = rest - filter_bytes;
-    // H = largest node count whose words [0, H] and labels [0, row_ptr[H]) fit
-    uint32_t lo = 0, hi = t.n_nodes - 1;
+    // H = largest BFS prefix whose node words [0, H], labels [0, row_ptr[H]),
+    // tail bitmap/rank words and tail records + bytes (tails of nodes < H)
+    // all fit the budget
+    const uint32_t *h_tbits = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_bits);
+    const uint32_t *h_trank = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_rank);
+    const uint32_t *h_tails = reinterpret_cast<const uint32_t *>(host_image + hh.off_tails);
+    auto tails_below = [&](uint32_t H) -> uint32_t {  // rank(H)
+        return h_trank[H >> 5] + (uint32_t)__builtin_popcount(h_tbits[H >> 5] & ((1u << (H & 31)) - 1u));
+    };
+    auto tbytes_below = [&](uint32_t nt) -> uint32_t {
+        return nt < hh.n_tails ? h_tails[4 * nt] : (uint32_t)hh.n_tail_bytes;
+    };
+    auto hot_bytes = [&](uint32_t H) -> uint64_t {
+        const uint32_t nt = tails_below(H);
+        return align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) + 2ull * align16(4 * ((H + 31) / 32)) +
+               16ull * nt + align16(tbytes_below(nt));
+    };
+    uint32_t lo = 1, hi = t.n_nodes - 1;
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        const uint64_t bytes = align16(4 * (mid + 1)) + align16(host_node[mid] & kEdgeMask);
-        if (bytes <= trie_budget) lo = mid; else hi = mid - 1;
+        if (hot_bytes(mid) <= trie_budget) lo = mid; else hi = mid - 1;
     }
     const uint32_t H = lo;
     const uint32_t EH = host_node[H] & kEdgeMask;
+    const uint32_t TH = tails_below(H);
+    const uint32_t TBH = tbytes_below(TH);
 
     ScanArgs a;
     a.t = t;
@@ -825,6 +916,22 @@ int launch_scan(const DevTrie &t, const uint32_t *host_node, int device, const u
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
     a.off_label = o;  o += align16(EH);
+    {   // terminal tables in smem when small and they fit what is left
+        const uint32_t tb = align16(4 * (uint32_t)(hh.n_terminals + 1 + hh.n_kept_terminals));
+        a.off_terms = 0;
+        if (hh.n_terminals + 1 + hh.n_kept_terminals < 8192 && o + align16(4 * (H + 1)) + align16(EH) + tb +
+            2 * align16(4 * ((H + 31) / 32)) + 16 * TH + align16(TBH) <= (uint32_t)di.max_smem_optin) {
+            a.off_terms = o;
+            o += tb;
+        }
+    }
+    a.off_tbits = o;  o += align16(4 * ((H + 31) / 32));
+    a.off_trank = o;  o += align16(4 * ((H + 31) / 32));
+    a.off_tails = o;  o += 16 * TH;
+    a.off_tbytes = o; o += align16(TBH);
+    a.hot_tails = TH;
+    a.hot_tail_bytes = TBH;
+    a.hot_words = (H + 31) / 32;
     const size_t smem = o;
     if (smem > (size_t)di.max_smem_optin) {
         err = "pfac_match_device: internal shared-memory plan error";
