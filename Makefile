@@ -26,6 +26,15 @@ $(PKG)/libpfac.so: $(CSRC) $(CHDR)
 $(PKG)/libpfac_timing.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -shared -o $@ $(CSRC) -lcudart
 
+$(PKG)/libpfac_stream.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_STREAM_ONLY -shared -o $@ $(CSRC) -lcudart
+
+$(PKG)/libpfac_exp1.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_EXP=1 -shared -o $@ $(CSRC) -lcudart
+
+$(PKG)/libpfac_exp2.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_EXP=2 -shared -o $@ $(CSRC) -lcudart
+
 clean:
 	rm -f gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so
 

@@ -13,6 +13,7 @@
 // order with children in ascending byte order -- exactly the row-major layout
 // whose child through edge e is node e+1.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -251,12 +252,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     const uint32_t gram = std::min<uint32_t>(4, min_len);
     uint32_t exact = gram <= 2 ? 1u : 0u;
     uint32_t log2_bits;
+    uint32_t kind = gram == 4 ? 1u : 0u;
     if (exact) {
         log2_bits = 8 * gram;
     } else {
-        // distinct d-grams -> ~32 filter bits per key (kind 0: ~3% false
-        // positives; kind 1, two bits per key in 64-bit blocks: ~0.5%),
-        // between 2^10 and 2^19 bits (64 KiB, the shared-memory budget)
         std::vector<uint32_t> keys(m);
         for (uint32_t k = 0; k < m; k++) {
             uint32_t x = 0;
@@ -264,17 +263,36 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
             keys[k] = x;
         }
         std::sort(keys.begin(), keys.end());
-        uint64_t distinct = std::unique(keys.begin(), keys.end()) - keys.begin();
-        log2_bits = 10;
-        while (log2_bits < 19 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+        const uint64_t distinct = std::unique(keys.begin(), keys.end()) - keys.begin();
+        // kind 2 (pair filter, d = 4): one bit per key and role, 2 keys/bit-set
+        // per 4-gram -> ~64 bits per 4-gram keeps the fill near 1.6%; used
+        // while that fits 2^18 bits.  Else kind 1 (blocked two-bit, ~32 bits
+        // per key, ~0.5% false positives) or kind 0 (d < 4, ~3%), capped at
+        // 2^19 bits (64 KiB, the shared-memory budget).
+        const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
+        const bool allow2 = !force || force[0] != '1';
+        if (kind == 1 && allow2 && distinct * 128 <= (1ull << 18)) {
+            kind = 2;
+            log2_bits = 12;
+            while ((1ull << log2_bits) < 128 * distinct) log2_bits++;
+        } else {
+            log2_bits = 10;
+            while (log2_bits < 19 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+        }
     }
     std::vector<uint32_t> filter((size_t)1 << (log2_bits - 5 > 0 ? log2_bits - 5 : 0), 0u);
     if (filter.empty()) filter.resize(1);
-    const uint32_t kind = gram == 4 ? 1u : 0u;
     for (uint32_t k = 0; k < m; k++) {
         uint32_t x = 0;
         for (uint32_t b = 0; b < gram; b++) x |= (uint32_t)pats[k][b] << (8 * b);
-        if (kind == 1) {
+        if (kind == 2) {
+            // as the first start of a pair: shared bytes are P[1..3], own byte P[0]
+            const uint32_t b1 = filter4_block(x >> 8, log2_bits);
+            filter[2 * b1] |= 1u << (31u - (x & 31u));
+            // as the second start: shared bytes are P[0..2], own byte P[3]
+            const uint32_t b2 = filter4_block(x, log2_bits);
+            filter[2 * b2 + 1] |= 1u << (31u - ((x >> 24) & 31u));
+        } else if (kind == 1) {
             const uint32_t b = filter4_block(x, log2_bits);
             filter[2 * b] |= 1u << filter4_bit_lo(x);
             filter[2 * b + 1] |= 1u << filter4_bit_hi(x);
@@ -369,7 +387,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
               in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && h.filter_gram <= 4 &&
               h.filter_gram <= h.min_len && h.min_len <= h.max_len && h.max_len <= kMaxPatternLen &&
-              h.filter_mul == kFilterMul && h.filter_kind == (h.filter_gram == 4 ? 1u : 0u) &&
+              h.filter_mul == kFilterMul && (h.filter_gram == 4 ? (h.filter_kind == 1 || h.filter_kind == 2) : h.filter_kind == 0) &&
               (h.filter_kind == 0 || h.filter_log2_bits >= 10) && in(h.off_tail_bits, 4 * ((N + 31) / 32)) &&
               in(h.off_tail_rank, 4 * ((N + 31) / 32)) && in(h.off_tails, 16 * h.n_tails) &&
               in(h.off_tail_bytes, h.n_tail_bytes) && in(h.off_level1, 40 * h.n_level1);

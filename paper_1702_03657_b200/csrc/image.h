@@ -50,6 +50,14 @@
 //                         31-(byte2 & 31) of word 2b+1 (bit-reversed so the
 //                         kernel tests each with one rotate; scan.cu stage 1).
 //                         A start passes iff both bits are set.
+//                       kind 2 (d = 4, small sets): the pair filter.  Starts k
+//                         and k+1 share bytes k+1..k+3, so one 64-bit block
+//                         b = filter4_block(bytes k+1..k+3) answers both: start
+//                         k passes iff bit 31-(byte k & 31) of word 2b is set,
+//                         start k+1 iff bit 31-(byte k+4 & 31) of word 2b+1 is
+//                         set.  A pattern 4-gram P sets word 2*block(P[1..3])
+//                         bit 31-(P[0]&31) and word 2*block(P[0..2])+1 bit
+//                         31-(P[3]&31).
 #pragma once
 #include <cstdint>
 

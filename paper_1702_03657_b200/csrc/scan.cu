@@ -42,16 +42,21 @@ namespace pfac {
 
 namespace {
 
-constexpr int kWarps = 16;
+constexpr int kWarps = 32;
 constexpr int kThreads = kWarps * 32;
-constexpr int kPerLane = 32;           // consecutive starts per lane per round
-constexpr int kRound = 32 * kPerLane;  // 1024 starts per warp round
+constexpr int kPerLane = 16;           // consecutive starts per lane per round
+constexpr int kRound = 32 * kPerLane;  // 512 starts per warp round
+constexpr int kWv = kPerLane / 4 + 1;  // text words a lane needs (its starts + 3 bytes)
 constexpr int kSlots = 4;              // text ring depth per warp (power of two)
 constexpr int kGroup = 2;              // rounds per survivor-compaction/walk pass
 constexpr int kSlotBytes = kRound;     // one round of text per slot
-static_assert(kSlotBytes == 1024 && (kSlots & (kSlots - 1)) == 0, "ring indexing uses shifts");
+constexpr int kSlotLog2 = 9;
+static_assert(kSlotBytes == (1 << kSlotLog2) && (kSlots & (kSlots - 1)) == 0, "ring indexing uses shifts");
 constexpr int kMaxCtas = 1024;
 constexpr int kQueue = 64;             // per-warp survivor queue (u16 round offsets)
+constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated filter
+constexpr uint32_t kHotCap = 24576;  // hot-trie smem when the trie does not fit (rest left to L1)
+constexpr int kDefer = 48;             // per-warp deferred-walk queue (offset + 16-byte snippet)
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
@@ -81,7 +86,7 @@ struct ScanArgs {
     // shared-memory layout (bytes from the dynamic smem base; filter at 0)
     uint32_t filter_words;          // words of the (unreplicated) filter
     uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
-    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_queue;
+    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_queue, off_defer;
     uint32_t off_tbits, off_trank, off_tails, off_tbytes;
     uint32_t hot_tails, hot_tail_bytes, hot_words;  // tails of nodes < H; bitmap words ceil(H/32)
     uint32_t off_terms;             // out_ptr[T+1] + term_node[TK] in smem (0 = in global memory)
@@ -215,19 +220,9 @@ struct RingText {
     uint32_t end;         // readable bytes from the window start
     const uint8_t *g;     // text + window start
     __device__ __forceinline__ uint32_t at(uint32_t r) const {
-        if (r < span) return ring[(((s0 + (r >> 10)) & (kSlots - 1)) << 10) | (r & 1023u)];
+        if (r < span)
+            return ring[(((s0 + (r >> kSlotLog2)) & (kSlots - 1)) << kSlotLog2) | (r & (kSlotBytes - 1u))];
         return __ldg(g + r);
-    }
-    __device__ __forceinline__ uint32_t word(uint32_t i) const {  // aligned word i of the window
-        return reinterpret_cast<const uint32_t *>(ring)[(((s0 + (i >> 8)) & (kSlots - 1)) << 8) | (i & 255u)];
-    }
-    // 4 bytes at offset r (little-endian; bytes past `end` are unspecified)
-    __device__ __forceinline__ uint32_t at4(uint32_t r) const {
-        if (r + 4 <= span) return __funnelshift_r(word(r >> 2), word((r >> 2) + 1), 8 * (r & 3));
-        uint32_t x = 0;
-        for (int b = 0; b < 4; ++b)
-            if (r + b < end) x |= at(r + b) << (8 * b);
-        return x;
     }
 };
 struct GlobalText {
@@ -238,6 +233,27 @@ struct GlobalText {
         uint32_t x = 0;
         for (int b = 0; b < 4; ++b)
             if (r + b < end) x |= (uint32_t)__ldg(g + r + b) << (8 * b);
+        return x;
+    }
+};
+
+// Text of a deferred survivor: the first kSnip bytes from its start were copied
+// into shared memory when it was deferred (the ring slot may be reused by the
+// time it is walked); later bytes come from global memory.
+constexpr uint32_t kSnip = 16;
+struct SnipText {
+    const uint8_t *snip;  // kSnip bytes (shared memory)
+    const uint8_t *g;     // text + start
+    uint32_t end;
+    __device__ __forceinline__ uint32_t at(uint32_t r) const { return r < kSnip ? snip[r] : __ldg(g + r); }
+    __device__ __forceinline__ uint32_t at4(uint32_t r) const {
+        uint32_t x = 0;
+        if (r + 4 <= kSnip) {
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(snip);
+            return __funnelshift_r(w[r >> 2], w[(r >> 2) + ((r & 3) ? 1 : 0)], 8 * (r & 3));
+        }
+        for (int b = 0; b < 4; ++b)
+            if (r + b < end) x |= at(r + b) << (8 * b);
         return x;
     }
 };
@@ -336,7 +352,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
 __device__ __forceinline__ uint32_t clamp32(uint64_t x) { return x > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)x; }
 
 
-// Stage 1 over one lane's 32 starts (text bytes wv[0..8] little-endian):
+// Stage 1 over one lane's kPerLane starts (text bytes wv[0..kWv) little-endian):
 // bit k set <=> start k may match.
 //  kind 1 (d = 4): word = hash of bytes k..k+2 (top bits of x*(M<<8)), bit =
 //    31 - (byte k+3 & 31): a rotate left by byte k+3 (the funnel shift takes
@@ -355,17 +371,37 @@ __device__ __forceinline__ uint2 lds64_abs(uint32_t addr) {
     return v;
 }
 template <int Kind>
-__device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[9], uint32_t sW, uint32_t sWmul,
+__device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[kWv], uint32_t sW, uint32_t sWmul,
                                              uint32_t stride, uint32_t base_lane) {
     uint32_t surv = 0;
-    if (Kind == 1) {
+    if (Kind == 2) {
+        // pair filter: one 64-bit block per start pair (k, k+1), chosen by the
+        // three shared bytes k+1..k+3 (x[k+1] * (M << 8) drops byte k+4)
+        constexpr uint32_t kMul = kFilterMul << 8;
+        uint32_t x[kPerLane + 1];
+#pragma unroll
+        for (int k = 0; k < kPerLane + 1; ++k)
+            x[k] = (k & 3) ? __funnelshift_r(wv[k >> 2], wv[(k >> 2) + 1], 8 * (k & 3)) : wv[k >> 2];
+        uint32_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int k = kPerLane - 2; k >= 0; k -= 2) {
+            const uint32_t blk = __umulhi(x[k + 1] * kMul, sWmul);
+            const uint2 w2 = lds64_abs(blk * stride + base_lane);
+            const uint32_t b4 = (k + 4 <= kPerLane) ? x[k + 4] : (wv[kWv - 1] >> 16);  // byte k+4 in the low bits
+            const uint32_t rb = __funnelshift_l(w2.y, w2.y, b4);    // start k+1: bit 31-(byte k+4 & 31)
+            const uint32_t ra = __funnelshift_l(w2.x, w2.x, x[k]);  // start k:   bit 31-(byte k & 31)
+            acc[k >> 3] = __funnelshift_l(ra, __funnelshift_l(rb, acc[k >> 3], 1), 1);
+        }
+        surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
+        static_assert(kPerLane <= 32, "");
+    } else if (Kind == 1) {
         constexpr uint32_t kMul = kFilterMul << 8;
         uint32_t x[kPerLane + 3];
 #pragma unroll
         for (int k = 0; k < kPerLane + 1; ++k)
             x[k] = (k & 3) ? __funnelshift_r(wv[k >> 2], wv[(k >> 2) + 1], 8 * (k & 3)) : wv[k >> 2];
-        x[kPerLane + 1] = x[kPerLane - 1] >> 16;  // byte 33 in the low bits
-        x[kPerLane + 2] = x[kPerLane - 1] >> 24;  // byte 34
+        x[kPerLane + 1] = x[kPerLane - 1] >> 16;  // byte kPerLane+1 in the low bits
+        x[kPerLane + 2] = x[kPerLane - 1] >> 24;  // byte kPerLane+2
         // four independent accumulation chains of 8 starts (short dependency
         // chains); the block index uses IMAD.HI (a right shift on the FMA pipe,
         // which the ALU-heavy bit test leaves idle): hi32(h * 2^(32-sW)) = h >> sW
@@ -393,8 +429,65 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
     return surv;
 }
 
+// Walk the deferred survivors dpos[0, n) (position order) with full warps;
+// hits are appended to the warp's hit list in the same order.  Returns (pid
+// count added by this lane, new hit count).
+__device__ __forceinline__ uint2 walk_deferred(const ScanArgs *ap, const Smem s, uint64_t range_lo, const uint32_t *dpos,
+                                            uint4 *dsnip, uint32_t n, uint2 *hits, uint32_t n_hits) {
+    const ScanArgs &a = *ap;
+    const int lane = threadIdx.x & 31;
+    uint32_t c = 0;
+    __syncwarp();
+    for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        uint32_t p = 0, tn = kNone;
+        if (j < n) {
+            p = dpos[j];
+            const uint64_t gp = range_lo + p;
+            // the ring slot may be gone: copy the first kSnip bytes from
+            // global memory (L2) into the lane's snippet, walk from there
+            uint8_t *sn = reinterpret_cast<uint8_t *>(dsnip + j);
+            if ((reinterpret_cast<uintptr_t>(a.text) & 3) == 0) {
+                const uint64_t gl = gp & ~3ull;
+                uint32_t w[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const uint64_t o = gl + 4 * q;
+                    w[q] = o + 4 <= a.readable ? __ldg(reinterpret_cast<const uint32_t *>(a.text + o)) : 0u;
+                    if (o < a.readable && o + 4 > a.readable) {  // ragged text end
+                        for (int b = 0; b < 4; ++b)
+                            if (o + b < a.readable) w[q] |= (uint32_t)__ldg(a.text + o + b) << (8 * b);
+                    }
+                }
+                const uint32_t sh = 8 * (uint32_t)(gp & 3);
+                uint4 v4;
+                v4.x = __funnelshift_r(w[0], w[1], sh);
+                v4.y = __funnelshift_r(w[1], w[2], sh);
+                v4.z = __funnelshift_r(w[2], w[3], sh);
+                v4.w = __funnelshift_r(w[3], w[4], sh);
+                *reinterpret_cast<uint4 *>(sn) = v4;
+            } else {  // unaligned text pointer: bytes
+#pragma unroll 1
+                for (uint32_t b = 0; b < kSnip; ++b) sn[b] = gp + b < a.readable ? __ldg(a.text + gp + b) : 0;
+            }
+            const SnipText st{sn, a.text + gp, clamp32(a.readable - gp)};
+            tn = walk(a, s, st, 0u);
+            if (tn != kNone) c += s.out_ptr[tn + 1] - s.out_ptr[tn];
+        }
+        const bool hit = tn != kNone;
+        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const uint32_t idx = n_hits + __popc(hb & ((1u << lane) - 1u));
+            if (idx < a.hit_cap) hits[idx] = make_uint2(p, tn);
+        }
+        n_hits += __popc(hb);
+    }
+    __syncwarp();
+    return make_uint2(c, n_hits);
+}
+
 template <int Kind>
-__global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t *s_filter = reinterpret_cast<uint32_t *>(smem);
@@ -432,8 +525,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     // word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
     // so the lanes of a phase spread over the banks
     const uint32_t rep = 1u << a.rep_log2;
-    const uint32_t unit = Kind == 1 ? 8u : 4u;
-    const uint32_t sW = 32u - (a.t.log2_bits - (Kind == 1 ? 6u : 5u));  // block index = hash >> sW
+    const uint32_t unit = Kind >= 1 ? 8u : 4u;
+    const uint32_t sW = 32u - (a.t.log2_bits - (Kind >= 1 ? 6u : 5u));  // block index = hash >> sW
     const uint32_t sWmul = 1u << (32u - sW);                              // (hash * sWmul) >> 32 == hash >> sW
     const uint32_t stride = rep * unit;
     const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
@@ -464,11 +557,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
                 mbar_arrive_expect_tx(&bars[slot], kSlotBytes);
                 bulk_g2s(dst, a.text + lo, kSlotBytes, &bars[slot], policy);
             }
-        } else {  // unaligned text or ragged tail: lanes copy, zero-fill past `readable`
-            for (int k = 0; k < kPerLane; ++k) {
-                const uint32_t o = lane + 32 * k;
+        } else {  // unaligned text or ragged tail (cold): lanes copy, zero-fill past `readable`
+#pragma unroll 1
+            for (uint32_t o = lane; o < (uint32_t)kSlotBytes; o += 32)
                 dst[o] = o < avail ? __ldg(a.text + lo + o) : (uint8_t)0;
-            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars[slot]);
         }
@@ -496,8 +588,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     }
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
-        const uint32_t nu = (Kind == 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
-        if (Kind == 1) {
+        const uint32_t nu = (Kind >= 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
+        if (Kind >= 1) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
             for (uint32_t j = tid; j < nu; j += kThreads) d[j] = __ldg(src + (j >> a.rep_log2));
@@ -523,50 +615,95 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
     // of the ring is in flight.
     uint32_t c = 0;       // pattern ids matched by this lane's starts
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
+    uint32_t dcount = 0;  // deferred survivors waiting for a walk batch (warp-uniform)
+    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * (kDefer * 5);
+    uint4 *dsnip = reinterpret_cast<uint4 *>(dpos + kDefer);
+    // Walk the deferred survivors (position order) with full warps; hits are
+    // appended to the hit list in the same order.
+    auto flush = [&]() {
+#if defined(PFAC_EXP) && PFAC_EXP == 2
+        dcount = 0;  // experiment: no walks
+        return;
+#endif
+        const uint2 r = walk_deferred(&a, s, range_lo, dpos, dsnip, dcount, hits, n_hits);
+        c += r.x;
+        n_hits = r.y;
+        dcount = 0;
+    };
     for (uint64_t i = 0; i < nr; i += kGroup) {
-#pragma unroll
+#pragma unroll 1
         for (int g = 0; g < kGroup; ++g)  // refill the slots of the previous group
             if (i + kSlots - kGroup + g < nr) issue(i + kSlots - kGroup + g);
         const uint32_t ng = nr - i < (uint64_t)kGroup ? (uint32_t)(nr - i) : (uint32_t)kGroup;
-        const uint32_t nres = nr - i < (uint64_t)(ng + 1) ? (uint32_t)(nr - i) : ng + 1;
-        for (uint32_t q = 0; q < nres; ++q) mbar_wait(&bars[(i + q) % kSlots], (uint32_t)(((i + q) / kSlots) & 1));
         const uint64_t gbase = (r_begin + i) * kRound;
-        const RingText tx{ring, (uint32_t)(i % kSlots), nres * (uint32_t)kSlotBytes, clamp32(a.readable - gbase),
-                          a.text + gbase};
-
-        // ---- stage 1: filter over the lane's 32 starts of each round
-        uint32_t surv[kGroup];
-#pragma unroll
-        for (int g = 0; g < kGroup; ++g) {
-            surv[g] = 0;
-            if ((uint32_t)g < ng) {
-                const uint8_t *p0 = ring + ((i + g) % kSlots) * kSlotBytes;
-                const uint4 q0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane);
-                const uint4 q1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16);
-                uint32_t w8 = __shfl_down_sync(0xffffffffu, q0.x, 1);
-                const uint64_t rbase = gbase + (uint64_t)g * kRound;
-                if (lane == 31) {
-                    if ((uint32_t)g + 1 < nres) {
-                        w8 = *reinterpret_cast<const uint32_t *>(ring + ((i + g + 1) % kSlots) * kSlotBytes);
-                    } else {
-                        w8 = 0;
-                        const uint64_t j0 = rbase + kRound;
-                        for (int b = 0; b < 4; ++b)
-                            if (j0 + b < a.readable) w8 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
-                    }
-                }
-                const uint32_t wv[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, w8};
-                const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
-                surv[g] = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
-                if (lbase + kPerLane > lim) {
-                    const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
-                    surv[g] &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
-                }
+        // the 4 bytes after the group (lane 31's last 4-gram window) come from
+        // global memory: prefetched now, so the group never waits for the next
+        // round (which was only just issued) -- rounds land a full group ahead
+        uint32_t tail4 = 0;
+        if (lane == 31) {
+            const uint64_t j0 = gbase + (uint64_t)ng * kRound;
+            if (j0 + 4 <= a.readable && a.aligned) {
+                tail4 = __ldg(reinterpret_cast<const uint32_t *>(a.text + j0));
+            } else {
+                for (int b = 0; b < 4; ++b)
+                    if (j0 + b < a.readable) tail4 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
             }
         }
+        for (uint32_t q = 0; q < ng; ++q) mbar_wait(&bars[(i + q) % kSlots], (uint32_t)(((i + q) / kSlots) & 1));
+        const RingText tx{ring, (uint32_t)(i % kSlots), ng * (uint32_t)kSlotBytes, clamp32(a.readable - gbase),
+                          a.text + gbase};
 
+#ifdef PFAC_STREAM_ONLY
+        // experiment (tools/timing.py): stream the text through the ring only
+        if (lane == 0 && ring[(i % kSlots) * kSlotBytes] == 0xFF && gbase == 0) c++;
+        __syncwarp();
+        continue;
+#endif
+        // ---- stage 1: filter over the lane's starts of each round (one copy
+        // of the filter code: the group loop is not unrolled)
+        uint32_t surv0 = 0, surv1 = 0;
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+            uint32_t sv = 0;
+            if ((uint32_t)g < ng) {
+                const uint8_t *p0 = ring + ((i + g) % kSlots) * kSlotBytes;
+                uint32_t wv[kWv];
+#pragma unroll
+                for (int q = 0; q < kPerLane / 16; ++q) {
+                    const uint4 t4 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * q);
+                    wv[4 * q] = t4.x;
+                    wv[4 * q + 1] = t4.y;
+                    wv[4 * q + 2] = t4.z;
+                    wv[4 * q + 3] = t4.w;
+                }
+                uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+                const uint64_t rbase = gbase + (uint64_t)g * kRound;
+                if (lane == 31)
+                    w8 = (uint32_t)g + 1 < ng ? *reinterpret_cast<const uint32_t *>(ring + ((i + g + 1) % kSlots) * kSlotBytes)
+                                              : tail4;
+                wv[kWv - 1] = w8;
+                const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
+                sv = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
+                if (lbase + kPerLane > lim) {
+                    const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
+                    sv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
+                }
+            }
+            if (g == 0) surv0 = sv; else surv1 = sv;
+        }
+        const uint32_t surv[kGroup] = {surv0, surv1};
+
+#if defined(PFAC_EXP) && PFAC_EXP == 1
+        // experiment: filter only (survivor masks folded into a dummy count)
+        c += (surv0 ^ surv1) == 0xDEADBEEFu;
+        __syncwarp();
+        continue;
+#endif
         // ---- stage 2: compact survivors (position order: round, lane, start)
-        // into the warp queue, walk them with full warps
+        // into the warp queue; a cheap first check (root table + level-1
+        // bitmapped node) kills most of them with full warps; the
+        // rest are deferred, in order, with a text snippet and walked in
+        // batches of >= 32 (the deep walk cost is paid once per batch)
         static_assert(kGroup == 2, "packed two-round scan below");
         const uint32_t ns0 = __popc(surv[0]), ns1 = __popc(surv[1]);
         if (__any_sync(0xffffffffu, (ns0 | ns1) != 0)) {
@@ -588,27 +725,36 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
                 __syncwarp();
                 const uint32_t n = stot - qb < (uint32_t)kQueue ? stot - qb : (uint32_t)kQueue;
                 for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+                    if (dcount > kDefer - 32) flush();
                     const uint32_t j = j0 + lane;
-                    uint32_t off = 0, tn = kNone;
+                    uint32_t off = 0;
+                    bool keep = false;
                     if (j < n) {
                         off = queue[j];
-                        tn = walk(a, s, tx, off);  // terminal index
-                        if (tn != kNone) c += s.out_ptr[tn + 1] - s.out_ptr[tn];
+                        const uint32_t v = s.root[tx.at(off)];
+                        if (v != 0) {
+                            const uint32_t w = node_word(a, s, v);
+                            keep = (w & (kTermBit | kTailBit)) != 0;
+                            if (!keep && off + 1 < tx.end) {
+                                const uint32_t c1 = tx.at(off + 1);
+                                keep = (s.bm[(v - 1) * 10 + (c1 >> 5)] >> (c1 & 31)) & 1u;
+                            }
+                        }
                     }
-                    const bool hit = tn != kNone;
-                    // hits in queue order == position order
-                    const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-                    if (hit) {
-                        const uint32_t idx = n_hits + __popc(hb & ((1u << lane) - 1u));
-                        if (idx < a.hit_cap) hits[idx] = make_uint2((uint32_t)(gbase - range_lo) + off, tn);
+                    const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {  // defer (order kept: ballot prefix)
+                        const uint32_t d = dcount + __popc(kb & ((1u << lane) - 1u));
+                        dpos[d] = (uint32_t)(gbase - range_lo) + off;
                     }
-                    n_hits += __popc(hb);
+                    dcount += __popc(kb);
                 }
                 __syncwarp();
             }
         }
+        if (dcount >= 32) flush();
         __syncwarp();
     }
+    if (dcount) flush();
     STAMP(2);
     uint64_t total;
     {
@@ -688,8 +834,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const ScanArgs a
         for (uint64_t i = 0; i < nr; ++i) {
             const uint64_t rbase = (r_begin + i) * kRound;
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
-            uint32_t wv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-            for (int b = 0; b < 36; ++b)
+            uint32_t wv[kWv];
+            for (int q = 0; q < kWv; ++q) wv[q] = 0;
+#pragma unroll 1
+            for (int b = 0; b < 4 * kWv; ++b)
                 if (lbase + b < a.readable) wv[b >> 2] |= (uint32_t)__ldg(a.text + lbase + b) << (8 * (b & 3));
             uint32_t surv = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
             if (lbase + kPerLane > lim) {
@@ -750,6 +898,9 @@ int device_info(int device, DeviceInfo &out, std::string &err) {
                                      di.max_smem_optin);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(pfac_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     di.max_smem_optin);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(pfac_scan_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      di.max_smem_optin);
         if (e != cudaSuccess) {
             err = std::string("device query: ") + cudaGetErrorString(e);
@@ -862,18 +1013,15 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + kWarps * kQueue * 2 + 1024 +
+                           kWarps * kDefer * 20 +
                            align16(40 * B) + 8 * (kWarps + 1) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
         return kStatusLimit;
     }
     const uint32_t rest = (uint32_t)di.max_smem_optin - fixed;
-    uint32_t rep_log2 = 0;
-    // the filter gets up to 64 KiB (replicas cut bank conflicts), the hot trie the rest
-    const uint32_t fcap = rest > 16384 + 65536 ? 65536u : (rest > 16384 ? rest - 16384 : rest / 2);
-    while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= fcap) rep_log2++;
-    const uint32_t filter_bytes = filter_words * 4 << rep_log2;
-    const uint32_t trie_budget = rest - filter_bytes;
+    // priority: ring (in `fixed`) > hot trie > filter replicas (cut bank conflicts)
+    const uint32_t trie_budget = rest - filter_words * 4;
     // H = largest BFS prefix whose node words [0, H], labels [0, row_ptr[H]),
     // tail bitmap/rank words and tail records + bytes (tails of nodes < H)
     // all fit the budget
@@ -891,15 +1039,24 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
         return align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) + 2ull * align16(4 * ((H + 31) / 32)) +
                16ull * nt + align16(tbytes_below(nt));
     };
+    // Whole trie in shared memory when it fits; otherwise only its upper
+    // levels (<= kHotCap bytes), so that the unified L1/shared array keeps a
+    // large L1 that caches the deeper nodes and tails the walks touch.
+    const uint32_t budget =
+        hot_bytes(t.n_nodes - 1) <= trie_budget ? trie_budget : (trie_budget < kHotCap ? trie_budget : kHotCap);
     uint32_t lo = 1, hi = t.n_nodes - 1;
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        if (hot_bytes(mid) <= trie_budget) lo = mid; else hi = mid - 1;
+        if (hot_bytes(mid) <= budget) lo = mid; else hi = mid - 1;
     }
     const uint32_t H = lo;
     const uint32_t EH = host_node[H] & kEdgeMask;
     const uint32_t TH = tails_below(H);
     const uint32_t TBH = tbytes_below(TH);
+    const uint32_t left = rest - (uint32_t)hot_bytes(H);  // >= filter_words * 4
+    uint32_t rep_log2 = 0;
+    while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= (left < kFilterCap ? left : kFilterCap)) rep_log2++;
+    const uint32_t filter_bytes = filter_words * 4 << rep_log2;
 
     ScanArgs a;
     a.t = t;
@@ -913,6 +1070,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
     a.off_queue = o;  o += kWarps * kQueue * 2;
+    a.off_defer = o;  o += kWarps * kDefer * 20;  // per warp: u32 pos[kDefer] + uint4 snippet[kDefer]
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
     a.off_label = o;  o += align16(EH);
@@ -963,7 +1121,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.rounds_per_warp = geo.rounds_per_warp;
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
-    const void *fn = t.kind == 1 ? (const void *)pfac_scan_kernel<1> : (const void *)pfac_scan_kernel<0>;
+    const void *fn = t.kind == 2 ? (const void *)pfac_scan_kernel<2>
+                     : t.kind == 1 ? (const void *)pfac_scan_kernel<1> : (const void *)pfac_scan_kernel<0>;
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)geo.grid), dim3(kThreads), args, smem, stream);
     if (e != cudaSuccess) {
         {   // the kernel did not run: the barrier counter in use is unchanged

@@ -49,13 +49,28 @@ def tail_index(h, v):
 def filter_bits(h, key):
     """Bit indices (word * 32 + bit) of the filter entries a d-gram key tests
     (all must be set for the start to survive)."""
+    if h["filter_kind"] == 2:  # d = 4: pair filter, tested here as the first start of a pair
+        raise ValueError("kind 2 tests depend on the start's parity; use filter_pass")
     if h["filter_kind"] == 1:  # d = 4: blocked two-bit filter (image.h)
         b = ((key * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
         return [2 * b * 32 + (31 - ((key >> 24) & 31)), (2 * b + 1) * 32 + (31 - ((key >> 16) & 31))]
     return [filter_index(h, key)]
 
 
-def filter_pass(h, key):
+def _block(h, x3):
+    return ((x3 * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
+
+
+def filter_pass(h, key, start=0):
+    """Does the start whose first d bytes are `key` pass the filter?  Kind 2
+    (pair filter) depends on the start's parity (image.h)."""
+    if h["filter_kind"] == 2:
+        f = h["filter"]
+        if start % 2 == 0:  # first of the pair: shared bytes 1..3, own byte 0
+            b = _block(h, key >> 8)
+            return bool((int(f[2 * b]) >> (31 - (key & 31))) & 1)
+        b = _block(h, key & 0xFFFFFF)  # second: shared bytes are the start's bytes 0..2, own byte 3
+        return bool((int(f[2 * b + 1]) >> (31 - ((key >> 24) & 31))) & 1)
     return all((int(h["filter"][i >> 5]) >> (i & 31)) & 1 for i in filter_bits(h, key))
 
 
@@ -116,7 +131,7 @@ def match(h, text: bytes, readable=None, n_starts=None):
     for i in range(ns):
         if i + d > L:
             continue
-        if not filter_pass(h, int.from_bytes(text[i:i + d], "little")):
+        if not filter_pass(h, int.from_bytes(text[i:i + d], "little"), i):
             continue
         ti = walk(h, text, i, L)
         if ti is not None:

@@ -130,7 +130,8 @@ def test_filter_is_complete():
         h = image_walker.parse(pf.Trie(ps).image())
         d = h["filter_gram"]
         for k in range(len(ps)):
-            assert image_walker.filter_pass(h, int.from_bytes(ps[k][:d], "little"))
+            key = int.from_bytes(ps[k][:d], "little")
+            assert image_walker.filter_pass(h, key, 0) and image_walker.filter_pass(h, key, 1)
 
 
 def test_attach_roundtrip_and_validation():
