@@ -35,7 +35,11 @@ $(PKG)/libpfac_exp1.so: $(CSRC) $(CHDR)
 $(PKG)/libpfac_exp2.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_EXP=2 -shared -o $@ $(CSRC) -lcudart
 
+# experiment / instrumented builds (tools/timing.py; never used by tests or bench)
+EXPLIBS := $(PKG)/libpfac_timing.so $(PKG)/libpfac_stream.so $(PKG)/libpfac_exp1.so $(PKG)/libpfac_exp2.so
+exp: $(EXPLIBS)
+
 clean:
-	rm -f gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so
+	rm -f gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so $(EXPLIBS)
 
 .PHONY: all clean

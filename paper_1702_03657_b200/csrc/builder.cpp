@@ -264,8 +264,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         }
         std::sort(keys.begin(), keys.end());
         const uint64_t distinct = std::unique(keys.begin(), keys.end()) - keys.begin();
-        // kind 2 (pair filter, d = 4): one bit per key and role, 2 keys/bit-set
-        // per 4-gram -> ~64 bits per 4-gram keeps the fill near 1.6%; used
+        // kind 2 (pair filter, d = 4): one bit per key and role, 2 bits set
+        // per 4-gram -> ~128 bits per 4-gram keeps the fill near 1.6%; used
         // while that fits 2^18 bits.  Else kind 1 (blocked two-bit, ~32 bits
         // per key, ~0.5% false positives) or kind 0 (d < 4, ~3%), capped at
         // 2^19 bits (64 KiB, the shared-memory budget).
@@ -286,12 +286,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         uint32_t x = 0;
         for (uint32_t b = 0; b < gram; b++) x |= (uint32_t)pats[k][b] << (8 * b);
         if (kind == 2) {
-            // as the first start of a pair: shared bytes are P[1..3], own byte P[0]
-            const uint32_t b1 = filter4_block(x >> 8, log2_bits);
-            filter[2 * b1] |= 1u << (31u - (x & 31u));
+            // as the first start of a pair: shared bytes are P[1..3], own byte P[0];
             // as the second start: shared bytes are P[0..2], own byte P[3]
-            const uint32_t b2 = filter4_block(x, log2_bits);
-            filter[2 * b2 + 1] |= 1u << (31u - ((x >> 24) & 31u));
+            filter[filter_pair_word(x >> 8, log2_bits)] |= 1u << (31u - (x & 31u));
+            filter[filter_pair_word(x, log2_bits)] |= 1u << (31u - ((x >> 24) & 31u));
         } else if (kind == 1) {
             const uint32_t b = filter4_block(x, log2_bits);
             filter[2 * b] |= 1u << filter4_bit_lo(x);

@@ -51,13 +51,14 @@
 //                         kernel tests each with one rotate; scan.cu stage 1).
 //                         A start passes iff both bits are set.
 //                       kind 2 (d = 4, small sets): the pair filter.  Starts k
-//                         and k+1 share bytes k+1..k+3, so one 64-bit block
-//                         b = filter4_block(bytes k+1..k+3) answers both: start
-//                         k passes iff bit 31-(byte k & 31) of word 2b is set,
-//                         start k+1 iff bit 31-(byte k+4 & 31) of word 2b+1 is
-//                         set.  A pattern 4-gram P sets word 2*block(P[1..3])
-//                         bit 31-(P[0]&31) and word 2*block(P[0..2])+1 bit
-//                         31-(P[3]&31).
+//                         and k+1 share bytes k+1..k+3, so one 32-bit word
+//                         b = filter_pair_word(bytes k+1..k+3) answers both:
+//                         start k passes iff bit 31-(byte k & 31) of word b is
+//                         set, start k+1 iff bit 31-(byte k+4 & 31) is set.
+//                         A pattern 4-gram P sets bit 31-(P[0]&31) of word
+//                         filter_pair_word(P[1..3]) and bit 31-(P[3]&31) of
+//                         word filter_pair_word(P[0..2]).  Half the bytes per
+//                         start of kind 1 at the same fill for 2 bits per key.
 #pragma once
 #include <cstdint>
 
@@ -69,7 +70,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 4;
+constexpr uint32_t kVersion = 5;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -101,6 +102,10 @@ PFAC_HD inline uint32_t filter_index(uint32_t key, uint32_t log2_bits, uint32_t 
 // 2b+1) of the 4-gram x.
 PFAC_HD inline uint32_t filter4_block(uint32_t x, uint32_t log2_bits) {
     return (x * (kFilterMul << 8)) >> (32u - (log2_bits - 6u));
+}
+// Kind 2 (d = 4): word index of the three shared bytes x (low 24 bits used).
+PFAC_HD inline uint32_t filter_pair_word(uint32_t x, uint32_t log2_bits) {
+    return (x * (kFilterMul << 8)) >> (32u - (log2_bits - 5u));
 }
 PFAC_HD inline uint32_t filter4_bit_lo(uint32_t x) { return 31u - ((x >> 24) & 31u); }
 PFAC_HD inline uint32_t filter4_bit_hi(uint32_t x) { return 31u - ((x >> 16) & 31u); }

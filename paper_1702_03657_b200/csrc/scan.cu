@@ -20,11 +20,11 @@
 //    (cp.async.bulk + mbarrier, evict-first in L2) kSlots-1 rounds ahead.
 //    Per round each lane tests its 32 consecutive starts against the filter
 //    (a clear bit means no pattern can start there: PFAC's early termination
-//    taken before the first trie access).  Survivors are compacted into a
-//    per-warp queue and walked with full warps to the first mismatch.  A
-//    start that passed a terminal is appended, in position order, to the
-//    warp's hit list (its offset; matches are rare, so phase 3 walks these
-//    starts again instead of storing the terminal).
+//    taken before the first trie access).  Each survivor gets an in-lane
+//    first check (root table + level-1 bitmapped node); the few that pass are
+//    deferred to a per-warp queue and walked in full-warp batches to the first
+//    mismatch.  A start that passed a terminal is appended, in position
+//    order, to the warp's hit list (offset, terminal index).
 //  * phase 2 (offsets): per-warp match counts -> CTA scan -> one grid barrier
 //    -> exclusive prefix over CTA totals.  Ranges are contiguous and ordered,
 //    so the concatenation is globally sorted by (pos, pid).
@@ -44,19 +44,16 @@ namespace {
 
 constexpr int kWarps = 32;
 constexpr int kThreads = kWarps * 32;
-constexpr int kPerLane = 16;           // consecutive starts per lane per round
-constexpr int kRound = 32 * kPerLane;  // 512 starts per warp round
+constexpr int kPerLane = 32;           // consecutive starts per lane per round
+constexpr int kRound = 32 * kPerLane;  // 1024 starts per warp round
 constexpr int kWv = kPerLane / 4 + 1;  // text words a lane needs (its starts + 3 bytes)
-constexpr int kSlots = 4;              // text ring depth per warp (power of two)
-constexpr int kGroup = 2;              // rounds per survivor-compaction/walk pass
+constexpr int kSlots = 3;              // text ring depth per warp (kSlots-1 rounds in flight)
 constexpr int kSlotBytes = kRound;     // one round of text per slot
-constexpr int kSlotLog2 = 9;
-static_assert(kSlotBytes == (1 << kSlotLog2) && (kSlots & (kSlots - 1)) == 0, "ring indexing uses shifts");
+static_assert(kSlots >= 2, "ring");
 constexpr int kMaxCtas = 1024;
-constexpr int kQueue = 64;             // per-warp survivor queue (u16 round offsets)
 constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated filter
 constexpr uint32_t kHotCap = 24576;  // hot-trie smem when the trie does not fit (rest left to L1)
-constexpr int kDefer = 48;             // per-warp deferred-walk queue (offset + 16-byte snippet)
+constexpr int kDefer = 64;             // per-warp deferred-walk queue (offset + 16-byte snippet)
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
@@ -86,7 +83,7 @@ struct ScanArgs {
     // shared-memory layout (bytes from the dynamic smem base; filter at 0)
     uint32_t filter_words;          // words of the (unreplicated) filter
     uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
-    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_queue, off_defer;
+    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_defer, off_pair;
     uint32_t off_tbits, off_trank, off_tails, off_tbytes;
     uint32_t hot_tails, hot_tail_bytes, hot_words;  // tails of nodes < H; bitmap words ceil(H/32)
     uint32_t off_terms;             // out_ptr[T+1] + term_node[TK] in smem (0 = in global memory)
@@ -155,11 +152,11 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int *p) {
 
 #ifdef PFAC_TIMING
 // Instrumented build only (tools/timing.py): per-warp %globaltimer stamps.
-__device__ unsigned long long g_pfac_timing[2048 * 8];
+__device__ unsigned long long g_pfac_timing[8192 * 8];
 __device__ __forceinline__ void stamp(int warp_global, int k) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if ((threadIdx.x & 31) == 0 && warp_global < 2048) g_pfac_timing[warp_global * 8 + k] = t;
+    if ((threadIdx.x & 31) == 0 && warp_global < 8192) g_pfac_timing[warp_global * 8 + k] = t;
 }
 #define STAMP(k) stamp((int)(blockIdx.x * kWarps + (threadIdx.x >> 5)), k)
 #else
@@ -210,21 +207,6 @@ __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, u
     return e < a.hot_edges ? (uint32_t)s.label[e] : (uint32_t)__ldg(a.t.label + e);
 }
 
-// Text seen by a walk, addressed relative to a global position: from the
-// warp's ring when the offset lies in it, else from global memory.
-// `end` = readable bytes from that position (clamped to 32 bits).
-struct RingText {
-    const uint8_t *ring;  // this warp's ring (kSlots slots of kSlotBytes)
-    uint32_t s0;          // slot holding the first round of the window
-    uint32_t span;        // resident bytes from the window start (whole rounds)
-    uint32_t end;         // readable bytes from the window start
-    const uint8_t *g;     // text + window start
-    __device__ __forceinline__ uint32_t at(uint32_t r) const {
-        if (r < span)
-            return ring[(((s0 + (r >> kSlotLog2)) & (kSlots - 1)) << kSlotLog2) | (r & (kSlotBytes - 1u))];
-        return __ldg(g + r);
-    }
-};
 struct GlobalText {
     const uint8_t *g;
     uint32_t end;
@@ -375,7 +357,7 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
                                              uint32_t stride, uint32_t base_lane) {
     uint32_t surv = 0;
     if (Kind == 2) {
-        // pair filter: one 64-bit block per start pair (k, k+1), chosen by the
+        // pair filter: one 32-bit word per start pair (k, k+1), chosen by the
         // three shared bytes k+1..k+3 (x[k+1] * (M << 8) drops byte k+4)
         constexpr uint32_t kMul = kFilterMul << 8;
         uint32_t x[kPerLane + 1];
@@ -386,10 +368,10 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
 #pragma unroll
         for (int k = kPerLane - 2; k >= 0; k -= 2) {
             const uint32_t blk = __umulhi(x[k + 1] * kMul, sWmul);
-            const uint2 w2 = lds64_abs(blk * stride + base_lane);
+            const uint32_t w = lds_abs(blk * stride + base_lane);
             const uint32_t b4 = (k + 4 <= kPerLane) ? x[k + 4] : (wv[kWv - 1] >> 16);  // byte k+4 in the low bits
-            const uint32_t rb = __funnelshift_l(w2.y, w2.y, b4);    // start k+1: bit 31-(byte k+4 & 31)
-            const uint32_t ra = __funnelshift_l(w2.x, w2.x, x[k]);  // start k:   bit 31-(byte k & 31)
+            const uint32_t rb = __funnelshift_l(w, w, b4);    // start k+1: bit 31-(byte k+4 & 31)
+            const uint32_t ra = __funnelshift_l(w, w, x[k]);  // start k:   bit 31-(byte k & 31)
             acc[k >> 3] = __funnelshift_l(ra, __funnelshift_l(rb, acc[k >> 3], 1), 1);
         }
         surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
@@ -498,7 +480,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.off_bar) + warp * kSlots;
     unsigned long long *s_wtot = reinterpret_cast<unsigned long long *>(smem + a.off_warp);  // [kWarps + 1]
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
-    uint16_t *queue = reinterpret_cast<uint16_t *>(smem + a.off_queue) + warp * kQueue;
 
     STAMP(0);
     // ---- barriers: per-warp text ring + one for the table staging
@@ -521,12 +502,12 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     s.tails = reinterpret_cast<const uint4 *>(smem + a.off_tails);
     s.tail_bytes = smem + a.off_tbytes;
     // filter addressing: copies interleaved at the unit the kernel loads
-    // (kind 1: 8-byte block b of copy r at filter + 8*(b*rep + r); kind 0:
-    // word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
+    // (kind 1: 8-byte block b of copy r at filter + 8*(b*rep + r); kinds 0
+    // and 2: word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
     // so the lanes of a phase spread over the banks
     const uint32_t rep = 1u << a.rep_log2;
-    const uint32_t unit = Kind >= 1 ? 8u : 4u;
-    const uint32_t sW = 32u - (a.t.log2_bits - (Kind >= 1 ? 6u : 5u));  // block index = hash >> sW
+    const uint32_t unit = Kind == 1 ? 8u : 4u;
+    const uint32_t sW = 32u - (a.t.log2_bits - (Kind == 1 ? 6u : 5u));  // block index = hash >> sW
     const uint32_t sWmul = 1u << (32u - sW);                              // (hash * sWmul) >> 32 == hash >> sW
     const uint32_t stride = rep * unit;
     const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
@@ -545,19 +526,19 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     const uint64_t range_lo = r_begin * kRound;
     uint2 *hits = a.hits + gw * a.hit_cap;
 
-    // Fill slot `i % kSlots` with round r_begin + i of this warp's range.
-    auto issue = [&](uint64_t i) {
-        const uint32_t slot = (uint32_t)(i % kSlots);
+    // Fill ring slot `slot` with round i of this warp's range (one 1 KiB TMA
+    // bulk copy; the unaligned-text / ragged-tail path copies with the lanes).
+    auto issue = [&](uint32_t i, uint32_t slot) {
         uint8_t *dst = ring + slot * kSlotBytes;
-        const uint64_t lo = (r_begin + i) * kRound;
-        const uint64_t avail = lo < a.readable ? a.readable - lo : 0;
-        if (a.aligned && avail >= (uint64_t)kSlotBytes) {
+        const uint64_t lo = range_lo + (uint64_t)i * kRound;
+        if (a.aligned && lo + kSlotBytes <= a.readable) {
             if (lane == 0) {
                 fence_proxy_async_smem();  // prior generic reads of the slot precede the async write
                 mbar_arrive_expect_tx(&bars[slot], kSlotBytes);
                 bulk_g2s(dst, a.text + lo, kSlotBytes, &bars[slot], policy);
             }
-        } else {  // unaligned text or ragged tail (cold): lanes copy, zero-fill past `readable`
+        } else {  // cold: lanes copy, zero-fill past `readable`
+            const uint64_t avail = lo < a.readable ? a.readable - lo : 0;
 #pragma unroll 1
             for (uint32_t o = lane; o < (uint32_t)kSlotBytes; o += 32)
                 dst[o] = o < avail ? __ldg(a.text + lo + o) : (uint8_t)0;
@@ -568,8 +549,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 
     // ---- start streaming this warp's text, then stage the tables (TMA bulk
     // copies of the image sections; the filter is replicated from 16-byte loads)
-    const uint64_t nr = r_end - r_begin;
-    for (uint64_t i = 0; i < nr && i < kSlots - kGroup; ++i) issue(i);
+    const uint32_t nr = (uint32_t)(r_end - r_begin);
+    for (uint32_t i = 0; i < nr && i < kSlots - 1; ++i) issue(i, i);
     if (tid == 0) {
         const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
                        nb_l1 = align16(40 * a.n_level1);
@@ -588,8 +569,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     }
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
-        const uint32_t nu = (Kind >= 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
-        if (Kind >= 1) {
+        const uint32_t nu = (Kind == 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
+        if (Kind == 1) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
             for (uint32_t j = tid; j < nu; j += kThreads) d[j] = __ldg(src + (j >> a.rep_log2));
@@ -606,155 +587,134 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     }
     mbar_wait(sbar, 0);
     __syncthreads();
+    // 2-gram prefix table: word (b0, q) bit j <=> the walk from a start with
+    // bytes (b0, 32q + j) gets past level 1 (or b0's node already is a
+    // terminal / tail start, where every b1 is kept)
+    uint32_t *s_pair = reinterpret_cast<uint32_t *>(smem + a.off_pair);
+    for (uint32_t j = tid; j < 2048; j += kThreads) {
+        const uint32_t v = s_root[j >> 3];
+        uint32_t wd = 0;
+        if (v != 0) wd = (__ldg(a.t.node + v) & (kTermBit | kTailBit)) ? 0xFFFFFFFFu : s_bm[(v - 1) * 10 + (j & 7)];
+        s_pair[j] = wd;
+    }
+    __syncthreads();
     STAMP(1);
 
     // ================================================= phase 1: scan
-    // Groups of kGroup rounds: stage 1 on each round, then one compaction +
-    // walk pass for the group's survivors (amortises the pass overhead).  The
-    // ring keeps the group + one round of look-ahead resident while the rest
-    // of the ring is in flight.
+    // One 1024-start round per iteration; the ring keeps kSlots-1 rounds in
+    // flight.  Stage 1 filters each lane's 32 starts (bit mask).  Stage 2
+    // tests each survivor in its lane against the 2-gram prefix table (the
+    // root's children and their level-1 bitmapped nodes): bytes
+    // (b0, b1) begin a pattern path, or b0 alone already reaches a terminal or
+    // tail.  The kept starts are appended to the warp's deferred queue in
+    // position order (lane-major = position order) and walked in full-warp
+    // batches whenever the queue may not take another round.
     uint32_t c = 0;       // pattern ids matched by this lane's starts
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
-    uint32_t dcount = 0;  // deferred survivors waiting for a walk batch (warp-uniform)
+    uint32_t dcount = 0;  // deferred starts in the queue (warp-uniform)
     uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * (kDefer * 5);
     uint4 *dsnip = reinterpret_cast<uint4 *>(dpos + kDefer);
-    // Walk the deferred survivors (position order) with full warps; hits are
-    // appended to the hit list in the same order.
-    auto flush = [&]() {
+    uint32_t slot = 0, phase = 0, slot2 = kSlots - 1;  // ring slot of round i, its parity; slot of round i+kSlots-1
+    uint32_t km = 0;     // this lane's kept starts of round i not yet queued
+    bool more = false;   // round i still has kept starts to queue (warp-uniform)
+    uint32_t i = 0;
+    for (;;) {
+        // ---- the single batch-walk site
+        if (dcount != 0 && (i == nr || more || dcount > (uint32_t)(kDefer - 32))) {
 #if defined(PFAC_EXP) && PFAC_EXP == 2
-        dcount = 0;  // experiment: no walks
-        return;
+            c += dpos[0] == 0xFFFFFFFFu + (dsnip == nullptr);  // experiment: no walks
+#else
+            const uint2 r = walk_deferred(&a, s, range_lo, dpos, dsnip, dcount, hits, n_hits);
+            c += r.x;
+            n_hits = r.y;
 #endif
-        const uint2 r = walk_deferred(&a, s, range_lo, dpos, dsnip, dcount, hits, n_hits);
-        c += r.x;
-        n_hits = r.y;
-        dcount = 0;
-    };
-    for (uint64_t i = 0; i < nr; i += kGroup) {
-#pragma unroll 1
-        for (int g = 0; g < kGroup; ++g)  // refill the slots of the previous group
-            if (i + kSlots - kGroup + g < nr) issue(i + kSlots - kGroup + g);
-        const uint32_t ng = nr - i < (uint64_t)kGroup ? (uint32_t)(nr - i) : (uint32_t)kGroup;
-        const uint64_t gbase = (r_begin + i) * kRound;
-        // the 4 bytes after the group (lane 31's last 4-gram window) come from
-        // global memory: prefetched now, so the group never waits for the next
-        // round (which was only just issued) -- rounds land a full group ahead
-        uint32_t tail4 = 0;
-        if (lane == 31) {
-            const uint64_t j0 = gbase + (uint64_t)ng * kRound;
-            if (j0 + 4 <= a.readable && a.aligned) {
-                tail4 = __ldg(reinterpret_cast<const uint32_t *>(a.text + j0));
-            } else {
-                for (int b = 0; b < 4; ++b)
-                    if (j0 + b < a.readable) tail4 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
-            }
+            dcount = 0;
         }
-        for (uint32_t q = 0; q < ng; ++q) mbar_wait(&bars[(i + q) % kSlots], (uint32_t)(((i + q) / kSlots) & 1));
-        const RingText tx{ring, (uint32_t)(i % kSlots), ng * (uint32_t)kSlotBytes, clamp32(a.readable - gbase),
-                          a.text + gbase};
-
+        if (i == nr) break;
+        const uint32_t rel = i * (uint32_t)kRound;  // round start relative to range_lo
+        if (!more) {
+            const uint64_t rbase = range_lo + rel;
+            const uint8_t *p0 = ring + slot * kSlotBytes;
+            __syncwarp();  // every lane's reads of round i-1's slot precede its refill
+            if (i + kSlots - 1 < nr) issue(i + kSlots - 1, slot2);
+            uint32_t tail4 = 0;  // the 4 bytes after this round (lane 31's last windows)
+            if (lane == 31) {
+                const uint64_t j0 = rbase + kRound;
+                if (j0 + 4 <= a.readable && a.aligned) {
+                    tail4 = __ldg(reinterpret_cast<const uint32_t *>(a.text + j0));
+                } else {
+                    for (int b = 0; b < 4; ++b)
+                        if (j0 + b < a.readable) tail4 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
+                }
+            }
+            mbar_wait(&bars[slot], phase);
 #ifdef PFAC_STREAM_ONLY
-        // experiment (tools/timing.py): stream the text through the ring only
-        if (lane == 0 && ring[(i % kSlots) * kSlotBytes] == 0xFF && gbase == 0) c++;
-        __syncwarp();
-        continue;
-#endif
-        // ---- stage 1: filter over the lane's starts of each round (one copy
-        // of the filter code: the group loop is not unrolled)
-        uint32_t surv0 = 0, surv1 = 0;
+            if (lane == 0 && p0[0] == 0xFF && rbase == 0) c++;
+            uint32_t pending = 0;
+#else
+            // ---- stage 1: filter over the lane's 32 starts
+            uint32_t wv[kWv];
 #pragma unroll
-        for (int g = 0; g < kGroup; ++g) {
-            uint32_t sv = 0;
-            if ((uint32_t)g < ng) {
-                const uint8_t *p0 = ring + ((i + g) % kSlots) * kSlotBytes;
-                uint32_t wv[kWv];
-#pragma unroll
-                for (int q = 0; q < kPerLane / 16; ++q) {
-                    const uint4 t4 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * q);
-                    wv[4 * q] = t4.x;
-                    wv[4 * q + 1] = t4.y;
-                    wv[4 * q + 2] = t4.z;
-                    wv[4 * q + 3] = t4.w;
-                }
-                uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
-                const uint64_t rbase = gbase + (uint64_t)g * kRound;
-                if (lane == 31)
-                    w8 = (uint32_t)g + 1 < ng ? *reinterpret_cast<const uint32_t *>(ring + ((i + g + 1) % kSlots) * kSlotBytes)
-                                              : tail4;
-                wv[kWv - 1] = w8;
-                const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
-                sv = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
-                if (lbase + kPerLane > lim) {
-                    const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
-                    sv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
-                }
+            for (int q = 0; q < kPerLane / 16; ++q) {
+                const uint4 t4 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * q);
+                wv[4 * q] = t4.x;
+                wv[4 * q + 1] = t4.y;
+                wv[4 * q + 2] = t4.z;
+                wv[4 * q + 3] = t4.w;
             }
-            if (g == 0) surv0 = sv; else surv1 = sv;
-        }
-        const uint32_t surv[kGroup] = {surv0, surv1};
-
+            const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+            wv[kWv - 1] = lane == 31 ? tail4 : w8;
+            uint32_t pending = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
+            const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
+            if (lbase + kPerLane > lim) {
+                const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
+                pending &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
+            }
+#endif
 #if defined(PFAC_EXP) && PFAC_EXP == 1
-        // experiment: filter only (survivor masks folded into a dummy count)
-        c += (surv0 ^ surv1) == 0xDEADBEEFu;
-        __syncwarp();
-        continue;
+            c += pending == 0xDEADBEEFu;  // experiment: filter only
+            pending = 0;
 #endif
-        // ---- stage 2: compact survivors (position order: round, lane, start)
-        // into the warp queue; a cheap first check (root table + level-1
-        // bitmapped node) kills most of them with full warps; the
-        // rest are deferred, in order, with a text snippet and walked in
-        // batches of >= 32 (the deep walk cost is paid once per batch)
-        static_assert(kGroup == 2, "packed two-round scan below");
-        const uint32_t ns0 = __popc(surv[0]), ns1 = __popc(surv[1]);
-        if (__any_sync(0xffffffffu, (ns0 | ns1) != 0)) {
-            uint32_t tot;
-            const uint32_t ex = warp_excl_scan(ns0 | (ns1 << 16), lane, &tot);  // both rounds in one scan
-            const uint32_t t0 = tot & 0xFFFFu, stot = t0 + (tot >> 16);
-            const uint32_t st[2] = {ex & 0xFFFFu, t0 + (ex >> 16)};
-            for (uint32_t qb = 0; qb < stot; qb += kQueue) {
-#pragma unroll
-                for (int g = 0; g < kGroup; ++g) {
-                    const uint32_t ns = g == 0 ? ns0 : ns1;
-                    if (ns && st[g] < qb + kQueue && st[g] + ns > qb) {
-                        uint32_t idx = st[g];
-                        for (uint32_t m = surv[g]; m; m &= m - 1, ++idx)
-                            if (idx >= qb && idx < qb + kQueue)
-                                queue[idx - qb] = (uint16_t)(g * kRound + lane * kPerLane + (__ffs(m) - 1));
-                    }
+            // ---- stage 2: 2-gram prefix test of the lane's survivors
+            const uint32_t rlim = a.readable > rbase ? clamp32(a.readable - rbase) : 0u;  // readable bytes from rbase
+            km = 0;
+            while (pending) {
+                const uint32_t k = __ffs(pending) - 1;
+                const uint32_t off = lane * kPerLane + k;
+                const uint32_t b0 = p0[off];
+                uint32_t keep;
+                if (off + 1 < rlim) {
+                    const uint32_t b1 = off + 1 < (uint32_t)kRound ? p0[off + 1] : (tail4 & 0xFFu);
+                    keep = (s_pair[b0 * 8 + (b1 >> 5)] >> (b1 & 31)) & 1u;
+                } else {
+                    keep = s.root[b0] != 0u;  // last readable byte: let the walk decide
                 }
-                __syncwarp();
-                const uint32_t n = stot - qb < (uint32_t)kQueue ? stot - qb : (uint32_t)kQueue;
-                for (uint32_t j0 = 0; j0 < n; j0 += 32) {
-                    if (dcount > kDefer - 32) flush();
-                    const uint32_t j = j0 + lane;
-                    uint32_t off = 0;
-                    bool keep = false;
-                    if (j < n) {
-                        off = queue[j];
-                        const uint32_t v = s.root[tx.at(off)];
-                        if (v != 0) {
-                            const uint32_t w = node_word(a, s, v);
-                            keep = (w & (kTermBit | kTailBit)) != 0;
-                            if (!keep && off + 1 < tx.end) {
-                                const uint32_t c1 = tx.at(off + 1);
-                                keep = (s.bm[(v - 1) * 10 + (c1 >> 5)] >> (c1 & 31)) & 1u;
-                            }
-                        }
-                    }
-                    const uint32_t kb = __ballot_sync(0xffffffffu, keep);
-                    if (keep) {  // defer (order kept: ballot prefix)
-                        const uint32_t d = dcount + __popc(kb & ((1u << lane) - 1u));
-                        dpos[d] = (uint32_t)(gbase - range_lo) + off;
-                    }
-                    dcount += __popc(kb);
-                }
-                __syncwarp();
+                km |= keep << k;
+                pending &= pending - 1;
             }
         }
-        if (dcount >= 32) flush();
-        __syncwarp();
+        // ---- queue this round's kept starts in position order (as many as fit)
+        more = false;
+        if (__any_sync(0xffffffffu, km != 0)) {
+            uint32_t tot;
+            uint32_t r = warp_excl_scan(__popc(km), lane, &tot);
+            const uint32_t room = (uint32_t)kDefer - dcount;
+            while (km && r < room) {
+                dpos[dcount + r] = rel + lane * kPerLane + (__ffs(km) - 1);
+                km &= km - 1;
+                ++r;
+            }
+            __syncwarp();
+            more = tot > room;
+            dcount += more ? room : tot;
+        }
+        if (!more) {
+            ++i;
+            slot = slot + 1 == kSlots ? 0 : slot + 1;
+            phase ^= slot == 0;
+            slot2 = slot2 + 1 == kSlots ? 0 : slot2 + 1;
+        }
     }
-    if (dcount) flush();
     STAMP(2);
     uint64_t total;
     {
@@ -835,10 +795,13 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             const uint64_t rbase = (r_begin + i) * kRound;
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
             uint32_t wv[kWv];
-            for (int q = 0; q < kWv; ++q) wv[q] = 0;
-#pragma unroll 1
-            for (int b = 0; b < 4 * kWv; ++b)
-                if (lbase + b < a.readable) wv[b >> 2] |= (uint32_t)__ldg(a.text + lbase + b) << (8 * (b & 3));
+#pragma unroll
+            for (int q = 0; q < kWv; ++q) {
+                wv[q] = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (lbase + 4 * q + b < a.readable) wv[q] |= (uint32_t)__ldg(a.text + lbase + 4 * q + b) << (8 * b);
+            }
             uint32_t surv = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
@@ -1012,16 +975,20 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
     const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
-    const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + kWarps * kQueue * 2 + 1024 +
-                           kWarps * kDefer * 20 +
+    const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
+                           kWarps * kDefer * 20 + 8192 +
                            align16(40 * B) + 8 * (kWarps + 1) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
         return kStatusLimit;
     }
     const uint32_t rest = (uint32_t)di.max_smem_optin - fixed;
-    // priority: ring (in `fixed`) > hot trie > filter replicas (cut bank conflicts)
-    const uint32_t trie_budget = rest - filter_words * 4;
+    // priority: ring (in `fixed`) > 4 filter copies (bank conflicts of the
+    // stage-1 loads) > hot trie > more filter copies
+    uint32_t rep0 = 0;
+    while (rep0 < 2 && filter_words * 4 * (2u << rep0) <= kFilterCap && filter_words * 4 * (2u << rep0) + 8192 <= rest)
+        rep0++;
+    const uint32_t trie_budget = rest - (filter_words * 4 << rep0);
     // H = largest BFS prefix whose node words [0, H], labels [0, row_ptr[H]),
     // tail bitmap/rank words and tail records + bytes (tails of nodes < H)
     // all fit the budget
@@ -1053,8 +1020,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const uint32_t EH = host_node[H] & kEdgeMask;
     const uint32_t TH = tails_below(H);
     const uint32_t TBH = tbytes_below(TH);
-    const uint32_t left = rest - (uint32_t)hot_bytes(H);  // >= filter_words * 4
-    uint32_t rep_log2 = 0;
+    const uint32_t left = rest - (uint32_t)hot_bytes(H);  // >= filter_words * 4 << rep0
+    uint32_t rep_log2 = rep0;
     while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= (left < kFilterCap ? left : kFilterCap)) rep_log2++;
     const uint32_t filter_bytes = filter_words * 4 << rep_log2;
 
@@ -1069,8 +1036,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.off_warp = o;   o += 8 * (kWarps + 1);
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
-    a.off_queue = o;  o += kWarps * kQueue * 2;
-    a.off_defer = o;  o += kWarps * kDefer * 20;  // per warp: u32 pos[kDefer] + uint4 snippet[kDefer]
+    a.off_defer = o;  o += kWarps * kDefer * 20;  // per warp: u32 pos[kDefer], uint4 snippet[kDefer]
+    a.off_pair = o;   o += 8192;                 // 2-gram prefix table [256][8] words
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
     a.off_label = o;  o += align16(EH);

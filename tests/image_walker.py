@@ -61,16 +61,20 @@ def _block(h, x3):
     return ((x3 * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
 
 
+def _pair_word(h, x3):
+    return ((x3 * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 5))
+
+
 def filter_pass(h, key, start=0):
     """Does the start whose first d bytes are `key` pass the filter?  Kind 2
     (pair filter) depends on the start's parity (image.h)."""
     if h["filter_kind"] == 2:
         f = h["filter"]
         if start % 2 == 0:  # first of the pair: shared bytes 1..3, own byte 0
-            b = _block(h, key >> 8)
-            return bool((int(f[2 * b]) >> (31 - (key & 31))) & 1)
-        b = _block(h, key & 0xFFFFFF)  # second: shared bytes are the start's bytes 0..2, own byte 3
-        return bool((int(f[2 * b + 1]) >> (31 - ((key >> 24) & 31))) & 1)
+            w = int(f[_pair_word(h, key >> 8)])
+            return bool((w >> (31 - (key & 31))) & 1)
+        w = int(f[_pair_word(h, key & 0xFFFFFF)])  # second: shared bytes are the start's bytes 0..2, own byte 3
+        return bool((w >> (31 - ((key >> 24) & 31))) & 1)
     return all((int(h["filter"][i >> 5]) >> (i & 31)) & 1 for i in filter_bits(h, key))
 
 
