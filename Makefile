@@ -43,3 +43,13 @@ clean:
 	rm -f gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so $(EXPLIBS)
 
 .PHONY: all clean
+
+# layout variants for A/B timing (tools/variants.sh)
+VARLIBS := $(PKG)/libpfac_v_s0.so $(PKG)/libpfac_v_e0.so $(PKG)/libpfac_v_s0e0.so
+$(PKG)/libpfac_v_s0.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_STATIC_NUM=0 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_v_e0.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_SLOT_EXTRA=0 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_v_s0e0.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_STATIC_NUM=0 -DPFAC_SLOT_EXTRA=0 -shared -o $@ $(CSRC) -lcudart
+variants: $(VARLIBS)

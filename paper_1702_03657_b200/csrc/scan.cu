@@ -46,14 +46,22 @@ constexpr int kWarps = 32;
 constexpr int kThreads = kWarps * 32;
 constexpr int kPerLane = 32;           // consecutive starts per lane per round
 constexpr int kRound = 32 * kPerLane;  // 1024 starts per warp round
+constexpr int kRoundLog2 = 10;
+static_assert(kRound == 1 << kRoundLog2, "");
 constexpr int kWv = kPerLane / 4 + 1;  // text words a lane needs (its starts + 3 bytes)
 constexpr int kSlots = 3;              // text ring depth per warp (kSlots-1 rounds in flight)
-constexpr int kSlotBytes = kRound;     // one round of text per slot
+#ifndef PFAC_SLOT_EXTRA
+#define PFAC_SLOT_EXTRA 16
+#endif
+#ifndef PFAC_STATIC_NUM
+#define PFAC_STATIC_NUM 3  // share of a CTA's rounds assigned statically, in quarters
+#endif
+constexpr int kSlotBytes = kRound + PFAC_SLOT_EXTRA;  // one round of text (+ the next 16 bytes: the last windows)
 static_assert(kSlots >= 2, "ring");
 constexpr int kMaxCtas = 1024;
 constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated filter
 constexpr uint32_t kHotCap = 24576;  // hot-trie smem when the trie does not fit (rest left to L1)
-constexpr int kDefer = 64;             // per-warp deferred-walk queue (offset + 16-byte snippet)
+constexpr int kDefer = 64;             // per-warp deferred-walk queue (start offsets)
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
@@ -79,7 +87,9 @@ struct ScanArgs {
     uint2 *hits;                    // [warps][hit_cap] (start offset within the warp's range, terminal index)
     uint32_t hit_cap;
     uint32_t parity;                // barrier counter used by this launch
-    uint64_t rounds_per_warp;
+    uint64_t rounds_per_cta;
+    unsigned long long *round_val;  // [n_rounds] pid count of the round, then its first row within the CTA
+    uint32_t *round_owner;          // [n_rounds] global warp that scanned the round
     // shared-memory layout (bytes from the dynamic smem base; filter at 0)
     uint32_t filter_words;          // words of the (unreplicated) filter
     uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
@@ -207,35 +217,23 @@ __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, u
     return e < a.hot_edges ? (uint32_t)s.label[e] : (uint32_t)__ldg(a.t.label + e);
 }
 
+// Text of a walk read from global memory (L1/L2): `g` = text + start,
+// `end` = readable bytes from there (clamped to 32 bits).
 struct GlobalText {
     const uint8_t *g;
     uint32_t end;
+    uint32_t aligned;  // the text pointer is 16-byte aligned
     __device__ __forceinline__ uint32_t at(uint32_t r) const { return __ldg(g + r); }
+    // bytes r..r+3 (little-endian; zero past `end`)
     __device__ __forceinline__ uint32_t at4(uint32_t r) const {
+        const uintptr_t ad = reinterpret_cast<uintptr_t>(g + r);
+        if (aligned && r + 8 <= end) {  // two aligned words hold the four bytes
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(ad & ~(uintptr_t)3);
+            return __funnelshift_r(__ldg(w), __ldg(w + 1), 8 * (uint32_t)(ad & 3));
+        }
         uint32_t x = 0;
         for (int b = 0; b < 4; ++b)
             if (r + b < end) x |= (uint32_t)__ldg(g + r + b) << (8 * b);
-        return x;
-    }
-};
-
-// Text of a deferred survivor: the first kSnip bytes from its start were copied
-// into shared memory when it was deferred (the ring slot may be reused by the
-// time it is walked); later bytes come from global memory.
-constexpr uint32_t kSnip = 16;
-struct SnipText {
-    const uint8_t *snip;  // kSnip bytes (shared memory)
-    const uint8_t *g;     // text + start
-    uint32_t end;
-    __device__ __forceinline__ uint32_t at(uint32_t r) const { return r < kSnip ? snip[r] : __ldg(g + r); }
-    __device__ __forceinline__ uint32_t at4(uint32_t r) const {
-        uint32_t x = 0;
-        if (r + 4 <= kSnip) {
-            const uint32_t *w = reinterpret_cast<const uint32_t *>(snip);
-            return __funnelshift_r(w[r >> 2], w[(r >> 2) + ((r & 3) ? 1 : 0)], 8 * (r & 3));
-        }
-        for (int b = 0; b < 4; ++b)
-            if (r + b < end) x |= at(r + b) << (8 * b);
         return x;
     }
 };
@@ -411,50 +409,26 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
     return surv;
 }
 
-// Walk the deferred survivors dpos[0, n) (position order) with full warps;
-// hits are appended to the warp's hit list in the same order.  Returns (pid
-// count added by this lane, new hit count).
-__device__ __forceinline__ uint2 walk_deferred(const ScanArgs *ap, const Smem s, uint64_t range_lo, const uint32_t *dpos,
-                                            uint4 *dsnip, uint32_t n, uint2 *hits, uint32_t n_hits) {
+// Walk the deferred starts dpos[0, n) (offsets from the CTA's first start,
+// position order) with full warps; hits are appended to the warp's hit list in
+// the same order and their pid counts added to their rounds' counts.  Returns
+// the new hit count.
+__device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem s, uint64_t cta_lo, uint64_t cta_round0,
+                                                  const uint32_t *dpos, uint32_t n, uint2 *hits, uint32_t n_hits) {
     const ScanArgs &a = *ap;
     const int lane = threadIdx.x & 31;
-    uint32_t c = 0;
     __syncwarp();
     for (uint32_t j0 = 0; j0 < n; j0 += 32) {
         const uint32_t j = j0 + lane;
         uint32_t p = 0, tn = kNone;
         if (j < n) {
             p = dpos[j];
-            const uint64_t gp = range_lo + p;
-            // the ring slot may be gone: copy the first kSnip bytes from
-            // global memory (L2) into the lane's snippet, walk from there
-            uint8_t *sn = reinterpret_cast<uint8_t *>(dsnip + j);
-            if ((reinterpret_cast<uintptr_t>(a.text) & 3) == 0) {
-                const uint64_t gl = gp & ~3ull;
-                uint32_t w[5];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) {
-                    const uint64_t o = gl + 4 * q;
-                    w[q] = o + 4 <= a.readable ? __ldg(reinterpret_cast<const uint32_t *>(a.text + o)) : 0u;
-                    if (o < a.readable && o + 4 > a.readable) {  // ragged text end
-                        for (int b = 0; b < 4; ++b)
-                            if (o + b < a.readable) w[q] |= (uint32_t)__ldg(a.text + o + b) << (8 * b);
-                    }
-                }
-                const uint32_t sh = 8 * (uint32_t)(gp & 3);
-                uint4 v4;
-                v4.x = __funnelshift_r(w[0], w[1], sh);
-                v4.y = __funnelshift_r(w[1], w[2], sh);
-                v4.z = __funnelshift_r(w[2], w[3], sh);
-                v4.w = __funnelshift_r(w[3], w[4], sh);
-                *reinterpret_cast<uint4 *>(sn) = v4;
-            } else {  // unaligned text pointer: bytes
-#pragma unroll 1
-                for (uint32_t b = 0; b < kSnip; ++b) sn[b] = gp + b < a.readable ? __ldg(a.text + gp + b) : 0;
-            }
-            const SnipText st{sn, a.text + gp, clamp32(a.readable - gp)};
-            tn = walk(a, s, st, 0u);
-            if (tn != kNone) c += s.out_ptr[tn + 1] - s.out_ptr[tn];
+            const uint64_t gp = cta_lo + p;
+            const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
+            tn = walk(a, s, gt, 0u);
+            if (tn != kNone)
+                atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2),
+                          (unsigned long long)(s.out_ptr[tn + 1] - s.out_ptr[tn]));
         }
         const bool hit = tn != kNone;
         const uint32_t hb = __ballot_sync(0xffffffffu, hit);
@@ -465,7 +439,7 @@ __device__ __forceinline__ uint2 walk_deferred(const ScanArgs *ap, const Smem s,
         n_hits += __popc(hb);
     }
     __syncwarp();
-    return make_uint2(c, n_hits);
+    return n_hits;
 }
 
 template <int Kind>
@@ -518,40 +492,81 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     const uint32_t gram = a.t.gram;
     const uint64_t lim = (a.readable + 1 >= gram && a.readable + 1 - gram < a.n_starts) ? a.readable + 1 - gram
                                                                                         : a.n_starts;
-    // ---- this warp's contiguous range of rounds
-    const uint64_t gw = (uint64_t)blockIdx.x * kWarps + warp;
+    // ---- this CTA's contiguous range of rounds; its warps take rounds from
+    // a shared counter (dynamic within the CTA: warps whose walks run long
+    // take fewer rounds), in increasing order per warp
+    const uint32_t gw = blockIdx.x * kWarps + warp;
     const uint64_t n_rounds = (a.n_starts + kRound - 1) / kRound;
-    const uint64_t r_begin = gw * a.rounds_per_warp < n_rounds ? gw * a.rounds_per_warp : n_rounds;
-    const uint64_t r_end = r_begin + a.rounds_per_warp < n_rounds ? r_begin + a.rounds_per_warp : n_rounds;
-    const uint64_t range_lo = r_begin * kRound;
-    uint2 *hits = a.hits + gw * a.hit_cap;
+    const uint64_t cta_round0 = (uint64_t)blockIdx.x * a.rounds_per_cta < n_rounds
+                                    ? (uint64_t)blockIdx.x * a.rounds_per_cta : n_rounds;
+    const uint32_t n_local = (uint32_t)((cta_round0 + a.rounds_per_cta < n_rounds ? cta_round0 + a.rounds_per_cta
+                                                                                    : n_rounds) - cta_round0);
+    const uint64_t cta_lo = cta_round0 * kRound;
+    uint2 *hits = a.hits + (uint64_t)gw * a.hit_cap;
+    uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 1);  // round counter of the CTA
 
-    // Fill ring slot `slot` with round i of this warp's range (one 1 KiB TMA
-    // bulk copy; the unaligned-text / ragged-tail path copies with the lanes).
-    auto issue = [&](uint32_t i, uint32_t slot) {
-        uint8_t *dst = ring + slot * kSlotBytes;
-        const uint64_t lo = range_lo + (uint64_t)i * kRound;
-        if (a.aligned && lo + kSlotBytes <= a.readable) {
+    // The warp's j-th round: rounds warp + 32j while j < n_static (static,
+    // interleaved), then from the CTA's shared counter (dynamic: warps whose
+    // walks ran long take fewer of the last rounds).  Increasing per warp;
+    // warp-uniform; >= n_local when none is left.
+    const uint32_t n_static = (n_local * PFAC_STATIC_NUM / 4) / kWarps;
+    uint32_t taken = 0;
+    auto take = [&]() -> uint32_t {
+        uint32_t r;
+        if (taken < n_static) {
+            r = warp + kWarps * taken;
+        } else {
+            r = 0;
             if (lane == 0) {
-                fence_proxy_async_smem();  // prior generic reads of the slot precede the async write
-                mbar_arrive_expect_tx(&bars[slot], kSlotBytes);
-                bulk_g2s(dst, a.text + lo, kSlotBytes, &bars[slot], policy);
+                asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(s_next)) : "memory");
             }
-        } else {  // cold: lanes copy, zero-fill past `readable`
-            const uint64_t avail = lo < a.readable ? a.readable - lo : 0;
+            r = kWarps * n_static + __shfl_sync(0xffffffffu, r, 0);
+        }
+        ++taken;
+        if (lane == 0 && r < n_local) a.round_owner[cta_round0 + r] = gw;
+        return r;
+    };
+    // Fill ring slot `slot` with local round r: one TMA bulk copy of the
+    // readable 16-byte-aligned part; the lanes copy the rest (the text's last
+    // bytes, zero-filled past `readable`, or everything when the text pointer
+    // is not 16-byte aligned), all loads issued before the stores.
+    auto issue = [&](uint32_t r, uint32_t slot) {
+        uint8_t *dst = ring + slot * kSlotBytes;
+        const uint64_t lo = cta_lo + (uint64_t)r * kRound;
+        const uint32_t avail = lo < a.readable ? (uint32_t)min(a.readable - lo, (uint64_t)kSlotBytes) : 0u;
+        const uint32_t nbulk = a.aligned ? (avail & ~15u) : 0u;
+        if (nbulk < (uint32_t)kSlotBytes) {  // cold: only the text's last round(s) / unaligned text
 #pragma unroll 1
-            for (uint32_t o = lane; o < (uint32_t)kSlotBytes; o += 32)
-                dst[o] = o < avail ? __ldg(a.text + lo + o) : (uint8_t)0;
+            for (uint32_t o0 = nbulk; o0 < (uint32_t)kSlotBytes; o0 += 8 * 32) {  // 8 loads in flight per lane
+                uint32_t v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t o = o0 + lane + 32 * q;
+                    v[q] = o < avail ? (uint32_t)__ldg(a.text + lo + o) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t o = o0 + lane + 32 * q;
+                    if (o < (uint32_t)kSlotBytes) dst[o] = (uint8_t)v[q];
+                }
+            }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bars[slot]);
+        }
+        if (lane == 0) {
+            if (nbulk) {
+                fence_proxy_async_smem();  // prior generic accesses of the slot precede the async write
+                mbar_arrive_expect_tx(&bars[slot], nbulk);
+                bulk_g2s(dst, a.text + lo, nbulk, &bars[slot], policy);
+            } else {
+                mbar_arrive(&bars[slot]);
+            }
         }
     };
 
-    // ---- start streaming this warp's text, then stage the tables (TMA bulk
-    // copies of the image sections; the filter is replicated from 16-byte loads)
-    const uint32_t nr = (uint32_t)(r_end - r_begin);
-    for (uint32_t i = 0; i < nr && i < kSlots - 1; ++i) issue(i, i);
+    // ---- stage the tables (TMA bulk copies of the image sections; the
+    // filter is replicated from 8/4-byte loads), then start streaming
     if (tid == 0) {
+        *s_next = 0u;
         const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
                        nb_l1 = align16(40 * a.n_level1);
         const uint32_t nb_w = align16(4 * a.hot_words), nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
@@ -569,13 +584,34 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     }
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
+        // (four loads in flight per thread: the image is cold in L2 here)
         const uint32_t nu = (Kind == 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
         if (Kind == 1) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
-            for (uint32_t j = tid; j < nu; j += kThreads) d[j] = __ldg(src + (j >> a.rep_log2));
+            for (uint32_t j0 = 0; j0 < nu; j0 += 4 * kThreads) {
+                uint2 v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t j = j0 + tid + q * kThreads;
+                    v[q] = j < nu ? __ldg(src + (j >> a.rep_log2)) : make_uint2(0, 0);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (j0 + tid + q * kThreads < nu) d[j0 + tid + q * kThreads] = v[q];
+            }
         } else {
-            for (uint32_t j = tid; j < nu; j += kThreads) s_filter[j] = __ldg(a.t.filter + (j >> a.rep_log2));
+            for (uint32_t j0 = 0; j0 < nu; j0 += 4 * kThreads) {
+                uint32_t v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t j = j0 + tid + q * kThreads;
+                    v[q] = j < nu ? __ldg(a.t.filter + (j >> a.rep_log2)) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (j0 + tid + q * kThreads < nu) s_filter[j0 + tid + q * kThreads] = v[q];
+            }
         }
         // terminal tables (pid-list offsets, kept terminal ids) when small
         if (a.off_terms) {
@@ -585,7 +621,17 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             for (uint32_t j = tid; j < a.t.n_kept_terminals; j += kThreads) so[n_op + j] = __ldg(a.t.term_node + j);
         }
     }
+    for (uint32_t r = tid; r < n_local; r += kThreads) a.round_val[cta_round0 + r] = 0ull;  // pid counts
+    __syncthreads();  // the round counter and counts are initialised
+    // the first kSlots-1 rounds of this warp start streaming
+    uint32_t rid[kSlots];
+#pragma unroll
+    for (int q = 0; q < kSlots - 1; ++q) {
+        rid[q] = take();
+        if (rid[q] < n_local) issue(rid[q], q);
+    }
     mbar_wait(sbar, 0);
+    STAMP(5);
     __syncthreads();
     // 2-gram prefix table: word (b0, q) bit j <=> the walk from a start with
     // bytes (b0, 32q + j) gets past level 1 (or b0's node already is a
@@ -594,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     for (uint32_t j = tid; j < 2048; j += kThreads) {
         const uint32_t v = s_root[j >> 3];
         uint32_t wd = 0;
-        if (v != 0) wd = (__ldg(a.t.node + v) & (kTermBit | kTailBit)) ? 0xFFFFFFFFu : s_bm[(v - 1) * 10 + (j & 7)];
+        if (v != 0) wd = (node_word(a, s, v) & (kTermBit | kTailBit)) ? 0xFFFFFFFFu : s_bm[(v - 1) * 10 + (j & 7)];
         s_pair[j] = wd;
     }
     __syncthreads();
@@ -607,36 +653,65 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // root's children and their level-1 bitmapped nodes): bytes
     // (b0, b1) begin a pattern path, or b0 alone already reaches a terminal or
     // tail.  The kept starts are appended to the warp's deferred queue in
-    // position order (lane-major = position order) and walked in full-warp
-    // batches whenever the queue may not take another round.
-    uint32_t c = 0;       // pattern ids matched by this lane's starts
+    // position order (lane-major = position order; a warp's rounds increase)
+    // and walked in full-warp batches whenever the queue may not take another
+    // round.
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
     uint32_t dcount = 0;  // deferred starts in the queue (warp-uniform)
-    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * (kDefer * 5);
-    uint4 *dsnip = reinterpret_cast<uint4 *>(dpos + kDefer);
-    uint32_t slot = 0, phase = 0, slot2 = kSlots - 1;  // ring slot of round i, its parity; slot of round i+kSlots-1
-    uint32_t km = 0;     // this lane's kept starts of round i not yet queued
-    bool more = false;   // round i still has kept starts to queue (warp-uniform)
-    uint32_t i = 0;
+    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * kDefer;
+    uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
+    uint32_t km = 0;     // this lane's kept starts of the current round not yet queued
+    bool more = false;   // the current round still has kept starts to queue (warp-uniform)
     for (;;) {
+        const bool done = rid[0] >= n_local;
         // ---- the single batch-walk site
-        if (dcount != 0 && (i == nr || more || dcount > (uint32_t)(kDefer - 32))) {
+        if (dcount != 0 && (done || more || dcount > (uint32_t)(kDefer - 32))) {
 #if defined(PFAC_EXP) && PFAC_EXP == 2
-            c += dpos[0] == 0xFFFFFFFFu + (dsnip == nullptr);  // experiment: no walks
+            if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
-            const uint2 r = walk_deferred(&a, s, range_lo, dpos, dsnip, dcount, hits, n_hits);
-            c += r.x;
-            n_hits = r.y;
+            n_hits = walk_deferred(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits);
 #endif
             dcount = 0;
         }
-        if (i == nr) break;
-        const uint32_t rel = i * (uint32_t)kRound;  // round start relative to range_lo
+        if (done) break;
+        const uint32_t rel = rid[0] * (uint32_t)kRound;  // round start relative to cta_lo
         if (!more) {
-            const uint64_t rbase = range_lo + rel;
+            const uint64_t rbase = cta_lo + rel;
             const uint8_t *p0 = ring + slot * kSlotBytes;
-            __syncwarp();  // every lane's reads of round i-1's slot precede its refill
-            if (i + kSlots - 1 < nr) issue(i + kSlots - 1, slot2);
+            // refill the slot of the previous round with the next round taken
+            __syncwarp();  // every lane's reads of that slot precede its refill
+            rid[kSlots - 1] = take();
+            if (rid[kSlots - 1] < n_local) issue(rid[kSlots - 1], slot == 0 ? kSlots - 1 : slot - 1);
+            mbar_wait(&bars[slot], phase);
+#ifdef PFAC_TIMING
+            if (taken == kSlots) STAMP(6);  // the first round's text is in
+#endif
+#ifdef PFAC_STREAM_ONLY
+            uint32_t pending = 0;
+            if (p0[lane] == 0xFF && a.pos_base == ~0ull) n_hits++;  // keeps the loads
+#else
+            // ---- stage 1: filter over the lane's 32 starts.  The lane's 32
+            // bytes are two 16-byte loads; lanes 4-7 of each group of 8 take
+            // the halves in the other order so that every load covers all 32
+            // banks once (4 wavefronts, not 8).
+            uint32_t wv[kWv];
+            {
+                const uint32_t sw = (lane >> 2) & 1u;
+                const uint4 h0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * sw);
+                const uint4 h1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * (sw ^ 1u));
+                wv[0] = sw ? h1.x : h0.x;
+                wv[1] = sw ? h1.y : h0.y;
+                wv[2] = sw ? h1.z : h0.z;
+                wv[3] = sw ? h1.w : h0.w;
+                wv[4] = sw ? h0.x : h1.x;
+                wv[5] = sw ? h0.y : h1.y;
+                wv[6] = sw ? h0.z : h1.z;
+                wv[7] = sw ? h0.w : h1.w;
+            }
+            const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+#if PFAC_SLOT_EXTRA
+            const uint32_t tail4 = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound) : 0u;
+#else
             uint32_t tail4 = 0;  // the 4 bytes after this round (lane 31's last windows)
             if (lane == 31) {
                 const uint64_t j0 = rbase + kRound;
@@ -647,22 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                         if (j0 + b < a.readable) tail4 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
                 }
             }
-            mbar_wait(&bars[slot], phase);
-#ifdef PFAC_STREAM_ONLY
-            if (lane == 0 && p0[0] == 0xFF && rbase == 0) c++;
-            uint32_t pending = 0;
-#else
-            // ---- stage 1: filter over the lane's 32 starts
-            uint32_t wv[kWv];
-#pragma unroll
-            for (int q = 0; q < kPerLane / 16; ++q) {
-                const uint4 t4 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * q);
-                wv[4 * q] = t4.x;
-                wv[4 * q + 1] = t4.y;
-                wv[4 * q + 2] = t4.z;
-                wv[4 * q + 3] = t4.w;
-            }
-            const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
+#endif
             wv[kWv - 1] = lane == 31 ? tail4 : w8;
             uint32_t pending = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
@@ -672,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             }
 #endif
 #if defined(PFAC_EXP) && PFAC_EXP == 1
-            c += pending == 0xDEADBEEFu;  // experiment: filter only
+            if (pending == 0xDEADBEEFu && a.pos_base == ~0ull) n_hits++;  // experiment: filter only
             pending = 0;
 #endif
             // ---- stage 2: 2-gram prefix test of the lane's survivors
@@ -684,7 +744,11 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 const uint32_t b0 = p0[off];
                 uint32_t keep;
                 if (off + 1 < rlim) {
+#if PFAC_SLOT_EXTRA
+                    const uint32_t b1 = p0[off + 1];  // the slot holds 16 bytes past the round
+#else
                     const uint32_t b1 = off + 1 < (uint32_t)kRound ? p0[off + 1] : (tail4 & 0xFFu);
+#endif
                     keep = (s_pair[b0 * 8 + (b1 >> 5)] >> (b1 & 31)) & 1u;
                 } else {
                     keep = s.root[b0] != 0u;  // last readable byte: let the walk decide
@@ -709,34 +773,49 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             dcount += more ? room : tot;
         }
         if (!more) {
-            ++i;
+#pragma unroll
+            for (int q = 0; q < kSlots - 1; ++q) rid[q] = rid[q + 1];
             slot = slot + 1 == kSlots ? 0 : slot + 1;
             phase ^= slot == 0;
-            slot2 = slot2 + 1 == kSlots ? 0 : slot2 + 1;
         }
     }
     STAMP(2);
-    uint64_t total;
-    {
-        uint32_t ct;
-        warp_excl_scan(c, lane, &ct);
-        total = ct;
-    }
 
     // ================================================= phase 2: offsets
-    if (lane == 0) s_wtot[warp] = total;
-    __syncthreads();
-    if (warp == 0) {
-        const unsigned long long v = lane < kWarps ? s_wtot[lane] : 0ull;
+    // Exclusive scan of the CTA's round counts in place (round_val becomes the
+    // round's first row relative to the CTA), CTA total -> grid barrier ->
+    // prefix over the CTA totals.
+    __syncthreads();  // every round of the CTA is done (round_val complete)
+    unsigned long long run = 0;
+    for (uint32_t b = 0; b < n_local; b += kThreads) {
+        const uint32_t r = b + tid;
+        const unsigned long long v = r < n_local ? a.round_val[cta_round0 + r] : 0ull;
         unsigned long long incl = v;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += y;
         }
-        if (lane < kWarps) s_wtot[lane] = incl - v;  // exclusive within the CTA
-        if (lane == 31) a.cta_total[blockIdx.x] = incl;
+        if (lane == 31) s_wtot[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const unsigned long long wv0 = s_wtot[lane];
+            unsigned long long wi = wv0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, d);
+                if (lane >= d) wi += y;
+            }
+            s_wtot[lane] = wi - wv0;
+            if (lane == 31) s_wtot[kWarps] = wi;
+        }
+        __syncthreads();
+        if (r < n_local) a.round_val[cta_round0 + r] = run + s_wtot[warp] + incl - v;
+        run += s_wtot[kWarps];
+        __syncthreads();
     }
+    if (tid == 0) a.cta_total[blockIdx.x] = run;
+    STAMP(7);
     grid_barrier(&a.ws->barrier[a.parity]);
     if (warp == 0) {
         unsigned long long pre = 0, all = 0;
@@ -756,44 +835,54 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         }
     }
     __syncthreads();
-    uint64_t off = s_wtot[kWarps] + s_wtot[warp];  // this warp's first output row
+    const uint64_t cta_off = s_wtot[kWarps];  // this CTA's first output row
     STAMP(3);
 
     // ================================================= phase 3: emit
-    if (total == 0) {
-        STAMP(4);
-        return;
-    }
     if (n_hits <= a.hit_cap) {
+        // hits are in position order; a round's hits are consecutive, so a
+        // row's index = its round's first row + rows of the round's earlier hits
+        uint64_t carry_run = 0, carry_seg = 0;  // warp-running rows before the batch / before its first round
+        uint32_t carry_round = 0xFFFFFFFFu;
         for (uint32_t b = 0; b < n_hits; b += 32) {
             const uint32_t i = b + lane;
-            uint32_t ti = kNone, cnt = 0;
-            uint64_t gi = 0;
+            uint32_t ti = 0, cnt = 0, rnd = 0xFFFFFFFEu, p = 0;
             if (i < n_hits) {
                 const uint2 h = hits[i];
-                gi = range_lo + h.x;
+                p = h.x;
                 ti = h.y;
+                rnd = p >> kRoundLog2;
                 cnt = s.out_ptr[ti + 1] - s.out_ptr[ti];
             }
             uint32_t ctot;
-            uint64_t o = off + warp_excl_scan(cnt, lane, &ctot);
+            const uint64_t ex = carry_run + warp_excl_scan(cnt, lane, &ctot);  // warp-running rows before hit i
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, rnd, 1);
+            const bool head = lane == 0 ? rnd != carry_round : rnd != prev;
+            const uint32_t hm = __ballot_sync(0xffffffffu, head) & (0xFFFFFFFFu >> (31 - lane));
+            const int hl = hm ? 31 - __clz(hm) : -1;
+            const uint64_t seg_h = __shfl_sync(0xffffffffu, ex, hl < 0 ? 0 : hl);
+            const uint64_t seg = hl < 0 ? carry_seg : seg_h;
             if (cnt) {
+                uint64_t o = cta_off + a.round_val[cta_round0 + rnd] + (ex - seg);
                 const uint32_t r0 = s.out_ptr[ti];
                 for (uint32_t e = 0; e < cnt; ++e, ++o) {
                     if (o < a.capacity) {
-                        a.out_pos[o] = a.pos_base + gi;
+                        a.out_pos[o] = a.pos_base + cta_lo + p;
                         a.out_pid[o] = __ldg(a.t.out_pid + r0 + e);
                     }
                 }
             }
-            off += ctot;
+            carry_seg = __shfl_sync(0xffffffffu, seg, 31);
+            carry_round = __shfl_sync(0xffffffffu, rnd, 31);
+            carry_run += ctot;
         }
     } else {
-        // hit list overflowed: scan the range again (text from global memory),
-        // writing rows directly in position order
-        for (uint64_t i = 0; i < nr; ++i) {
-            const uint64_t rbase = (r_begin + i) * kRound;
-            const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
+        // hit list overflowed: scan this warp's rounds again (text from global
+        // memory), writing rows directly in position order
+        for (uint32_t r = 0; r < n_local; ++r) {
+            if (__ldcg(a.round_owner + cta_round0 + r) != gw) continue;
+            uint64_t off = cta_off + a.round_val[cta_round0 + r];
+            const uint64_t lbase = cta_lo + (uint64_t)r * kRound + (uint64_t)lane * kPerLane;
             uint32_t wv[kWv];
 #pragma unroll
             for (int q = 0; q < kWv; ++q) {
@@ -807,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
                 surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
             }
-            const GlobalText gt{a.text + lbase, clamp32(a.readable - lbase)};
+            const GlobalText gt{a.text + lbase, clamp32(a.readable - lbase), a.aligned};
             uint32_t cc = 0, hm = 0;
             for (uint32_t m = surv; m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
@@ -830,7 +919,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     }
                 }
             }
-            off += ctot;
         }
     }
     STAMP(4);
@@ -875,26 +963,34 @@ int device_info(int device, DeviceInfo &out, std::string &err) {
     return kStatusOk;
 }
 
-// Launch geometry shared by workspace sizing and the launch itself.
+// Launch geometry shared by workspace sizing and the launch itself.  CTA b
+// owns rounds [b * rounds_per_cta, (b + 1) * rounds_per_cta); workspace =
+// fixed header | round_val[n_rounds] u64 | round_owner[n_rounds] u32 (padded) |
+// hit lists [warps][hit_cap] uint2.
 struct Geometry {
-    uint64_t grid, warps, rounds_per_warp;
+    uint64_t grid, warps, n_rounds, rounds_per_cta;
     uint32_t hit_cap;
+    uint64_t off_owner, off_hits, ws_bytes;
 };
 Geometry geometry(uint64_t n_starts, int sms) {
     Geometry g;
-    const uint64_t n_rounds = (n_starts + kRound - 1) / kRound;
+    g.n_rounds = (n_starts + kRound - 1) / kRound;
     g.grid = (uint64_t)sms;
-    if (g.grid * kWarps > n_rounds) g.grid = (n_rounds + kWarps - 1) / kWarps;
+    if (g.grid * kWarps > g.n_rounds) g.grid = (g.n_rounds + kWarps - 1) / kWarps;
     if (g.grid < 1) g.grid = 1;
     g.warps = g.grid * kWarps;
-    g.rounds_per_warp = (n_rounds + g.warps - 1) / g.warps;
-    if (g.rounds_per_warp < 1) g.rounds_per_warp = 1;
-    // hit records per warp: 1/16 of its starts, between 64 and 4096 (a warp
-    // that finds more re-scans its range in phase 3 instead)
-    uint64_t cap = g.rounds_per_warp * kRound / 16;
+    g.rounds_per_cta = (g.n_rounds + g.grid - 1) / g.grid;
+    if (g.rounds_per_cta < 1) g.rounds_per_cta = 1;
+    // hit records per warp: 1/16 of twice its average share of starts,
+    // between 64 and 4096 (a warp that finds more re-scans its rounds in
+    // phase 3 instead)
+    uint64_t cap = 2 * ((g.rounds_per_cta + kWarps - 1) / kWarps) * kRound / 16;
     if (cap < 64) cap = 64;
     if (cap > 4096) cap = 4096;
     g.hit_cap = (uint32_t)cap;
+    g.off_owner = kWsFixed + 8 * g.n_rounds;
+    g.off_hits = g.off_owner + ((4 * g.n_rounds + 15) & ~15ull);
+    g.ws_bytes = g.off_hits + 8ull * g.warps * g.hit_cap;
     return g;
 }
 
@@ -930,7 +1026,7 @@ int workspace_bytes_for(uint64_t n_starts, int device, uint64_t *out, std::strin
     int st = device_info(device, di, err);
     if (st != kStatusOk) return st;
     const Geometry g = geometry(n_starts, di.sms);
-    *out = kWsFixed + 8ull * g.warps * g.hit_cap;
+    *out = g.ws_bytes;
     return kStatusOk;
 }
 
@@ -963,7 +1059,11 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     int st = device_info(device, di, err);
     if (st != kStatusOk) return st;
     const Geometry geo = geometry(n_starts, di.sms);
-    const uint64_t need = kWsFixed + 8ull * geo.warps * geo.hit_cap;
+    const uint64_t need = geo.ws_bytes;
+    if (geo.rounds_per_cta >= (1ull << (32 - kRoundLog2))) {  // start offsets within a CTA are 32-bit
+        err = "pfac_match_device: n_starts too large for one launch (split the text)";
+        return kStatusLimit;
+    }
     if (!d_ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(d_ws) & 15)) {
         err = "pfac_match_device: workspace too small or misaligned";
         return kStatusInvalid;
@@ -976,8 +1076,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
-                           kWarps * kDefer * 20 + 8192 +
-                           align16(40 * B) + 8 * (kWarps + 1) + 512;
+                           kWarps * kDefer * 4 + 8192 +
+                           align16(40 * B) + 8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
         return kStatusLimit;
@@ -1033,10 +1133,10 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     o = align_up(o, 128);
     a.off_ring = o;   o += kWarps * kSlots * kSlotBytes;
     a.off_bar = o;    o += (kWarps * kSlots + 1) * 8;
-    a.off_warp = o;   o += 8 * (kWarps + 1);
+    a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 1] + the CTA's round counter
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
-    a.off_defer = o;  o += kWarps * kDefer * 20;  // per warp: u32 pos[kDefer], uint4 snippet[kDefer]
+    a.off_defer = o;  o += kWarps * kDefer * 4;  // per warp: u32 pos[kDefer]
     a.off_pair = o;   o += 8192;                 // 2-gram prefix table [256][8] words
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
@@ -1082,10 +1182,12 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.out_count = d_count;
     a.ws = reinterpret_cast<WsHeader *>(d_ws);
     a.cta_total = reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(d_ws) + sizeof(WsHeader));
-    a.hits = reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(d_ws) + kWsFixed);
+    a.round_val = reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(d_ws) + kWsFixed);
+    a.round_owner = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_ws) + geo.off_owner);
+    a.hits = reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(d_ws) + geo.off_hits);
     a.hit_cap = geo.hit_cap;
     a.parity = parity;
-    a.rounds_per_warp = geo.rounds_per_warp;
+    a.rounds_per_cta = geo.rounds_per_cta;
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
     const void *fn = t.kind == 2 ? (const void *)pfac_scan_kernel<2>
