@@ -60,8 +60,8 @@ constexpr int kSlotBytes = kRound + PFAC_SLOT_EXTRA;  // one round of text (+ th
 static_assert(kSlots >= 2, "ring");
 constexpr int kMaxCtas = 1024;
 constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated filter
+constexpr int kDefer = 48;             // per-warp queue of starts to walk
 constexpr uint32_t kHotCap = 24576;  // hot-trie smem when the trie does not fit (rest left to L1)
-constexpr int kDefer = 64;             // per-warp deferred-walk queue (start offsets)
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
@@ -162,11 +162,11 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int *p) {
 
 #ifdef PFAC_TIMING
 // Instrumented build only (tools/timing.py): per-warp %globaltimer stamps.
-__device__ unsigned long long g_pfac_timing[8192 * 8];
+__device__ unsigned long long g_pfac_timing[8192 * 16];
 __device__ __forceinline__ void stamp(int warp_global, int k) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if ((threadIdx.x & 31) == 0 && warp_global < 8192) g_pfac_timing[warp_global * 8 + k] = t;
+    if ((threadIdx.x & 31) == 0 && warp_global < 8192) g_pfac_timing[warp_global * 16 + k] = t;
 }
 #define STAMP(k) stamp((int)(blockIdx.x * kWarps + (threadIdx.x >> 5)), k)
 #else
@@ -409,10 +409,11 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
     return surv;
 }
 
-// Walk the deferred starts dpos[0, n) (offsets from the CTA's first start,
-// position order) with full warps; hits are appended to the warp's hit list in
-// the same order and their pid counts added to their rounds' counts.  Returns
-// the new hit count.
+// Walk the queued starts dpos[0, n) (offsets from the CTA's first start,
+// position order) with full warps, text from global memory (L2: it was
+// streamed moments ago); hits are appended to the warp's hit list in the same
+// order and their pid counts added to their rounds' counts.  Returns the new
+// hit count.
 __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem s, uint64_t cta_lo, uint64_t cta_round0,
                                                   const uint32_t *dpos, uint32_t n, uint2 *hits, uint32_t n_hits) {
     const ScanArgs &a = *ap;
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     if (tid == 0) mbar_init(sbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;  // for the next launch
-    __syncthreads();
+    __syncthreads();  // barriers initialised
     Smem s;
     // terminal tables: shared-memory copies when staged (generic pointers)
     s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem + a.off_terms) : a.t.out_ptr;
@@ -509,7 +510,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // interleaved), then from the CTA's shared counter (dynamic: warps whose
     // walks ran long take fewer of the last rounds).  Increasing per warp;
     // warp-uniform; >= n_local when none is left.
-    const uint32_t n_static = (n_local * PFAC_STATIC_NUM / 4) / kWarps;
+    const uint32_t n_static = max((uint32_t)(kSlots - 1), (n_local * PFAC_STATIC_NUM / 4) / kWarps);  // the first
+                                                                       // kSlots-1 takes never touch the counter
     uint32_t taken = 0;
     auto take = [&]() -> uint32_t {
         uint32_t r;
@@ -565,51 +567,56 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 
     // ---- stage the tables (TMA bulk copies of the image sections; the
     // filter is replicated from 8/4-byte loads), then start streaming
-    if (tid == 0) {
-        *s_next = 0u;
+    {   // one bulk copy per warp (lane 0), so the copies are in flight together
         const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
                        nb_l1 = align16(40 * a.n_level1);
         const uint32_t nb_w = align16(4 * a.hot_words), nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
-        mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1 + 2 * nb_w + nb_t + nb_tb);
-        bulk_g2s(s_root, a.t.root, 1024, sbar, policy_last);
-        bulk_g2s(s_node, a.t.node, nb_node, sbar, policy_last);
-        if (nb_label) bulk_g2s(s_label, a.t.label, nb_label, sbar, policy_last);
-        bulk_g2s(s_bm, a.t.level1, nb_l1, sbar, policy_last);
-        if (nb_w) {
-            bulk_g2s(smem + a.off_tbits, a.t.tail_bits, nb_w, sbar, policy_last);
-            bulk_g2s(smem + a.off_trank, a.t.tail_rank, nb_w, sbar, policy_last);
+        if (tid == 0) {
+            *s_next = 0u;
+            mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1 + 2 * nb_w + nb_t + nb_tb);
         }
-        if (nb_t) bulk_g2s(smem + a.off_tails, a.t.tails, nb_t, sbar, policy_last);
-        if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, policy_last);
+        if (lane == 0) {
+            switch (warp) {
+                case 0: bulk_g2s(s_root, a.t.root, 1024, sbar, policy_last); break;
+                case 1: bulk_g2s(s_node, a.t.node, nb_node, sbar, policy_last); break;
+                case 2: if (nb_label) bulk_g2s(s_label, a.t.label, nb_label, sbar, policy_last); break;
+                case 3: bulk_g2s(s_bm, a.t.level1, nb_l1, sbar, policy_last); break;
+                case 4: if (nb_w) bulk_g2s(smem + a.off_tbits, a.t.tail_bits, nb_w, sbar, policy_last); break;
+                case 5: if (nb_w) bulk_g2s(smem + a.off_trank, a.t.tail_rank, nb_w, sbar, policy_last); break;
+                case 6: if (nb_t) bulk_g2s(smem + a.off_tails, a.t.tails, nb_t, sbar, policy_last); break;
+                case 7: if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, policy_last); break;
+                default: break;
+            }
+        }
     }
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
-        // (four loads in flight per thread: the image is cold in L2 here)
+        // (8-16 loads in flight per thread: the image is cold in L2 here)
         const uint32_t nu = (Kind == 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
         if (Kind == 1) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
-            for (uint32_t j0 = 0; j0 < nu; j0 += 4 * kThreads) {
-                uint2 v[4];
+            for (uint32_t j0 = 0; j0 < nu; j0 += 8 * kThreads) {
+                uint2 v[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 8; ++q) {
                     const uint32_t j = j0 + tid + q * kThreads;
                     v[q] = j < nu ? __ldg(src + (j >> a.rep_log2)) : make_uint2(0, 0);
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < 8; ++q)
                     if (j0 + tid + q * kThreads < nu) d[j0 + tid + q * kThreads] = v[q];
             }
         } else {
-            for (uint32_t j0 = 0; j0 < nu; j0 += 4 * kThreads) {
-                uint32_t v[4];
+            for (uint32_t j0 = 0; j0 < nu; j0 += 16 * kThreads) {
+                uint32_t v[16];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 16; ++q) {
                     const uint32_t j = j0 + tid + q * kThreads;
                     v[q] = j < nu ? __ldg(a.t.filter + (j >> a.rep_log2)) : 0u;
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < 16; ++q)
                     if (j0 + tid + q * kThreads < nu) s_filter[j0 + tid + q * kThreads] = v[q];
             }
         }
@@ -621,15 +628,19 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             for (uint32_t j = tid; j < a.t.n_kept_terminals; j += kThreads) so[n_op + j] = __ldg(a.t.term_node + j);
         }
     }
+    STAMP(8);
     for (uint32_t r = tid; r < n_local; r += kThreads) a.round_val[cta_round0 + r] = 0ull;  // pid counts
     __syncthreads();  // the round counter and counts are initialised
-    // the first kSlots-1 rounds of this warp start streaming
+    STAMP(9);
+    // the first kSlots-1 rounds of this warp (static ones) start streaming
+    // (after the table requests: those are on the critical path)
     uint32_t rid[kSlots];
 #pragma unroll
     for (int q = 0; q < kSlots - 1; ++q) {
         rid[q] = take();
         if (rid[q] < n_local) issue(rid[q], q);
     }
+    STAMP(10);
     mbar_wait(sbar, 0);
     STAMP(5);
     __syncthreads();
@@ -649,35 +660,25 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // ================================================= phase 1: scan
     // One 1024-start round per iteration; the ring keeps kSlots-1 rounds in
     // flight.  Stage 1 filters each lane's 32 starts (bit mask).  Stage 2
-    // tests each survivor in its lane against the 2-gram prefix table (the
+    // compacts the survivors in position order (lane-major = position order)
+    // and tests them, one per lane, against the 2-gram prefix table (the
     // root's children and their level-1 bitmapped nodes): bytes
-    // (b0, b1) begin a pattern path, or b0 alone already reaches a terminal or
-    // tail.  The kept starts are appended to the warp's deferred queue in
-    // position order (lane-major = position order; a warp's rounds increase)
-    // and walked in full-warp batches whenever the queue may not take another
-    // round.
+    // (b0, b1) begin a pattern path, or b0 alone already reaches a terminal
+    // or tail.  The few kept starts are queued (position order; a warp's
+    // rounds increase) and walked in full-warp batches to their first
+    // mismatch whenever the queue may not take another 32.
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
-    uint32_t dcount = 0;  // deferred starts in the queue (warp-uniform)
-    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * kDefer;
+    uint32_t dcount = 0;  // queued starts (warp-uniform)
+    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * (kDefer + 16);
+    uint16_t *list = reinterpret_cast<uint16_t *>(dpos + kDefer);  // 32 survivor offsets
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
-    uint32_t km = 0;     // this lane's kept starts of the current round not yet queued
-    bool more = false;   // the current round still has kept starts to queue (warp-uniform)
     for (;;) {
         const bool done = rid[0] >= n_local;
-        // ---- the single batch-walk site
-        if (dcount != 0 && (done || more || dcount > (uint32_t)(kDefer - 32))) {
-#if defined(PFAC_EXP) && PFAC_EXP == 2
-            if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
-#else
-            n_hits = walk_deferred(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits);
-#endif
-            dcount = 0;
-        }
-        if (done) break;
         const uint32_t rel = rid[0] * (uint32_t)kRound;  // round start relative to cta_lo
-        if (!more) {
-            const uint64_t rbase = cta_lo + rel;
-            const uint8_t *p0 = ring + slot * kSlotBytes;
+        const uint64_t rbase = cta_lo + rel;
+        const uint8_t *p0 = ring + slot * kSlotBytes;
+        uint32_t pending = 0, tot = 0, r = 0, rlim = 0;
+        if (!done) {
             // refill the slot of the previous round with the next round taken
             __syncwarp();  // every lane's reads of that slot precede its refill
             rid[kSlots - 1] = take();
@@ -687,7 +688,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             if (taken == kSlots) STAMP(6);  // the first round's text is in
 #endif
 #ifdef PFAC_STREAM_ONLY
-            uint32_t pending = 0;
             if (p0[lane] == 0xFF && a.pos_base == ~0ull) n_hits++;  // keeps the loads
 #else
             // ---- stage 1: filter over the lane's 32 starts.  The lane's 32
@@ -709,22 +709,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 wv[7] = sw ? h0.w : h1.w;
             }
             const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
-#if PFAC_SLOT_EXTRA
-            const uint32_t tail4 = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound) : 0u;
-#else
-            uint32_t tail4 = 0;  // the 4 bytes after this round (lane 31's last windows)
-            if (lane == 31) {
-                const uint64_t j0 = rbase + kRound;
-                if (j0 + 4 <= a.readable && a.aligned) {
-                    tail4 = __ldg(reinterpret_cast<const uint32_t *>(a.text + j0));
-                } else {
-                    for (int b = 0; b < 4; ++b)
-                        if (j0 + b < a.readable) tail4 |= (uint32_t)__ldg(a.text + j0 + b) << (8 * b);
-                }
-            }
-#endif
-            wv[kWv - 1] = lane == 31 ? tail4 : w8;
-            uint32_t pending = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
+            wv[kWv - 1] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound) : w8;
+            pending = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
@@ -735,49 +721,50 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             if (pending == 0xDEADBEEFu && a.pos_base == ~0ull) n_hits++;  // experiment: filter only
             pending = 0;
 #endif
-            // ---- stage 2: 2-gram prefix test of the lane's survivors
-            const uint32_t rlim = a.readable > rbase ? clamp32(a.readable - rbase) : 0u;  // readable bytes from rbase
-            km = 0;
-            while (pending) {
-                const uint32_t k = __ffs(pending) - 1;
-                const uint32_t off = lane * kPerLane + k;
-                const uint32_t b0 = p0[off];
-                uint32_t keep;
-                if (off + 1 < rlim) {
-#if PFAC_SLOT_EXTRA
-                    const uint32_t b1 = p0[off + 1];  // the slot holds 16 bytes past the round
+            if (__any_sync(0xffffffffu, pending != 0)) {
+                r = warp_excl_scan(__popc(pending), lane, &tot);  // rank of the lane's first survivor
+                rlim = a.readable > rbase ? clamp32(a.readable - rbase) : 0u;  // readable bytes from rbase
+            }
+        }
+        // ---- stage 2, 32 survivors per pass; the single batch-walk site at its top
+        for (uint32_t cb = 0;; cb += 32) {
+            if (dcount != 0 && (done || dcount > (uint32_t)(kDefer - 32))) {
+#if defined(PFAC_EXP) && PFAC_EXP == 2
+                if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
-                    const uint32_t b1 = off + 1 < (uint32_t)kRound ? p0[off + 1] : (tail4 & 0xFFu);
+                n_hits = walk_deferred(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits);
 #endif
+                dcount = 0;
+            }
+            if (cb >= tot) break;
+            while (pending && r < cb + 32) {
+                list[r - cb] = (uint16_t)(lane * kPerLane + (__ffs(pending) - 1));
+                pending &= pending - 1;
+                ++r;
+            }
+            __syncwarp();
+            uint32_t off = 0;
+            bool keep = false;
+            if (cb + lane < tot) {
+                off = list[lane];
+                const uint32_t b0 = p0[off];
+                if (off + 1 < rlim) {
+                    const uint32_t b1 = p0[off + 1];  // the slot holds 16 bytes past the round
                     keep = (s_pair[b0 * 8 + (b1 >> 5)] >> (b1 & 31)) & 1u;
                 } else {
                     keep = s.root[b0] != 0u;  // last readable byte: let the walk decide
                 }
-                km |= keep << k;
-                pending &= pending - 1;
             }
+            __syncwarp();  // list reuse
+            const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+            if (keep) dpos[dcount + __popc(kb & ((1u << lane) - 1u))] = rel + off;
+            dcount += __popc(kb);
         }
-        // ---- queue this round's kept starts in position order (as many as fit)
-        more = false;
-        if (__any_sync(0xffffffffu, km != 0)) {
-            uint32_t tot;
-            uint32_t r = warp_excl_scan(__popc(km), lane, &tot);
-            const uint32_t room = (uint32_t)kDefer - dcount;
-            while (km && r < room) {
-                dpos[dcount + r] = rel + lane * kPerLane + (__ffs(km) - 1);
-                km &= km - 1;
-                ++r;
-            }
-            __syncwarp();
-            more = tot > room;
-            dcount += more ? room : tot;
-        }
-        if (!more) {
+        if (done) break;
 #pragma unroll
-            for (int q = 0; q < kSlots - 1; ++q) rid[q] = rid[q + 1];
-            slot = slot + 1 == kSlots ? 0 : slot + 1;
-            phase ^= slot == 0;
-        }
+        for (int q = 0; q < kSlots - 1; ++q) rid[q] = rid[q + 1];
+        slot = slot + 1 == kSlots ? 0 : slot + 1;
+        phase ^= slot == 0;
     }
     STAMP(2);
 
@@ -1076,7 +1063,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
-                           kWarps * kDefer * 4 + 8192 +
+                           kWarps * (kDefer + 16) * 4 + 8192 +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
@@ -1136,8 +1123,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 1] + the CTA's round counter
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
-    a.off_defer = o;  o += kWarps * kDefer * 4;  // per warp: u32 pos[kDefer]
-    a.off_pair = o;   o += 8192;                 // 2-gram prefix table [256][8] words
+    a.off_defer = o;  o += kWarps * (kDefer + 16) * 4;  // per warp: queue u32[kDefer] + survivor list u16[32]
+    a.off_pair = o;   o += 8192;                          // 2-gram prefix table [256][8] words
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
     a.off_label = o;  o += align16(EH);

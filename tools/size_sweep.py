@@ -17,6 +17,9 @@ t = pf.Trie(gen.patterns(cid))
 big = 256 << 20
 text = torch.from_numpy(gen.text(cid, 0, big)).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush2 = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+sink = torch.zeros((), dtype=torch.int64, device="cuda")
+CLEAN = os.environ.get("CLEAN_FLUSH") == "1"
 sc = pf.Scanner(t, "cuda:0", capacity=big // 256 + 4096)
 rows = []
 for n in [1 << 10, 1 << 16, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 128 << 20, 256 << 20]:
@@ -25,6 +28,8 @@ for n in [1 << 10, 1 << 16, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 128 << 20, 256
     evs = []
     for rep in range(12):
         flush.fill_(rep)  # the GPU is busy flushing while the host enqueues the launch
+        if CLEAN:
+            sink.copy_(flush2.sum(dtype=torch.int64))  # read pass: the dirty lines are written back before the scan
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         h0 = time.perf_counter()

@@ -23,19 +23,19 @@ sc = pf.Scanner(t, "cuda:0", capacity=n // 256 + 4096)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 lib = pf._lib()
 lib.pfac_debug_timing.argtypes = [C.c_void_p, C.c_uint64]
-buf = np.zeros(8192 * 8, dtype=np.uint64)
+buf = np.zeros(8192 * 16, dtype=np.uint64)
 for rep in range(4):
     flush.fill_(rep)
     torch.cuda.synchronize()
     sc.launch(text)
     torch.cuda.synchronize()
 lib.pfac_debug_timing(buf.ctypes.data, buf.size)
-b = buf.reshape(8192, 8).astype(np.int64)
+b = buf.reshape(8192, 16).astype(np.int64)
 used = b[:, 0] > 0
 b = b[used]
 t0 = b[:, 0].min()
 names = ["start", "tables staged", "phase1 end", "offsets known", "end", "tables arrived", "first text in",
-         "local scan done"]
+         "local scan done", "filter copied", "after sync", "first issued"]
 print(f"config C{cid}, {n} bytes, {used.sum()} warps; times in us relative to the first warp start")
 for k, nm in enumerate(names):
     col = (b[:, k] - t0) / 1e3
