@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;  // for the next launch
     __syncthreads();  // barriers initialised
+    STAMP(11);
     Smem s;
     // terminal tables: shared-memory copies when staged (generic pointers)
     s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem + a.off_terms) : a.t.out_ptr;
@@ -589,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             }
         }
     }
+    STAMP(12);
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
         // (8-16 loads in flight per thread: the image is cold in L2 here)
