@@ -249,11 +249,34 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         uint32_t s = node_word[0] & kEdgeMask, e = node_word[1] & kEdgeMask;
         for (uint32_t k = s; k < e; k++) root[label[k]] = k + 1;
     }
-    const uint32_t gram = std::min<uint32_t>(4, min_len);
+    // DNA pattern sets (every byte in {A,C,G,T}, shortest >= 16): kind 3
+    bool dna = min_len >= kDnaGram;
+    for (uint32_t k = 0; dna && k < m; k++)
+        for (uint32_t b = 0; dna && b < lens[k]; b++) {
+            const uint8_t c = pats[k][b];
+            dna = c == 'A' || c == 'C' || c == 'G' || c == 'T';
+        }
+    {
+        const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
+        if (force && force[0] != '3') dna = false;
+    }
+    const uint32_t gram = dna ? kDnaGram : std::min<uint32_t>(4, min_len);
     uint32_t exact = gram <= 2 ? 1u : 0u;
     uint32_t log2_bits;
-    uint32_t kind = gram == 4 ? 1u : 0u;
-    if (exact) {
+    uint32_t kind = dna ? 3u : gram == 4 ? 1u : 0u;
+    auto dna_key = [&](const uint8_t *pt) {
+        uint32_t key = 0;
+        for (uint32_t b = 0; b < kDnaGram; b++) key |= dna_code(pt[b]) << (2 * b);
+        return key;
+    };
+    if (dna) {
+        std::vector<uint32_t> keys(m);
+        for (uint32_t k = 0; k < m; k++) keys[k] = dna_key(pats[k]);
+        std::sort(keys.begin(), keys.end());
+        const uint64_t distinct = std::unique(keys.begin(), keys.end()) - keys.begin();
+        log2_bits = 10;  // ~32 bits per key (two of them set per key), at most 2^19 bits (64 KiB)
+        while (log2_bits < 19 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+    } else if (exact) {
         log2_bits = 8 * gram;
     } else {
         std::vector<uint32_t> keys(m);
@@ -285,7 +308,12 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     for (uint32_t k = 0; k < m; k++) {
         uint32_t x = 0;
         for (uint32_t b = 0; b < gram; b++) x |= (uint32_t)pats[k][b] << (8 * b);
-        if (kind == 2) {
+        if (kind == 3) {
+            const uint32_t key = dna_key(pats[k]);
+            const uint32_t b = dna_block(key, log2_bits);
+            filter[2 * b] |= 1u << dna_bit_lo(key);
+            filter[2 * b + 1] |= 1u << dna_bit_hi(key);
+        } else if (kind == 2) {
             // as the first start of a pair: shared bytes are P[1..3], own byte P[0];
             // as the second start: shared bytes are P[0..2], own byte P[3]
             filter[filter_pair_word(x >> 8, log2_bits)] |= 1u << (31u - (x & 31u));
@@ -383,9 +411,10 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
               h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails == T && h.n_nodes_full >= N &&
               in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
-              in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && h.filter_gram <= 4 &&
+              in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && (h.filter_gram <= 4 || (h.filter_kind == 3 && h.filter_gram == kDnaGram)) &&
               h.filter_gram <= h.min_len && h.min_len <= h.max_len && h.max_len <= kMaxPatternLen &&
-              h.filter_mul == kFilterMul && (h.filter_gram == 4 ? (h.filter_kind == 1 || h.filter_kind == 2) : h.filter_kind == 0) &&
+              h.filter_mul == kFilterMul && (h.filter_gram == kDnaGram ? h.filter_kind == 3
+                                          : h.filter_gram == 4 ? (h.filter_kind == 1 || h.filter_kind == 2) : h.filter_kind == 0) &&
               (h.filter_kind == 0 || h.filter_log2_bits >= 10) && in(h.off_tail_bits, 4 * ((N + 31) / 32)) &&
               in(h.off_tail_rank, 4 * ((N + 31) / 32)) && in(h.off_tails, 16 * h.n_tails) &&
               in(h.off_tail_bytes, h.n_tail_bytes) && in(h.off_level1, 40 * h.n_level1);

@@ -351,10 +351,39 @@ __device__ __forceinline__ uint2 lds64_abs(uint32_t addr) {
     return v;
 }
 template <int Kind>
-__device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[kWv], uint32_t sW, uint32_t sWmul,
-                                             uint32_t stride, uint32_t base_lane) {
+__device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[kWv], const uint32_t ext[3],
+                                             uint32_t sW, uint32_t sWmul, uint32_t stride, uint32_t base_lane) {
     uint32_t surv = 0;
-    if (Kind == 2) {
+    if (Kind == 3) {
+        // DNA k-mer filter: 2-bit codes of the lane's 48 bytes (its 32 starts
+        // + 15) packed into c[0..2] (byte i's code at bits 2i of the stream);
+        // per word: ((w & 0x06060606) * 0x820820) >> 24 gathers the four codes
+        // (b >> 1) & 3 into one byte (no carries reach bits 24..31)
+        uint32_t c[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int j = 4 * q + t;
+                const uint32_t w = j < kWv ? wv[j] : ext[j - kWv];
+                pk[t] = __umulhi((w & 0x06060606u) * 0x820820u, 1u << 8);  // >> 24 on the FMA pipe
+            }
+            c[q] = pk[0] + pk[1] * 0x100u + pk[2] * 0x10000u + pk[3] * 0x1000000u;
+        }
+        uint32_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int k = kPerLane - 1; k >= 0; --k) {
+            const uint32_t key = (k & 15) ? __funnelshift_r(c[k >> 4], c[(k >> 4) + 1], 2 * (k & 15)) : c[k >> 4];
+            const uint32_t blk = __umulhi(key * kFilterMul, sWmul);
+            const uint2 w2 = lds64_abs(blk * stride + base_lane);
+            const uint32_t h2 = __umulhi(key, kFilterMul2);
+            // rotate by key / h2 (funnel amounts are mod 32): tested bits -> 31
+            const uint32_t r = __funnelshift_l(w2.x, w2.x, key) & __funnelshift_l(w2.y, w2.y, h2);
+            acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);  // acc << 1 | bit
+        }
+        surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
+    } else if (Kind == 2) {
         // pair filter: one 32-bit word per start pair (k, k+1), chosen by the
         // three shared bytes k+1..k+3 (x[k+1] * (M << 8) drops byte k+4)
         constexpr uint32_t kMul = kFilterMul << 8;
@@ -482,8 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // and 2: word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
     // so the lanes of a phase spread over the banks
     const uint32_t rep = 1u << a.rep_log2;
-    const uint32_t unit = Kind == 1 ? 8u : 4u;
-    const uint32_t sW = 32u - (a.t.log2_bits - (Kind == 1 ? 6u : 5u));  // block index = hash >> sW
+    const uint32_t unit = (Kind == 1 || Kind == 3) ? 8u : 4u;
+    const uint32_t sW = 32u - (a.t.log2_bits - ((Kind == 1 || Kind == 3) ? 6u : 5u));  // block index = hash >> sW
     const uint32_t sWmul = 1u << (32u - sW);                              // (hash * sWmul) >> 32 == hash >> sW
     const uint32_t stride = rep * unit;
     const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
@@ -594,8 +623,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
         // (8-16 loads in flight per thread: the image is cold in L2 here)
-        const uint32_t nu = (Kind == 1 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
-        if (Kind == 1) {
+        const uint32_t nu = ((Kind == 1 || Kind == 3) ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
+        if (Kind == 1 || Kind == 3) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
             for (uint32_t j0 = 0; j0 < nu; j0 += 8 * kThreads) {
@@ -712,7 +741,15 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             }
             const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
             wv[kWv - 1] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound) : w8;
-            pending = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
+            uint32_t ext[3] = {0, 0, 0};  // kind 3: the next 12 bytes (the slot holds 16 past the round)
+            if (Kind == 3) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const uint32_t e = __shfl_down_sync(0xffffffffu, wv[q + 1], 1);
+                    ext[q] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound + 4 + 4 * q) : e;
+                }
+            }
+            pending = filter32<Kind>(a, wv, ext, sW, sWmul, stride, base_lane);
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
@@ -747,7 +784,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             __syncwarp();
             uint32_t off = 0;
             bool keep = false;
-            if (cb + lane < tot) {
+            if (cb + lane < tot && Kind == 3) {  // DNA: the 2-gram test keeps everything
+                off = list[lane];
+                keep = true;
+            } else if (cb + lane < tot) {
                 off = list[lane];
                 const uint32_t b0 = p0[off];
                 if (off + 1 < rlim) {
@@ -872,15 +912,16 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             if (__ldcg(a.round_owner + cta_round0 + r) != gw) continue;
             uint64_t off = cta_off + a.round_val[cta_round0 + r];
             const uint64_t lbase = cta_lo + (uint64_t)r * kRound + (uint64_t)lane * kPerLane;
-            uint32_t wv[kWv];
+            uint32_t wv[kWv], ext[3];
 #pragma unroll
-            for (int q = 0; q < kWv; ++q) {
-                wv[q] = 0;
+            for (int q = 0; q < kWv + 3; ++q) {
+                uint32_t x = 0;
 #pragma unroll
                 for (int b = 0; b < 4; ++b)
-                    if (lbase + 4 * q + b < a.readable) wv[q] |= (uint32_t)__ldg(a.text + lbase + 4 * q + b) << (8 * b);
+                    if (lbase + 4 * q + b < a.readable) x |= (uint32_t)__ldg(a.text + lbase + 4 * q + b) << (8 * b);
+                if (q < kWv) wv[q] = x; else ext[q - kWv] = x;
             }
-            uint32_t surv = filter32<Kind>(a, wv, sW, sWmul, stride, base_lane);
+            uint32_t surv = filter32<Kind>(a, wv, ext, sW, sWmul, stride, base_lane);
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
                 surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
@@ -941,6 +982,9 @@ int device_info(int device, DeviceInfo &out, std::string &err) {
                                      di.max_smem_optin);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(pfac_scan_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     di.max_smem_optin);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(pfac_scan_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      di.max_smem_optin);
         if (e != cudaSuccess) {
             err = std::string("device query: ") + cudaGetErrorString(e);
@@ -1179,7 +1223,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.rounds_per_cta = geo.rounds_per_cta;
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
-    const void *fn = t.kind == 2 ? (const void *)pfac_scan_kernel<2>
+    const void *fn = t.kind == 3 ? (const void *)pfac_scan_kernel<3>
+                     : t.kind == 2 ? (const void *)pfac_scan_kernel<2>
                      : t.kind == 1 ? (const void *)pfac_scan_kernel<1> : (const void *)pfac_scan_kernel<0>;
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)geo.grid), dim3(kThreads), args, smem, stream);
     if (e != cudaSuccess) {

@@ -65,9 +65,21 @@ def _pair_word(h, x3):
     return ((x3 * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 5))
 
 
+def dna_key(window: bytes) -> int:
+    """Kind 3: 2-bit codes (b >> 1) & 3 of the first 16 bytes, byte i at bits 2i."""
+    return sum(((b >> 1) & 3) << (2 * i) for i, b in enumerate(window[:16]))
+
+
 def filter_pass(h, key, start=0):
     """Does the start whose first d bytes are `key` pass the filter?  Kind 2
-    (pair filter) depends on the start's parity (image.h)."""
+    (pair filter) depends on the start's parity (image.h).  Kind 3 takes the
+    DNA key (dna_key of the start's 16 bytes)."""
+    if h["filter_kind"] == 3:
+        f = h["filter"]
+        b = ((key * 0x9E3779B1) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
+        lo = 31 - (key & 31)
+        hi = 31 - (((key * 0x85EBCA6B) >> 32) & 31)
+        return bool((int(f[2 * b]) >> lo) & 1) and bool((int(f[2 * b + 1]) >> hi) & 1)
     if h["filter_kind"] == 2:
         f = h["filter"]
         if start % 2 == 0:  # first of the pair: shared bytes 1..3, own byte 0
@@ -135,7 +147,8 @@ def match(h, text: bytes, readable=None, n_starts=None):
     for i in range(ns):
         if i + d > L:
             continue
-        if not filter_pass(h, int.from_bytes(text[i:i + d], "little"), i):
+        key = dna_key(text[i:i + d]) if h["filter_kind"] == 3 else int.from_bytes(text[i:i + d], "little")
+        if not filter_pass(h, key, i):
             continue
         ti = walk(h, text, i, L)
         if ti is not None:
