@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -1198,6 +1199,14 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.n_level1 = B;
     a.hot_nodes = H;
     a.hot_edges = EH;
+    if (std::getenv("PFAC_DEBUG_PLAN")) {  // tools only
+        std::fprintf(stderr,
+                         "pfac plan: kind %u smem %zu of %d; filter %u B x%u; hot nodes %u of %u (edges %u, tails %u, "
+                         "tail bytes %u); terms in smem %d; grid %llu x %d warps, %llu rounds/CTA, hit cap %u\n",
+                         t.kind, smem, di.max_smem_optin, filter_words * 4, 1u << rep_log2, H, t.n_nodes, EH, TH, TBH,
+                         a.off_terms != 0, (unsigned long long)geo.grid, kWarps,
+                         (unsigned long long)geo.rounds_per_cta, geo.hit_cap);
+    }
     uint32_t parity;
     {
         std::lock_guard<std::mutex> lk(g_ws_mu);

@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""A/B kernel timing: alternates processes running the working-tree library
+(libpfac.so) and a reference build (libpfac_ref.so, tools/ab_build.sh) on one
+config; bench-style timing (L2 flush outside CUDA events).
+usage: python tools/ab.py [config] [rounds]"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r'''
+import os, sys, torch, numpy as np
+sys.path.insert(0, %r)
+import gen, paper_1702_03657_b200 as pf
+cid = int(sys.argv[1]); n = min(gen.config(cid)["text_len"], 1 << 30)
+text = torch.from_numpy(gen.text(cid, 0, n)).cuda()
+sc = pf.Scanner(pf.Trie(gen.patterns(cid)), "cuda:0", capacity=n // 256 + 4096)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(5):
+    flush.fill_(1); sc.launch(text)
+torch.cuda.synchronize()
+ev = []
+for i in range(int(sys.argv[2])):
+    flush.fill_(i)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); sc.launch(text); b.record(); ev.append((a, b))
+torch.cuda.synchronize()
+print(" ".join("%%.2f" %% (a.elapsed_time(b) * 1e3) for a, b in ev))
+''' % HERE
+
+cid = sys.argv[1] if len(sys.argv) > 1 else "2"
+rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+reps = "60" if cid == "2" else "6"
+res = {"new": [], "ref": []}
+for r in range(rounds):
+    for name, lib in [("ref", "libpfac_ref.so"), ("new", "libpfac.so")]:
+        env = dict(os.environ, PFAC_LIB=os.path.join(HERE, "paper_1702_03657_b200", lib))
+        out = subprocess.run([sys.executable, "-c", CHILD, cid, reps], env=env, capture_output=True, text=True)
+        if out.returncode:
+            print(out.stderr[-2000:])
+            sys.exit(1)
+        res[name] += [float(x) for x in out.stdout.split()]
+for k in ["ref", "new"]:
+    v = np.array(res[k])
+    print(f"C{cid} {k}: median {np.median(v):.2f} us  p10 {np.percentile(v, 10):.2f}  p90 {np.percentile(v, 90):.2f}  (n={len(v)})")
+print(f"new/ref = {np.median(res['new']) / np.median(res['ref']):.4f}")
