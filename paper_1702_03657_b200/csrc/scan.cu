@@ -537,6 +537,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint2 *hits = a.hits + (uint64_t)gw * a.hit_cap;
     uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 1);  // round counter of the CTA
 
+    // local rounds r < n_fast have their whole slot (round + overhang) readable
+    const uint32_t n_fast = !a.aligned || a.readable < cta_lo + kSlotBytes
+                                ? 0u
+                                : (uint32_t)min((uint64_t)n_local, (a.readable - cta_lo - kSlotBytes) / kRound + 1);
     // The warp's j-th round: rounds warp + 32j while j < n_static (static,
     // interleaved), then from the CTA's shared counter (dynamic: warps whose
     // walks ran long take fewer of the last rounds).  Increasing per warp;
@@ -555,8 +559,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             }
             r = kWarps * n_static + __shfl_sync(0xffffffffu, r, 0);
         }
+        // the owner of a dynamic round is recorded (phase 3's re-scan
+        // fallback); a static round r < kWarps * n_static belongs to warp r % kWarps
+        if (taken >= n_static && lane == 0 && r < n_local) a.round_owner[cta_round0 + r] = gw;
         ++taken;
-        if (lane == 0 && r < n_local) a.round_owner[cta_round0 + r] = gw;
         return r;
     };
     // Fill ring slot `slot` with local round r: one TMA bulk copy of the
@@ -565,6 +571,14 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // is not 16-byte aligned), all loads issued before the stores.
     auto issue = [&](uint32_t r, uint32_t slot) {
         uint8_t *dst = ring + slot * kSlotBytes;
+        if (r < n_fast) {  // the whole slot is readable and aligned: one bulk copy
+            if (lane == 0) {
+                fence_proxy_async_smem();  // prior generic accesses of the slot precede the async write
+                mbar_arrive_expect_tx(&bars[slot], kSlotBytes);
+                bulk_g2s(dst, a.text + cta_lo + (uint64_t)r * kRound, kSlotBytes, &bars[slot], policy);
+            }
+            return;
+        }
         const uint64_t lo = cta_lo + (uint64_t)r * kRound;
         const uint32_t avail = lo < a.readable ? (uint32_t)min(a.readable - lo, (uint64_t)kSlotBytes) : 0u;
         const uint32_t nbulk = a.aligned ? (avail & ~15u) : 0u;
@@ -763,7 +777,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #endif
             if (__any_sync(0xffffffffu, pending != 0)) {
                 r = warp_excl_scan(__popc(pending), lane, &tot);  // rank of the lane's first survivor
-                rlim = a.readable > rbase ? clamp32(a.readable - rbase) : 0u;  // readable bytes from rbase
+                rlim = rid[0] < n_fast ? (uint32_t)kSlotBytes                       // readable bytes from rbase
+                                       : (a.readable > rbase ? clamp32(a.readable - rbase) : 0u);
             }
         }
         // ---- stage 2, 32 survivors per pass; the single batch-walk site at its top
@@ -910,7 +925,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         // hit list overflowed: scan this warp's rounds again (text from global
         // memory), writing rows directly in position order
         for (uint32_t r = 0; r < n_local; ++r) {
-            if (__ldcg(a.round_owner + cta_round0 + r) != gw) continue;
+            const uint32_t owner = r < kWarps * n_static ? blockIdx.x * kWarps + r % kWarps
+                                                         : __ldcg(a.round_owner + cta_round0 + r);
+            if (owner != gw) continue;
             uint64_t off = cta_off + a.round_val[cta_round0 + r];
             const uint64_t lbase = cta_lo + (uint64_t)r * kRound + (uint64_t)lane * kPerLane;
             uint32_t wv[kWv], ext[3];
