@@ -53,3 +53,15 @@ $(PKG)/libpfac_v_e0.so: $(CSRC) $(CHDR)
 $(PKG)/libpfac_v_s0e0.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_STATIC_NUM=0 -DPFAC_SLOT_EXTRA=0 -shared -o $@ $(CSRC) -lcudart
 variants: $(VARLIBS)
+
+# A/B variants of the production build (tools/ab.py)
+ABLIBS := $(PKG)/libpfac_nosw.so $(PKG)/libpfac_d64.so $(PKG)/libpfac_w24.so $(PKG)/libpfac_w16.so
+$(PKG)/libpfac_nosw.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_NO_SWIZZLE -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_d64.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=64 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_w24.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=24 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_w16.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=16 -shared -o $@ $(CSRC) -lcudart
+ab: $(ABLIBS)

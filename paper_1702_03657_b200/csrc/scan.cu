@@ -43,7 +43,10 @@ namespace pfac {
 
 namespace {
 
-constexpr int kWarps = 32;
+#ifndef PFAC_WARPS
+#define PFAC_WARPS 32
+#endif
+constexpr int kWarps = PFAC_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr int kPerLane = 32;           // consecutive starts per lane per round
 constexpr int kRound = 32 * kPerLane;  // 1024 starts per warp round
@@ -61,7 +64,10 @@ constexpr int kSlotBytes = kRound + PFAC_SLOT_EXTRA;  // one round of text (+ th
 static_assert(kSlots >= 2, "ring");
 constexpr int kMaxCtas = 1024;
 constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated filter
-constexpr int kDefer = 48;             // per-warp queue of starts to walk
+#ifndef PFAC_DEFER
+#define PFAC_DEFER 48
+#endif
+constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to walk
 constexpr uint32_t kHotCap = 24576;  // hot-trie smem when the trie does not fit (rest left to L1)
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
@@ -742,7 +748,11 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             // banks once (4 wavefronts, not 8).
             uint32_t wv[kWv];
             {
+#ifdef PFAC_NO_SWIZZLE
+                const uint32_t sw = 0;
+#else
                 const uint32_t sw = (lane >> 2) & 1u;
+#endif
                 const uint4 h0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * sw);
                 const uint4 h1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * (sw ^ 1u));
                 wv[0] = sw ? h1.x : h0.x;
@@ -844,14 +854,15 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         if (lane == 31) s_wtot[warp] = incl;
         __syncthreads();
         if (warp == 0) {
-            const unsigned long long wv0 = s_wtot[lane];
+            const unsigned long long wv0 = lane < kWarps ? s_wtot[lane] : 0ull;
             unsigned long long wi = wv0;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, d);
                 if (lane >= d) wi += y;
             }
-            s_wtot[lane] = wi - wv0;
+            if (lane < kWarps) s_wtot[lane] = wi - wv0;
+            __syncwarp();
             if (lane == 31) s_wtot[kWarps] = wi;
         }
         __syncthreads();

@@ -32,17 +32,21 @@ print(" ".join("%%.2f" %% (a.elapsed_time(b) * 1e3) for a, b in ev))
 
 cid = sys.argv[1] if len(sys.argv) > 1 else "2"
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-reps = "60" if cid == "2" else "6"
-res = {"new": [], "ref": []}
+libs = sys.argv[3:] or ["libpfac_ref.so", "libpfac.so"]
+reps = "100" if cid == "2" else "6"
+res = {lib: [] for lib in libs}
 for r in range(rounds):
-    for name, lib in [("ref", "libpfac_ref.so"), ("new", "libpfac.so")]:
+    for lib in libs:
+        name = lib
         env = dict(os.environ, PFAC_LIB=os.path.join(HERE, "paper_1702_03657_b200", lib))
         out = subprocess.run([sys.executable, "-c", CHILD, cid, reps], env=env, capture_output=True, text=True)
         if out.returncode:
             print(out.stderr[-2000:])
             sys.exit(1)
         res[name] += [float(x) for x in out.stdout.split()]
-for k in ["ref", "new"]:
+# CUDA event timestamps are quantised (~2 us steps on this box): compare means
+base = np.mean(res[libs[0]])
+for k in libs:
     v = np.array(res[k])
-    print(f"C{cid} {k}: median {np.median(v):.2f} us  p10 {np.percentile(v, 10):.2f}  p90 {np.percentile(v, 90):.2f}  (n={len(v)})")
-print(f"new/ref = {np.median(res['new']) / np.median(res['ref']):.4f}")
+    print(f"C{cid} {k:24s}: mean {np.mean(v):8.2f} us  median {np.median(v):8.2f}  p10 {np.percentile(v, 10):8.2f}"
+          f"  p90 {np.percentile(v, 90):8.2f}  (n={len(v)})  x{np.mean(v) / base:.4f}")
