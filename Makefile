@@ -65,3 +65,7 @@ $(PKG)/libpfac_w24.so: $(CSRC) $(CHDR)
 $(PKG)/libpfac_w16.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=16 -shared -o $@ $(CSRC) -lcudart
 ab: $(ABLIBS)
+$(PKG)/libpfac_s2l.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_s2l_nosw.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -DPFAC_NO_SWIZZLE -shared -o $@ $(CSRC) -lcudart

@@ -712,24 +712,24 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // ================================================= phase 1: scan
     // One 1024-start round per iteration; the ring keeps kSlots-1 rounds in
     // flight.  Stage 1 filters each lane's 32 starts (bit mask).  Stage 2
-    // compacts the survivors in position order (lane-major = position order)
-    // and tests them, one per lane, against the 2-gram prefix table (the
+    // tests each survivor, in its lane, against the 2-gram prefix table (the
     // root's children and their level-1 bitmapped nodes): bytes
     // (b0, b1) begin a pattern path, or b0 alone already reaches a terminal
-    // or tail.  The few kept starts are queued (position order; a warp's
-    // rounds increase) and walked in full-warp batches to their first
+    // or tail.  The few kept starts are queued in position order (lane-major
+    // = position order; a warp's rounds increase: a ballot when no lane keeps
+    // two, else a warp scan) and walked in full-warp batches to their first
     // mismatch whenever the queue may not take another 32.
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
     uint32_t dcount = 0;  // queued starts (warp-uniform)
-    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * (kDefer + 16);
-    uint16_t *list = reinterpret_cast<uint16_t *>(dpos + kDefer);  // 32 survivor offsets
+    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * kDefer;
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
     for (;;) {
         const bool done = rid[0] >= n_local;
         const uint32_t rel = rid[0] * (uint32_t)kRound;  // round start relative to cta_lo
         const uint64_t rbase = cta_lo + rel;
         const uint8_t *p0 = ring + slot * kSlotBytes;
-        uint32_t pending = 0, tot = 0, r = 0, rlim = 0;
+        uint32_t pending = 0, tot = 0, r = 0;
+        bool single = false;
         if (!done) {
             // refill the slot of the previous round with the next round taken
             __syncwarp();  // every lane's reads of that slot precede its refill
@@ -742,27 +742,21 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #ifdef PFAC_STREAM_ONLY
             if (p0[lane] == 0xFF && a.pos_base == ~0ull) n_hits++;  // keeps the loads
 #else
-            // ---- stage 1: filter over the lane's 32 starts.  The lane's 32
-            // bytes are two 16-byte loads; lanes 4-7 of each group of 8 take
-            // the halves in the other order so that every load covers all 32
-            // banks once (4 wavefronts, not 8).
+            // ---- stage 1: filter over the lane's 32 starts (its 32 bytes: two
+            // 16-byte loads; the 2-way bank conflict of the 32-byte stride costs
+            // less than un-swizzling in registers)
             uint32_t wv[kWv];
             {
-#ifdef PFAC_NO_SWIZZLE
-                const uint32_t sw = 0;
-#else
-                const uint32_t sw = (lane >> 2) & 1u;
-#endif
-                const uint4 h0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * sw);
-                const uint4 h1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16 * (sw ^ 1u));
-                wv[0] = sw ? h1.x : h0.x;
-                wv[1] = sw ? h1.y : h0.y;
-                wv[2] = sw ? h1.z : h0.z;
-                wv[3] = sw ? h1.w : h0.w;
-                wv[4] = sw ? h0.x : h1.x;
-                wv[5] = sw ? h0.y : h1.y;
-                wv[6] = sw ? h0.z : h1.z;
-                wv[7] = sw ? h0.w : h1.w;
+                const uint4 h0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane);
+                const uint4 h1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16);
+                wv[0] = h0.x;
+                wv[1] = h0.y;
+                wv[2] = h0.z;
+                wv[3] = h0.w;
+                wv[4] = h1.x;
+                wv[5] = h1.y;
+                wv[6] = h1.z;
+                wv[7] = h1.w;
             }
             const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
             wv[kWv - 1] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound) : w8;
@@ -785,13 +779,37 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             if (pending == 0xDEADBEEFu && a.pos_base == ~0ull) n_hits++;  // experiment: filter only
             pending = 0;
 #endif
+            // ---- stage 2 in the lane: 2-gram prefix test of each survivor;
+            // `pending` becomes the kept set (sparse: appended by ballot)
+            if (Kind != 3) {
+                const uint32_t rl = rid[0] < n_fast ? (uint32_t)kSlotBytes  // readable bytes from rbase
+                                                    : (a.readable > rbase ? clamp32(a.readable - rbase) : 0u);
+                uint32_t km = 0;
+                for (uint32_t m = pending; m; m &= m - 1) {
+                    const uint32_t k = __ffs(m) - 1;
+                    const uint32_t off = lane * kPerLane + k;
+                    const uint32_t b0 = p0[off];
+                    uint32_t keep;
+                    if (off + 1 < rl) {
+                        const uint32_t b1 = p0[off + 1];  // the slot holds 16 bytes past the round
+                        keep = (s_pair[b0 * 8 + (b1 >> 5)] >> (b1 & 31)) & 1u;
+                    } else {
+                        keep = s.root[b0] != 0u;  // last readable byte: let the walk decide
+                    }
+                    km |= keep << k;
+                }
+                pending = km;
+            }
             if (__any_sync(0xffffffffu, pending != 0)) {
-                r = warp_excl_scan(__popc(pending), lane, &tot);  // rank of the lane's first survivor
-                rlim = rid[0] < n_fast ? (uint32_t)kSlotBytes                       // readable bytes from rbase
-                                       : (a.readable > rbase ? clamp32(a.readable - rbase) : 0u);
+                if (__any_sync(0xffffffffu, (pending & (pending - 1)) != 0)) {
+                    r = warp_excl_scan(__popc(pending), lane, &tot);
+                } else {
+                    single = true;  // at most one kept start per lane
+                    tot = 1;
+                }
             }
         }
-        // ---- stage 2, 32 survivors per pass; the single batch-walk site at its top
+        // ---- queue the kept starts, 32 per pass; the single batch-walk site at its top
         for (uint32_t cb = 0;; cb += 32) {
             if (dcount != 0 && (done || dcount > (uint32_t)(kDefer - 32))) {
 #if defined(PFAC_EXP) && PFAC_EXP == 2
@@ -802,31 +820,19 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 dcount = 0;
             }
             if (cb >= tot) break;
-            while (pending && r < cb + 32) {
-                list[r - cb] = (uint16_t)(lane * kPerLane + (__ffs(pending) - 1));
+            if (single) {  // append by ballot (the queue has room for 32)
+                const uint32_t kb = __ballot_sync(0xffffffffu, pending != 0);
+                if (pending) dpos[dcount + __popc(kb & ((1u << lane) - 1u))] = rel + lane * kPerLane + (__ffs(pending) - 1);
+                dcount += __popc(kb);
+                break;
+            }
+            while (pending && r < cb + 32) {  // the next 32 in position order (the queue has room for 32)
+                dpos[dcount + r - cb] = rel + lane * kPerLane + (__ffs(pending) - 1);
                 pending &= pending - 1;
                 ++r;
             }
             __syncwarp();
-            uint32_t off = 0;
-            bool keep = false;
-            if (cb + lane < tot && Kind == 3) {  // DNA: the 2-gram test keeps everything
-                off = list[lane];
-                keep = true;
-            } else if (cb + lane < tot) {
-                off = list[lane];
-                const uint32_t b0 = p0[off];
-                if (off + 1 < rlim) {
-                    const uint32_t b1 = p0[off + 1];  // the slot holds 16 bytes past the round
-                    keep = (s_pair[b0 * 8 + (b1 >> 5)] >> (b1 & 31)) & 1u;
-                } else {
-                    keep = s.root[b0] != 0u;  // last readable byte: let the walk decide
-                }
-            }
-            __syncwarp();  // list reuse
-            const uint32_t kb = __ballot_sync(0xffffffffu, keep);
-            if (keep) dpos[dcount + __popc(kb & ((1u << lane) - 1u))] = rel + off;
-            dcount += __popc(kb);
+            dcount += min(32u, tot - cb);
         }
         if (done) break;
 #pragma unroll
@@ -1138,7 +1144,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
-                           kWarps * (kDefer + 16) * 4 + 8192 +
+                           kWarps * kDefer * 4 + 8192 +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
@@ -1198,7 +1204,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 1] + the CTA's round counter
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
-    a.off_defer = o;  o += kWarps * (kDefer + 16) * 4;  // per warp: queue u32[kDefer] + survivor list u16[32]
+    a.off_defer = o;  o += kWarps * kDefer * 4;  // per warp: queue u32[kDefer]
     a.off_pair = o;   o += 8192;                          // 2-gram prefix table [256][8] words
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
