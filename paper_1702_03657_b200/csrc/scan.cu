@@ -493,10 +493,31 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
 
     STAMP(0);
-    // ---- barriers: per-warp text ring + one for the table staging
+    // ---- barriers: per-warp text ring + one for the table staging; thread 0
+    // starts the table copies (TMA bulk, evict-last) before anything else
     uint64_t *sbar = reinterpret_cast<uint64_t *>(smem + a.off_bar) + kWarps * kSlots;
+    if (tid == 0) {
+        mbar_init(sbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint64_t pl = evict_last_policy();
+        const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
+                       nb_l1 = align16(40 * a.n_level1);
+        const uint32_t nb_w = align16(4 * a.hot_words), nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
+        mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1 + 2 * nb_w + nb_t + nb_tb);
+        bulk_g2s(s_root, a.t.root, 1024, sbar, pl);
+        bulk_g2s(s_node, a.t.node, nb_node, sbar, pl);
+        if (nb_label) bulk_g2s(s_label, a.t.label, nb_label, sbar, pl);
+        bulk_g2s(s_bm, a.t.level1, nb_l1, sbar, pl);
+        if (nb_w) {
+            bulk_g2s(smem + a.off_tbits, a.t.tail_bits, nb_w, sbar, pl);
+            bulk_g2s(smem + a.off_trank, a.t.tail_rank, nb_w, sbar, pl);
+        }
+        if (nb_t) bulk_g2s(smem + a.off_tails, a.t.tails, nb_t, sbar, pl);
+        if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, pl);
+    }
     if (lane < kSlots) mbar_init(&bars[lane], 1);
-    if (tid == 0) mbar_init(sbar, 1);
+    uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 1);  // round counter of the CTA
+    if (tid == 32) *s_next = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;  // for the next launch
     __syncthreads();  // barriers initialised
@@ -525,7 +546,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
 
     const uint64_t policy = evict_first_policy();
-    const uint64_t policy_last = evict_last_policy();
     // starts < lim are valid: inside [0, n_starts) and their d-gram fits
     const uint32_t gram = a.t.gram;
     const uint64_t lim = (a.readable + 1 >= gram && a.readable + 1 - gram < a.n_starts) ? a.readable + 1 - gram
@@ -541,7 +561,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                                                                                     : n_rounds) - cta_round0);
     const uint64_t cta_lo = cta_round0 * kRound;
     uint2 *hits = a.hits + (uint64_t)gw * a.hit_cap;
-    uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 1);  // round counter of the CTA
 
     // local rounds r < n_fast have their whole slot (round + overhang) readable
     const uint32_t n_fast = !a.aligned || a.readable < cta_lo + kSlotBytes
@@ -618,28 +637,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 
     // ---- stage the tables (TMA bulk copies of the image sections; the
     // filter is replicated from 8/4-byte loads), then start streaming
-    {   // one bulk copy per warp (lane 0), so the copies are in flight together
-        const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
-                       nb_l1 = align16(40 * a.n_level1);
-        const uint32_t nb_w = align16(4 * a.hot_words), nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
-        if (tid == 0) {
-            *s_next = 0u;
-            mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1 + 2 * nb_w + nb_t + nb_tb);
-        }
-        if (lane == 0) {
-            switch (warp) {
-                case 0: bulk_g2s(s_root, a.t.root, 1024, sbar, policy_last); break;
-                case 1: bulk_g2s(s_node, a.t.node, nb_node, sbar, policy_last); break;
-                case 2: if (nb_label) bulk_g2s(s_label, a.t.label, nb_label, sbar, policy_last); break;
-                case 3: bulk_g2s(s_bm, a.t.level1, nb_l1, sbar, policy_last); break;
-                case 4: if (nb_w) bulk_g2s(smem + a.off_tbits, a.t.tail_bits, nb_w, sbar, policy_last); break;
-                case 5: if (nb_w) bulk_g2s(smem + a.off_trank, a.t.tail_rank, nb_w, sbar, policy_last); break;
-                case 6: if (nb_t) bulk_g2s(smem + a.off_tails, a.t.tails, nb_t, sbar, policy_last); break;
-                case 7: if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, policy_last); break;
-                default: break;
-            }
-        }
-    }
     STAMP(12);
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
