@@ -69,3 +69,15 @@ $(PKG)/libpfac_s2l.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_s2l_nosw.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -DPFAC_NO_SWIZZLE -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_st2.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=2 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_st0.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=0 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_st4.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=4 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_d32.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=32 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_hot200.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_HOTCAP=200000 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_hot8.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_HOTCAP=8192 -shared -o $@ $(CSRC) -lcudart

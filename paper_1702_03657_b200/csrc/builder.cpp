@@ -274,8 +274,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         for (uint32_t k = 0; k < m; k++) keys[k] = dna_key(pats[k]);
         std::sort(keys.begin(), keys.end());
         const uint64_t distinct = std::unique(keys.begin(), keys.end()) - keys.begin();
-        log2_bits = 10;  // ~32 bits per key (two of them set per key), at most 2^19 bits (64 KiB)
-        while (log2_bits < 19 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+        log2_bits = 10;  // ~32 bits per key (two of them set per key), at most 2^20 bits (128 KiB)
+        while (log2_bits < 20 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
     } else if (exact) {
         log2_bits = 8 * gram;
     } else {
@@ -291,7 +291,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         // per 4-gram -> ~128 bits per 4-gram keeps the fill near 1.6%; used
         // while that fits 2^18 bits.  Else kind 1 (blocked two-bit, ~32 bits
         // per key, ~0.5% false positives) or kind 0 (d < 4, ~3%), capped at
-        // 2^19 bits (64 KiB, the shared-memory budget).
+        // 2^20 bits (kind 1, 128 KiB) or 2^19 bits (kind 0).
         const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
         const bool allow2 = !force || force[0] != '1';
         if (kind == 1 && allow2 && distinct * 128 <= (1ull << 18)) {
@@ -299,8 +299,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
             log2_bits = 12;
             while ((1ull << log2_bits) < 128 * distinct) log2_bits++;
         } else {
-            log2_bits = 10;
-            while (log2_bits < 19 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+            log2_bits = 10;  // at most 2^20 bits (128 KiB; the kernel then keeps 2 text rounds per warp)
+            while (log2_bits < (kind == 1 ? 20u : 19u) && (1ull << log2_bits) < 32 * distinct) log2_bits++;
         }
     }
     std::vector<uint32_t> filter((size_t)1 << (log2_bits - 5 > 0 ? log2_bits - 5 : 0), 0u);

@@ -53,7 +53,8 @@ constexpr int kRound = 32 * kPerLane;  // 1024 starts per warp round
 constexpr int kRoundLog2 = 10;
 static_assert(kRound == 1 << kRoundLog2, "");
 constexpr int kWv = kPerLane / 4 + 1;  // text words a lane needs (its starts + 3 bytes)
-constexpr int kSlots = 3;              // text ring depth per warp (kSlots-1 rounds in flight)
+constexpr int kSlotsMax = 3;           // text ring depth per warp (kSlots-1 rounds in flight); 2 when the filter
+                                       // takes more than 64 KiB of shared memory
 #ifndef PFAC_SLOT_EXTRA
 #define PFAC_SLOT_EXTRA 16
 #endif
@@ -61,14 +62,17 @@ constexpr int kSlots = 3;              // text ring depth per warp (kSlots-1 rou
 #define PFAC_STATIC_NUM 3  // share of a CTA's rounds assigned statically, in quarters
 #endif
 constexpr int kSlotBytes = kRound + PFAC_SLOT_EXTRA;  // one round of text (+ the next 16 bytes: the last windows)
-static_assert(kSlots >= 2, "ring");
+static_assert(kSlotsMax >= 2, "ring");
 constexpr int kMaxCtas = 1024;
 constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated filter
 #ifndef PFAC_DEFER
 #define PFAC_DEFER 48
 #endif
 constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to walk
-constexpr uint32_t kHotCap = 24576;  // hot-trie smem when the trie does not fit (rest left to L1)
+#ifndef PFAC_HOTCAP
+#define PFAC_HOTCAP 0xFFFFFFFFu
+#endif
+constexpr uint32_t kHotCap = PFAC_HOTCAP;  // cap on hot-trie smem when the trie does not fit
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
@@ -479,7 +483,7 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
     return n_hits;
 }
 
-template <int Kind>
+template <int Kind, int kSlots>
 __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -986,6 +990,20 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     STAMP(4);
 }
 
+// Kernel instance for a filter kind and ring depth (2 slots only where the
+// filter can exceed 64 KiB: kinds 1 and 3).
+const void *kernel_for(uint32_t kind, uint32_t slots) {
+    if (slots == 2) return kind == 1 ? (const void *)pfac_scan_kernel<1, 2> : kind == 3 ? (const void *)pfac_scan_kernel<3, 2>
+                                                                                         : nullptr;
+    switch (kind) {
+        case 0: return (const void *)pfac_scan_kernel<0, 3>;
+        case 1: return (const void *)pfac_scan_kernel<1, 3>;
+        case 2: return (const void *)pfac_scan_kernel<2, 3>;
+        case 3: return (const void *)pfac_scan_kernel<3, 3>;
+        default: return nullptr;
+    }
+}
+
 struct DeviceInfo {
     bool init = false;
     int sms = 0;
@@ -1006,18 +1024,10 @@ int device_info(int device, DeviceInfo &out, std::string &err) {
         cudaError_t e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, device);
         if (e == cudaSuccess)
             e = cudaDeviceGetAttribute(&di.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(pfac_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     di.max_smem_optin);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(pfac_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     di.max_smem_optin);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(pfac_scan_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     di.max_smem_optin);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(pfac_scan_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     di.max_smem_optin);
+        for (uint32_t kind = 0; kind < 4 && e == cudaSuccess; ++kind)
+            for (uint32_t slots = 2; slots <= 3 && e == cudaSuccess; ++slots)
+                if (const void *fn = kernel_for(kind, slots))
+                    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, di.max_smem_optin);
         if (e != cudaSuccess) {
             err = std::string("device query: ") + cudaGetErrorString(e);
             return kStatusCuda;
@@ -1140,6 +1150,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
     const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
+    const uint32_t kSlots = filter_words * 4 > 65536u ? 2u : (uint32_t)kSlotsMax;  // ring depth
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
                            kWarps * kDefer * 4 + 8192 +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;
@@ -1171,9 +1182,9 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
         return align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) + 2ull * align16(4 * ((H + 31) / 32)) +
                16ull * nt + align16(tbytes_below(nt));
     };
-    // Whole trie in shared memory when it fits; otherwise only its upper
-    // levels (<= kHotCap bytes), so that the unified L1/shared array keeps a
-    // large L1 that caches the deeper nodes and tails the walks touch.
+    // Whole trie in shared memory when it fits; otherwise its upper levels
+    // (the BFS prefix) in all that is left (measured: more hot levels beat a
+    // larger L1 for the deeper ones; kHotCap is a tuning knob, default off).
     const uint32_t budget =
         hot_bytes(t.n_nodes - 1) <= trie_budget ? trie_budget : (trie_budget < kHotCap ? trie_budget : kHotCap);
     uint32_t lo = 1, hi = t.n_nodes - 1;
@@ -1263,9 +1274,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.rounds_per_cta = geo.rounds_per_cta;
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
-    const void *fn = t.kind == 3 ? (const void *)pfac_scan_kernel<3>
-                     : t.kind == 2 ? (const void *)pfac_scan_kernel<2>
-                     : t.kind == 1 ? (const void *)pfac_scan_kernel<1> : (const void *)pfac_scan_kernel<0>;
+    const void *fn = kernel_for(t.kind, kSlots);
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)geo.grid), dim3(kThreads), args, smem, stream);
     if (e != cudaSuccess) {
         {   // the kernel did not run: the barrier counter in use is unchanged
