@@ -157,53 +157,96 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
             chain_end[v] = chain_end[u];
         }
     }
-    std::vector<uint8_t> is_tail(N, 0), internal(N, 0);
+    std::vector<uint8_t> is_tail(N, 0), removed(N, 0);
     for (uint64_t v = 1; v < N; v++)
         if (chain_ok[v] && !chain_ok[parent[v]] && q[chain_end[v]].depth - q[v].depth >= 2) is_tail[v] = 1;
-    for (uint64_t v = 1; v < N; v++) internal[v] = internal[parent[v]] || is_tail[parent[v]];
+    for (uint64_t v = 1; v < N; v++) removed[v] = removed[parent[v]] || is_tail[parent[v]];
+    // ---- internal chains: a kept node v (not the root) whose single child u
+    // is non-terminal with a single child starts a chain: the nodes below v
+    // down to the first node x that is terminal, branching, a leaf or a tail
+    // start are removed, and v carries the chain's bytes and x (a walk
+    // compares the bytes in one go and continues at x; no terminal is skipped).
+    auto first_child = [&](uint64_t v) { return (uint64_t)(node_word[v] & kEdgeMask) + 1; };
+    auto is_term = [&](uint64_t v) { return (node_word[v] & kTermBit) != 0; };
+    std::vector<uint32_t> chain_to(N, kNone);
+    for (uint64_t v = 1; v < N; v++) {
+        if (removed[v] || is_tail[v] || nchild(v) != 1) continue;
+        uint64_t x = first_child(v);
+        if (is_term(x) || nchild(x) != 1 || is_tail[x]) continue;
+        while (!is_term(x) && nchild(x) == 1 && !is_tail[x]) {
+            removed[x] = 1;
+            x = first_child(x);
+        }
+        chain_to[v] = (uint32_t)x;
+    }
     std::vector<uint32_t> old_ti(N, kNone);
     for (uint64_t t = 0; t < T; t++) old_ti[term_node[t]] = (uint32_t)t;
+    // BFS numbering of the compressed tree (a chain start's one child is its
+    // chain's end), so that the child through edge e is still node e+1
+    std::vector<uint32_t> order;  // old ids in new order
+    order.reserve(N);
+    order.push_back(0);
+    for (size_t h = 0; h < order.size(); h++) {
+        const uint64_t v = order[h];
+        if (is_tail[v]) continue;
+        if (chain_to[v] != kNone) {
+            order.push_back(chain_to[v]);
+            continue;
+        }
+        for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++) order.push_back(e + 1);
+    }
+    const uint64_t NK = order.size();
     std::vector<uint32_t> new_id(N, kNone);
-    uint64_t NK = 0;
-    for (uint64_t v = 0; v < N; v++)
-        if (!internal[v]) new_id[v] = (uint32_t)NK++;
+    for (uint64_t i = 0; i < NK; i++) new_id[order[i]] = (uint32_t)i;
 
-    // compressed CSR (BFS order of the kept nodes; child through edge e is e+1)
+    // compressed CSR (bit 30 marks a tail or chain start: its record holds the bytes)
     std::vector<uint32_t> cnode;
     std::vector<uint8_t> clabel;
     std::vector<uint32_t> nterm_old;  // old terminal index of each new terminal index
     std::vector<uint32_t> cterm_node;
     cnode.reserve(NK + 1);
     clabel.reserve(NK);
-    for (uint64_t v = 0; v < N; v++) {
-        if (internal[v]) continue;
-        const bool term = (node_word[v] & kTermBit) != 0;
-        cnode.push_back((uint32_t)clabel.size() | (term ? kTermBit : 0u) | (is_tail[v] ? kTailBit : 0u));
+    for (uint64_t i = 0; i < NK; i++) {
+        const uint64_t v = order[i];
+        const bool term = is_term(v);
+        const bool rec = is_tail[v] || chain_to[v] != kNone;
+        cnode.push_back((uint32_t)clabel.size() | (term ? kTermBit : 0u) | (rec ? kTailBit : 0u));
         if (term) {
             nterm_old.push_back(old_ti[v]);
-            cterm_node.push_back(new_id[v]);
+            cterm_node.push_back((uint32_t)i);
         }
-        if (!is_tail[v])
+        if (chain_to[v] != kNone) {
+            clabel.push_back(label[node_word[v] & kEdgeMask]);  // the chain's first byte (CSR shape only)
+        } else if (!is_tail[v]) {
             for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++) clabel.push_back(label[e]);
+        }
     }
     cnode.push_back((uint32_t)clabel.size());
     const uint64_t TK = cterm_node.size();  // kept terminals: indices [0, TK), sorted by node id
     std::vector<uint32_t> tail_bits((NK + 31) / 32, 0u), tail_rank((NK + 31) / 32, 0u);
-    std::vector<uint32_t> tails;  // 4 words per tail: bytes offset, length, terminal index, 0
+    // 4 words per record: bytes offset, length, terminal index (tail) or kNone
+    // (chain), chain end node (chain) or 0 (tail)
+    std::vector<uint32_t> tails;
     std::vector<uint8_t> tail_bytes;
-    for (uint64_t v = 0; v < N; v++) {
-        if (internal[v] || !is_tail[v]) continue;
-        const uint32_t end = chain_end[v];
+    for (uint64_t i = 0; i < NK; i++) {
+        const uint64_t v = order[i];
+        if (!is_tail[v] && chain_to[v] == kNone) continue;
+        const uint32_t end = is_tail[v] ? chain_end[v] : chain_to[v];
         const uint32_t dv = q[v].depth, de = q[end].depth;
-        const uint32_t k = own_pid[end];
+        const uint32_t k = ord[q[end].lo];  // a pattern through `end`
         tails.push_back((uint32_t)tail_bytes.size());  // 4-byte aligned
         tails.push_back(de - dv);
-        tails.push_back((uint32_t)nterm_old.size());
-        tails.push_back(0u);
-        nterm_old.push_back(old_ti[end]);
+        if (is_tail[v]) {
+            tails.push_back((uint32_t)nterm_old.size());
+            tails.push_back(0u);
+            nterm_old.push_back(old_ti[end]);
+        } else {
+            tails.push_back(kNone);
+            tails.push_back(new_id[end]);
+        }
         tail_bytes.insert(tail_bytes.end(), pats[k] + dv, pats[k] + de);
         while (tail_bytes.size() & 3) tail_bytes.push_back(0);
-        tail_bits[new_id[v] >> 5] |= 1u << (new_id[v] & 31);
+        tail_bits[i >> 5] |= 1u << (i & 31);
     }
     {
         uint32_t acc = 0;
@@ -408,7 +451,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
     const uint64_t N = h.n_nodes, E = h.n_edges, T = h.n_terminals;
     auto in = [&](uint64_t off, uint64_t bytes) { return off >= sizeof(ImageHeader) && off + bytes <= size; };
     bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
-              h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails == T && h.n_nodes_full >= N &&
+              h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails >= T && h.n_nodes_full >= N &&
               in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
               in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && (h.filter_gram <= 4 || (h.filter_kind == 3 && h.filter_gram == kDnaGram)) &&
@@ -425,8 +468,15 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
              h.n_level1 == (node[1] & kEdgeMask) && h.n_level1 >= 1 && h.n_level1 <= 256;
         for (uint64_t v = 0; ok && v < N; v++) ok = (node[v] & kEdgeMask) <= (node[v + 1] & kEdgeMask);
         const uint32_t *tails = reinterpret_cast<const uint32_t *>(p + h.off_tails);
-        for (uint64_t i = 0; ok && i < h.n_tails; i++)
-            ok = (uint64_t)tails[4 * i] + tails[4 * i + 1] <= h.n_tail_bytes && tails[4 * i + 2] < T;
+        uint64_t n_tail_ends = 0;  // tail records end at a terminal; chain records at a node
+        for (uint64_t i = 0; ok && i < h.n_tails; i++) {
+            const bool chain = tails[4 * i + 2] == kNone;
+            ok = (uint64_t)tails[4 * i] + tails[4 * i + 1] <= h.n_tail_bytes &&
+                 (chain ? (tails[4 * i + 3] > 0 && tails[4 * i + 3] < N && tails[4 * i + 1] >= 2)
+                        : (tails[4 * i + 2] >= h.n_kept_terminals && tails[4 * i + 2] < T && tails[4 * i + 3] == 0));
+            n_tail_ends += !chain;
+        }
+        ok = ok && h.n_kept_terminals + n_tail_ends == T;
     }
     if (!ok) {
         err = "pfac_attach: inconsistent image sections";

@@ -25,13 +25,23 @@
 //                     terminal passed (prefix closure).
 //   root   u32[256]   child of the root per byte (0 = none): level 1 direct.
 //   tail_bits u32[ceil(N/32)], tail_rank u32[ceil(N/32)]  bit v = node v is a
-//                     tail start; rank = tail_rank[v/32] + popc(bits below v).
-//   tails  uint4[n_tails]  {offset into tail_bytes, path length L, terminal
-//                     index of the path's end, 0}.  Path compression: below a
-//                     tail start the uncompressed trie is a single path whose
-//                     only terminal is its end; those nodes are not in the
-//                     image, and a walk at a tail start compares the next L
-//                     text bytes with tail_bytes[offset, offset+L) in one go.
+//                     tail or chain start (node word bit 30); rank =
+//                     tail_rank[v/32] + popc(bits below v) = its record.
+//   tails  uint4[n_tails]  records {offset into tail_bytes, path length L,
+//                     terminal index t, chain end node x}:
+//                     * tail (x = 0): below a tail start the uncompressed trie
+//                       is a single path whose only terminal is its end; those
+//                       nodes are not in the image, and a walk at a tail start
+//                       compares the next L text bytes with tail_bytes[offset,
+//                       offset+L) in one go (match -> terminal t).
+//                     * chain (t = 0xFFFFFFFF, L >= 2): below a chain start the
+//                       trie is a single path of L edges through non-terminal
+//                       one-child nodes down to node x (terminal, branching or
+//                       a leaf); the path's inner nodes are not in the image.
+//                       A walk compares the L bytes and continues at x (depth
+//                       + L).  The chain start keeps one CSR edge (to x) so
+//                       the BFS numbering of the compressed tree keeps the
+//                       implicit child rule.
 //   tail_bytes u8[..] the labels of each tail path, concatenated (each tail
 //                     starts 4-byte aligned; 4 zero bytes of slack at the end).
 //   level1 u32[B][10] the root's children (nodes 1..B) as the paper's bitmapped
@@ -79,7 +89,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 6;
+constexpr uint32_t kVersion = 7;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;

@@ -267,13 +267,17 @@ __device__ __forceinline__ uint32_t term_index(const uint32_t *term_node, uint32
 // terminal index of node `last` (kNone stays kNone); needs `a` and `s` in scope
 #define term_of(last_) ((last_) == kNone ? kNone : term_index(s.term_node, a.t.n_kept_terminals, (last_)))
 
-// Tail jump at tail-start node v with the next text byte at offset j: below v
-// the trie is one path of L bytes ending at a terminal, so it matches iff the
-// next L text bytes equal the path's bytes.  Returns a terminal index.
+// Jump at a tail or chain start v (node word bit 30) with the next text
+// byte at offset j: its record holds the L bytes of the single path below v.
+// Tail: the path ends at a terminal; the walk ends with that terminal if the
+// next L text bytes equal the path, else with `last`.  Chain: the path ends at
+// node x; on a match the walk continues at x (*nv = x, *len = L), else it ends
+// with `last`.  *nv = kNone when the walk ends (the result is returned).
 template <class Text>
-__device__ __forceinline__ uint32_t tail_jump(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t v, uint32_t j,
-                                              uint32_t last) {
-    const bool hot = v < a.hot_nodes;  // hot tails (records + bytes) are in shared memory
+__device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t v, uint32_t j,
+                                         uint32_t last, uint32_t &nv, uint32_t &len) {
+    nv = kNone;
+    const bool hot = v < a.hot_nodes;  // hot records + bytes are in shared memory
     const uint32_t below = (1u << (v & 31)) - 1u;
     const uint32_t idx = hot ? s.tail_rank[v >> 5] + __popc(s.tail_bits[v >> 5] & below)
                              : __ldg(a.t.tail_rank + (v >> 5)) + __popc(__ldg(a.t.tail_bits + (v >> 5)) & below);
@@ -286,9 +290,18 @@ __device__ __forceinline__ uint32_t tail_jump(const ScanArgs &a, const Smem &s, 
         const uint32_t pwk = hot ? pw[k >> 2] : __ldg(pw + (k >> 2));
         if ((tx.at4(j + k) ^ pwk) & m) return term_of(last);
     }
-    return rec.z;
+    if (rec.z != kNone) return rec.z;  // tail
+    nv = rec.w;                         // chain
+    len = rec.y;
+    return kNone;
 }
 
+// Walk from the start at offset r0 to the first mismatch; returns
+// the terminal index of the deepest terminal passed, or kNone.  Level 1 (the
+// root's children, nodes [1, B]) uses the paper's bitmapped node (PAPER.md:97,
+// Fig. 3: 256-bit child bitmap + offset, child = offset + rank of c among the
+// set bits); deeper nodes use the CSR label list of the image; tail and chain
+// starts compare their path's bytes at once.
 template <class Text>
 __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0) {
     uint32_t v = s.root[tx.at(r0)];
@@ -296,44 +309,47 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
     uint32_t w = node_word(a, s, v);
     uint32_t last = (w & kTermBit) ? v : kNone;
     uint32_t j = r0 + 1;
-    if (j >= tx.end) return term_of(last);
-    if (w & kTailBit) return tail_jump(a, s, tx, v, j, last);
-    {   // level 1 -> 2 through the bitmap
-        const uint32_t c = tx.at(j);
-        const uint32_t *bm = s.bm + (v - 1) * 10;
-        const uint32_t word = bm[c >> 5];
-        if (!((word >> (c & 31)) & 1u)) return term_of(last);
-        const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
-        v = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
-        w = node_word(a, s, v);
-        if (w & kTermBit) last = v;
-        ++j;
-    }
-    for (; j < tx.end; ++j) {
-        if (w & kTailBit) return tail_jump(a, s, tx, v, j, last);
-        const uint32_t lo0 = w & kEdgeMask;
-        const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
-        if (lo0 == hi0) break;  // leaf
-        const uint32_t c = tx.at(j);
-        uint32_t found = kNone;
-        if (hi0 - lo0 == 1) {
-            if (label_at(a, s, lo0) == c) found = lo0;
+    bool l1 = true;  // v is a level-1 node: the next step uses its bitmap
+    while (j < tx.end) {
+        uint32_t nv = kNone;
+        if (w & kTailBit) {
+            uint32_t len = 0;
+            const uint32_t r = jump(a, s, tx, v, j, last, nv, len);
+            if (nv == kNone) return r;
+            j += len;
         } else {
-            uint32_t lo = lo0, hi = hi0;  // labels[lo, hi) ascending
-            while (hi - lo > 4) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (label_at(a, s, mid) <= c) lo = mid; else hi = mid;
-            }
-            for (uint32_t k = lo; k < hi; ++k) {
-                const uint32_t l = label_at(a, s, k);
-                if (l >= c) {
-                    if (l == c) found = k;
-                    break;
+            const uint32_t c = tx.at(j);
+            if (l1) {  // level 1 -> 2 through the bitmap
+                const uint32_t *bm = s.bm + (v - 1) * 10;
+                const uint32_t word = bm[c >> 5];
+                if (!((word >> (c & 31)) & 1u)) break;
+                const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
+                nv = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
+            } else {
+                const uint32_t lo0 = w & kEdgeMask;
+                const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
+                if (hi0 - lo0 == 1) {
+                    if (label_at(a, s, lo0) == c) nv = lo0 + 1;
+                } else {
+                    uint32_t lo = lo0, hi = hi0;  // labels[lo, hi) ascending
+                    while (hi - lo > 4) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (label_at(a, s, mid) <= c) lo = mid; else hi = mid;
+                    }
+                    for (uint32_t k = lo; k < hi; ++k) {
+                        const uint32_t l = label_at(a, s, k);
+                        if (l >= c) {
+                            if (l == c) nv = k + 1;  // BFS order: the child through edge e is node e+1
+                            break;
+                        }
+                    }
                 }
             }
+            if (nv == kNone) break;  // mismatch: the thread terminates
+            ++j;
         }
-        if (found == kNone) break;  // mismatch: the thread terminates
-        v = found + 1;              // BFS order: the child through edge e is node e+1
+        l1 = false;
+        v = nv;
         w = node_word(a, s, v);
         if (w & kTermBit) last = v;
     }

@@ -105,36 +105,43 @@ def term_of(h, last):
 
 
 def walk(h, text, i, L):
-    """Terminal index of the deepest terminal passed by the walk from start i."""
+    """Terminal index of the deepest terminal passed by the walk from start i.
+    Bit 30 marks a tail start (record ends at a terminal: compare and stop) or
+    a chain start (record ends at node x: compare, continue at x)."""
     node, label = h["node"], h["label"]
     v = int(h["root"][text[i]])
     if v == 0:
         return None
     last = v if node[v] & TERM else None
     j = i + 1
+    l1 = True
     while j < L:
-        if node[v] & TAIL:  # path-compressed tail: compare its bytes at once
-            off, ln, ti, _ = (int(x) for x in h["tails"][tail_index(h, v)])
-            if j + ln <= L and bytes(text[j:j + ln]) == h["tail_bytes"][off:off + ln].tobytes():
+        if node[v] & TAIL:
+            off, ln, ti, x = (int(y) for y in h["tails"][tail_index(h, v)])
+            if not (j + ln <= L and bytes(text[j:j + ln]) == h["tail_bytes"][off:off + ln].tobytes()):
+                return term_of(h, last)
+            if ti != 0xFFFFFFFF:  # tail: ends at its terminal
                 return ti
-            return term_of(h, last)
-        s, e = int(node[v]) & MASK, int(node[v + 1]) & MASK
-        if 1 <= v <= h["n_level1"]:  # level 1: the bitmapped node (PAPER.md:97)
-            bm = [int(x) for x in h["level1"][v - 1]]
-            c = text[j]
-            if not (bm[c >> 5] >> (c & 31)) & 1:
-                break
-            pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFF
-            v = s + pre + bin(bm[c >> 5] & ((1 << (c & 31)) - 1)).count("1") + 1
+            v, j = x, j + ln  # chain: continue at its end node
         else:
-            labs = label[s:e]
-            k = np.searchsorted(labs, text[j])
-            if k >= len(labs) or labs[k] != text[j]:
-                break
-            v = s + int(k) + 1
+            s_, e_ = int(node[v]) & MASK, int(node[v + 1]) & MASK
+            if l1:  # level 1: the bitmapped node (PAPER.md:97)
+                bm = [int(y) for y in h["level1"][v - 1]]
+                c = text[j]
+                if not (bm[c >> 5] >> (c & 31)) & 1:
+                    break
+                pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFF
+                v = s_ + pre + bin(bm[c >> 5] & ((1 << (c & 31)) - 1)).count("1") + 1
+            else:
+                labs = label[s_:e_]
+                k = np.searchsorted(labs, text[j])
+                if k >= len(labs) or labs[k] != text[j]:
+                    break
+                v = s_ + int(k) + 1
+            j += 1
+        l1 = False
         if node[v] & TERM:
             last = v
-        j += 1
     return term_of(h, last)
 
 
