@@ -328,8 +328,23 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
             } else {
                 const uint32_t lo0 = w & kEdgeMask;
                 const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
-                if (hi0 - lo0 == 1) {
-                    if (label_at(a, s, lo0) == c) nv = lo0 + 1;
+                if (hi0 - lo0 <= 16) {
+                    // labels[lo0, hi0) lie in <= 5 aligned words: load them all
+                    // at once and compare 4 bytes per word (a label occurs once)
+                    const bool hotl = hi0 <= a.hot_edges;
+                    const uint32_t base = lo0 & ~3u, c4 = c * 0x01010101u;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) {
+                        const uint32_t e0 = base + 4 * q;
+                        if (e0 < hi0) {
+                            const uint32_t wq = hotl ? *reinterpret_cast<const uint32_t *>(s.label + e0)
+                                                     : __ldg(reinterpret_cast<const uint32_t *>(a.t.label + e0));
+                            uint32_t eq = __vcmpeq4(wq, c4);
+                            if (e0 < lo0) eq &= 0xFFFFFFFFu << (8 * (lo0 - e0));
+                            if (hi0 - e0 < 4) eq &= (1u << (8 * (hi0 - e0))) - 1u;
+                            if (eq) nv = e0 + ((__ffs(eq) - 1) >> 3) + 1;  // the child through edge e is node e+1
+                        }
+                    }
                 } else {
                     uint32_t lo = lo0, hi = hi0;  // labels[lo, hi) ascending
                     while (hi - lo > 4) {
