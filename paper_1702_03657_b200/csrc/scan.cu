@@ -296,6 +296,55 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
     return kNone;
 }
 
+// Child of node v (node word w) through byte c, or kNone: level-1 nodes by
+// their bitmap (Fig. 3), deeper nodes by their CSR labels.
+__device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, uint32_t v, uint32_t w, uint32_t c,
+                                     bool l1) {
+    uint32_t nv = kNone;
+    if (l1) {  // level 1 -> 2 through the bitmap
+        const uint32_t *bm = s.bm + (v - 1) * 10;
+        const uint32_t word = bm[c >> 5];
+        if (!((word >> (c & 31)) & 1u)) return kNone;
+        const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
+        nv = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
+    } else {
+        const uint32_t lo0 = w & kEdgeMask;
+        const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
+        if (hi0 - lo0 <= 16) {
+            // labels[lo0, hi0) lie in <= 5 aligned words: load them all
+            // at once and compare 4 bytes per word (a label occurs once)
+            const bool hotl = hi0 <= a.hot_edges;
+            const uint32_t base = lo0 & ~3u, c4 = c * 0x01010101u;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const uint32_t e0 = base + 4 * q;
+                if (e0 < hi0) {
+                    const uint32_t wq = hotl ? *reinterpret_cast<const uint32_t *>(s.label + e0)
+                                             : __ldg(reinterpret_cast<const uint32_t *>(a.t.label + e0));
+                    uint32_t eq = __vcmpeq4(wq, c4);
+                    if (e0 < lo0) eq &= 0xFFFFFFFFu << (8 * (lo0 - e0));
+                    if (hi0 - e0 < 4) eq &= (1u << (8 * (hi0 - e0))) - 1u;
+                    if (eq) nv = e0 + ((__ffs(eq) - 1) >> 3) + 1;  // the child through edge e is node e+1
+                }
+            }
+        } else {
+            uint32_t lo = lo0, hi = hi0;  // labels[lo, hi) ascending
+            while (hi - lo > 4) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (label_at(a, s, mid) <= c) lo = mid; else hi = mid;
+            }
+            for (uint32_t k = lo; k < hi; ++k) {
+                const uint32_t l = label_at(a, s, k);
+                if (l >= c) {
+                    if (l == c) nv = k + 1;  // BFS order: the child through edge e is node e+1
+                    break;
+                }
+            }
+        }
+    }
+    return nv;
+}
+
 // Walk from the start at offset r0 to the first mismatch; returns
 // the terminal index of the deepest terminal passed, or kNone.  Level 1 (the
 // root's children, nodes [1, B]) uses the paper's bitmapped node (PAPER.md:97,
@@ -319,47 +368,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
             j += len;
         } else {
             const uint32_t c = tx.at(j);
-            if (l1) {  // level 1 -> 2 through the bitmap
-                const uint32_t *bm = s.bm + (v - 1) * 10;
-                const uint32_t word = bm[c >> 5];
-                if (!((word >> (c & 31)) & 1u)) break;
-                const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
-                nv = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
-            } else {
-                const uint32_t lo0 = w & kEdgeMask;
-                const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
-                if (hi0 - lo0 <= 16) {
-                    // labels[lo0, hi0) lie in <= 5 aligned words: load them all
-                    // at once and compare 4 bytes per word (a label occurs once)
-                    const bool hotl = hi0 <= a.hot_edges;
-                    const uint32_t base = lo0 & ~3u, c4 = c * 0x01010101u;
-#pragma unroll
-                    for (int q = 0; q < 5; ++q) {
-                        const uint32_t e0 = base + 4 * q;
-                        if (e0 < hi0) {
-                            const uint32_t wq = hotl ? *reinterpret_cast<const uint32_t *>(s.label + e0)
-                                                     : __ldg(reinterpret_cast<const uint32_t *>(a.t.label + e0));
-                            uint32_t eq = __vcmpeq4(wq, c4);
-                            if (e0 < lo0) eq &= 0xFFFFFFFFu << (8 * (lo0 - e0));
-                            if (hi0 - e0 < 4) eq &= (1u << (8 * (hi0 - e0))) - 1u;
-                            if (eq) nv = e0 + ((__ffs(eq) - 1) >> 3) + 1;  // the child through edge e is node e+1
-                        }
-                    }
-                } else {
-                    uint32_t lo = lo0, hi = hi0;  // labels[lo, hi) ascending
-                    while (hi - lo > 4) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (label_at(a, s, mid) <= c) lo = mid; else hi = mid;
-                    }
-                    for (uint32_t k = lo; k < hi; ++k) {
-                        const uint32_t l = label_at(a, s, k);
-                        if (l >= c) {
-                            if (l == c) nv = k + 1;  // BFS order: the child through edge e is node e+1
-                            break;
-                        }
-                    }
-                }
-            }
+            nv = child_of(a, s, v, w, c, l1);
             if (nv == kNone) break;  // mismatch: the thread terminates
             ++j;
         }
