@@ -11,7 +11,7 @@ PKG     := paper_1702_03657_b200
 CSRC    := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cpp)
 CHDR    := $(wildcard $(PKG)/csrc/*.h) $(wildcard $(PKG)/csrc/*.cuh) include/pfac.h
 
-all: gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so
+all: gen/libpfacgen.so oracle/liboracle.so $(PKG)/libpfac.so tools/probe/libkb0.so
 
 gen/libpfacgen.so: gen/pfac_gen.c gen/pfac_gen.h
 	$(CC) $(CFLAGS) -shared -o $@ gen/pfac_gen.c -lm -lpthread
@@ -81,3 +81,7 @@ $(PKG)/libpfac_hot200.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_HOTCAP=200000 -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_hot8.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_HOTCAP=8192 -shared -o $@ $(CSRC) -lcudart
+
+# KB0 read-stream probe (bench.py reports its bandwidth next to the scan)
+tools/probe/libkb0.so: tools/probe/kb0.cu
+	$(NVCC) $(NVFLAGS) -shared -o $@ $< -lcudart

@@ -160,6 +160,41 @@ def run_reference(args, rank):
     }), flush=True)
 
 
+def read_stream_ceiling(dev, text, flush, scan_s):
+    """KB0 (tools/probe/kb0.cu): a pure 16-byte read stream, timed like the scan
+    (L2 flushed outside CUDA events), on the bench's own text buffer and on a
+    1 GiB buffer: the read-only ceiling next to the copy-based MEASURED_PEAKS
+    figure.  Outside the scan's timed region; None if the probe is not built."""
+    import ctypes as C
+
+    import torch
+    lib_path = os.path.join(ROOT, "tools", "probe", "libkb0.so")
+    if not os.path.exists(lib_path):
+        return None
+    lib = C.CDLL(lib_path)
+    lib.kb0_launch.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.zeros(sms * 4 * 16, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    out = {}
+    for name, buf in [("bench_text", text), ("1GiB", torch.ones(1 << 30, dtype=torch.uint8, device=dev))]:
+        n = buf.numel() // 16 * 16
+        ts = []
+        for i in range(12):
+            flush.fill_(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            lib.kb0_launch(buf.data_ptr(), n, sink.data_ptr(), sms, stream.cuda_stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(a.elapsed_time(b) / 1e3)
+        t = sum(ts) / len(ts)
+        out[name] = {"bytes": n, "us": 1e6 * t, "GBs": n / t / 1e9}
+    out["scan_vs_kb0_same_bytes"] = out["bench_text"]["us"] / (1e6 * scan_s)
+    return out
+
+
 def cpu_baseline(seconds):
     """Oracle timed on a bounded sample of the same workload (rank 0, N=1)."""
     import gen
@@ -293,6 +328,8 @@ def main():
                "h2d_bytes_per_step": int(r1 - r0), "d2h_bytes_per_step": int(8 + 12 * len(pos)),
                "api": "pfac_match (host buffers)"}
 
+    kb0 = read_stream_ceiling(dev, text, flush, kern_s) if rank == 0 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_seconds)
@@ -320,6 +357,7 @@ def main():
                            "image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed")},
             "step_ms": {"median": statistics.median(per_step), "min": min(per_step), "max": max(per_step)},
             "paper_context": PAPER_CONTEXT,
+            "kb0": kb0,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
