@@ -15,21 +15,24 @@
 //    nodes of the breadth-first CSR trie (BFS order = level order, so the
 //    first H nodes are the hot upper levels; PAPER.md:89 kept row_ptr on chip
 //    for the same reason).
-//  * phase 1 (scan): warp w owns a contiguous range of 1024-start rounds.  A
-//    per-warp ring of kSlots 1 KiB slots is filled by TMA bulk copies
-//    (cp.async.bulk + mbarrier, evict-first in L2) kSlots-1 rounds ahead.
-//    Per round each lane tests its 32 consecutive starts against the filter
-//    (a clear bit means no pattern can start there: PFAC's early termination
-//    taken before the first trie access).  Each survivor gets an in-lane
-//    first check (root table + level-1 bitmapped node); the few that pass are
-//    deferred to a per-warp queue and walked in full-warp batches to the first
-//    mismatch.  A start that passed a terminal is appended, in position
-//    order, to the warp's hit list (offset, terminal index).
-//  * phase 2 (offsets): per-warp match counts -> CTA scan -> one grid barrier
-//    -> exclusive prefix over CTA totals.  Ranges are contiguous and ordered,
-//    so the concatenation is globally sorted by (pos, pid).
-//  * phase 3 (emit): each warp expands its hit list into (pos, pid) rows.  A
-//    warp whose list overflowed re-scans its range writing rows directly.
+//  * phase 1 (scan): CTA b owns a contiguous range of 1024-start rounds; its
+//    warps take them statically interleaved, the last quarter from a shared
+//    counter.  A per-warp ring of kSlots slots (1 KiB + 16-byte overhang) is
+//    filled by TMA bulk copies (cp.async.bulk + mbarrier, evict-first in L2)
+//    kSlots-1 rounds ahead.  Per round each lane tests its 32 consecutive
+//    starts against the filter (a clear bit means no pattern can start there:
+//    PFAC's early termination taken before the first trie access), then
+//    tests each survivor against the 2-gram prefix table (level-1 bitmapped
+//    nodes); the few kept are queued in position order and walked in
+//    full-warp batches to the first mismatch.  A start that passed a terminal
+//    is appended, in position order, to the warp's hit list (offset, terminal
+//    index), its pid count to the round's count.
+//  * phase 2 (offsets): CTA exclusive scan of the round counts -> one grid
+//    barrier -> exclusive prefix over CTA totals.  Ranges are contiguous and
+//    ordered, so the concatenation is globally sorted by (pos, pid).
+//  * phase 3 (emit): each warp expands its hit list into (pos, pid) rows (a
+//    segmented scan gives each row its index).  A warp whose list overflowed
+//    re-scans its rounds writing rows directly.
 #include <cuda_runtime.h>
 
 #include <cstdio>
