@@ -222,6 +222,33 @@ def _full_size_check(cid, n_bytes, windows=6, win=1 << 20):
     return len(pos)
 
 
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_configs_unaligned_exact(cid):
+    """4 MiB of each config's text at a 16-byte-unaligned device address (the
+    lane-copy ring path instead of TMA for every round), every filter kind
+    and ring depth, compared with the oracle element by element."""
+    ps = gen.patterns(cid)
+    text = gen.text(cid, 0, 4 << 20)
+    want = oracle.Trie(ps).match(text)
+    assert_same(gpu_rows(pf.Trie(ps), text, offset=5), want, f"C{cid} unaligned 4 MiB")
+
+
+def test_dna_filter_other_bytes():
+    """Kind 3 (DNA k-mer filter): bytes outside {A,C,G,T} (N, lowercase, any
+    byte) alias in the 2-bit code; they may only add filter survivors, never
+    drop a match.  Text = C5 text with 2% of its bytes replaced."""
+    ps = gen.patterns(5)
+    text = gen.text(5, 0, 2 << 20).copy()
+    rng = np.random.default_rng(55)
+    idx = rng.choice(len(text), len(text) // 50, replace=False)
+    text[idx] = rng.choice(np.frombuffer(b"NnacgtRYK\x00\xff", np.uint8), len(idx))
+    t = pf.Trie(ps)
+    assert t.stats()["filter_gram"] == 16  # kind 3 in use
+    want = oracle.Trie(ps).match(text)
+    assert len(want[0]) > 0
+    assert_same(gpu_rows(t, text), want, "C5 text with non-ACGT bytes")
+
+
 def test_full_c2_exact():
     ps = gen.patterns(2)
     n = gen.config(2)["text_len"]
