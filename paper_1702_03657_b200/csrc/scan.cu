@@ -313,21 +313,29 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
     } else {
         const uint32_t lo0 = w & kEdgeMask;
         const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
-        if (hi0 - lo0 <= 16) {
-            // labels[lo0, hi0) lie in <= 5 aligned words: load them all
-            // at once and compare 4 bytes per word (a label occurs once)
+        const uint32_t deg = hi0 - lo0;
+        if (deg == 1) {
+            if (label_at(a, s, lo0) == c) nv = lo0 + 1;
+        } else if (deg <= 16) {
+            // labels[lo0, hi0) lie in <= 5 aligned words: load them at once and
+            // find the byte equal to c with the zero-byte test on (word ^ c),
+            // bytes outside the node forced non-zero (a label occurs once, and
+            // the lowest flagged byte of the test is exact)
             const bool hotl = hi0 <= a.hot_edges;
-            const uint32_t base = lo0 & ~3u, c4 = c * 0x01010101u;
-#pragma unroll
-            for (int q = 0; q < 5; ++q) {
+            const uint32_t base = lo0 & ~3u, c4 = c * 0x01010101u, nw = (hi0 - base + 3) >> 2;
+#pragma unroll 1
+            for (uint32_t q = 0; q < nw; ++q) {
                 const uint32_t e0 = base + 4 * q;
-                if (e0 < hi0) {
-                    const uint32_t wq = hotl ? *reinterpret_cast<const uint32_t *>(s.label + e0)
-                                             : __ldg(reinterpret_cast<const uint32_t *>(a.t.label + e0));
-                    uint32_t eq = __vcmpeq4(wq, c4);
-                    if (e0 < lo0) eq &= 0xFFFFFFFFu << (8 * (lo0 - e0));
-                    if (hi0 - e0 < 4) eq &= (1u << (8 * (hi0 - e0))) - 1u;
-                    if (eq) nv = e0 + ((__ffs(eq) - 1) >> 3) + 1;  // the child through edge e is node e+1
+                const uint32_t wq = hotl ? *reinterpret_cast<const uint32_t *>(s.label + e0)
+                                         : __ldg(reinterpret_cast<const uint32_t *>(a.t.label + e0));
+                uint32_t oor = 0;  // 0xFF in the bytes outside [lo0, hi0)
+                if (e0 < lo0) oor = (1u << (8 * (lo0 - e0))) - 1u;
+                if (hi0 - e0 < 4) oor |= ~((1u << (8 * (hi0 - e0))) - 1u);
+                const uint32_t x = (wq ^ c4) | oor;
+                const uint32_t f = (x - 0x01010101u) & ~x & 0x80808080u;
+                if (f) {
+                    nv = e0 + ((__ffs(f) - 1) >> 3) + 1;  // the child through edge e is node e+1
+                    break;
                 }
             }
         } else {

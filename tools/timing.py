@@ -37,12 +37,16 @@ b = b[used]
 t0 = b[:, 0].min()
 names = ["start", "tables staged", "phase1 end", "offsets known", "end", "tables arrived", "first text in",
          "local scan done", "filter copied", "after sync", "first issued", "mbar init synced",
-         "table copies issued"]
+         "table copies issued", "-", "last round done"]
 print(f"config C{cid}, {n} bytes, {used.sum()} warps; times in us relative to the first warp start")
 for k, nm in enumerate(names):
+    if nm == "-":
+        continue
     col = (b[:, k] - t0) / 1e3
     print(f"{nm:15s} min {col.min():8.2f} med {np.median(col):8.2f} p90 {np.percentile(col, 90):8.2f} max {col.max():8.2f}")
 ph1 = (b[:, 2] - b[:, 1]) / 1e3
+fl = (b[:, 2] - b[:, 13]) / 1e3
+print(f"final queue flush per warp: med {np.median(fl):.2f} p90 {np.percentile(fl, 90):.2f} max {fl.max():.2f} us")
 print(f"phase-1 duration per warp: min {ph1.min():.2f} med {np.median(ph1):.2f} max {ph1.max():.2f} us")
 # per-CTA view: is the phase-1 end spread between SMs or between warps of one SM?
 W = 32
