@@ -272,6 +272,24 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     out_pid.swap(cout_pid);
     const uint64_t NI = NK, EI = NK - 1;  // image nodes / edges
 
+    // ---- aux word per node (one load next to the node word, no dependent
+    // label or rank loads): record index of a tail/chain start; the labels of
+    // a node with 1..4 children, packed little-endian; 0 otherwise
+    std::vector<uint32_t> aux(NI, 0u);
+    {
+        uint32_t rank = 0;
+        for (uint64_t v = 0; v < NI; v++) {
+            const uint32_t e0 = node_word[v] & kEdgeMask, e1 = node_word[v + 1] & kEdgeMask;
+            if (node_word[v] & kTailBit) {
+                aux[v] = rank++;
+            } else if (e1 - e0 >= 1 && e1 - e0 <= 4) {
+                uint32_t x = 0;
+                for (uint32_t e = e0; e < e1; e++) x |= (uint32_t)label[e] << (8 * (e - e0));
+                aux[v] = x;
+            }
+        }
+    }
+
     // ---- level 1 as bitmapped nodes (Fig. 3)
     const uint32_t B = node_word[1] & kEdgeMask;  // root's children are nodes 1..B
     std::vector<uint32_t> level1((size_t)B * 10, 0u);
@@ -393,6 +411,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     h.filter_kind = kind;
     uint64_t o = align256(sizeof(ImageHeader));
     h.off_node = o;      o = align256(o + 4 * (NI + 1));
+    const uint64_t off_aux = aux_offset(h.off_node, NI);  o = align256(off_aux + 4 * NI);  // aux u32[N] (image.h)
     h.off_label = o;     o = align256(o + EI + 16);
     h.off_term_node = o; o = align256(o + 4 * TK);
     h.off_out_ptr = o;   o = align256(o + 4 * (T + 1));
@@ -422,6 +441,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     uint8_t *p = image.data();
     std::memcpy(p, &h, sizeof h);
     std::memcpy(p + h.off_node, node_word.data(), 4 * (NI + 1));
+    std::memcpy(p + off_aux, aux.data(), 4 * NI);
     if (EI) std::memcpy(p + h.off_label, label.data(), EI);
     if (TK) std::memcpy(p + h.off_term_node, term_node.data(), 4 * TK);
     std::memcpy(p + h.off_out_ptr, out_ptr.data(), 4 * (T + 1));
@@ -450,7 +470,9 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
     }
     const uint64_t N = h.n_nodes, E = h.n_edges, T = h.n_terminals;
     auto in = [&](uint64_t off, uint64_t bytes) { return off >= sizeof(ImageHeader) && off + bytes <= size; };
+    const uint64_t off_aux = aux_offset(h.off_node, N);  // image.h: aux follows node
     bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
+              in(off_aux, 4 * N) && off_aux + 4 * N <= h.off_label &&
               h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails >= T && h.n_nodes_full >= N &&
               in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&

@@ -13,6 +13,11 @@
 //                     node are consecutive and in ascending byte order, so the
 //                     child reached through edge e is node e+1 (implicit
 //                     col_ind: the BFS numbering makes it redundant).
+//   aux    u32[N]     at align256(off_node + 4(N+1)) (no header field): per
+//                     node, its record index if it is a tail/chain start, else
+//                     its labels packed little-endian if it has 1..4 children,
+//                     else 0.  Read next to the node word, it saves the walk a
+//                     dependent label (or rank) load per level.
 //   label  u8[E]      edge labels (CRS val, one byte per edge).
 //   term_node u32[TK] ascending ids of the terminal nodes kept in the image
 //                     (terminal indices 0..TK-1); terminal indices TK..T-1 are
@@ -89,7 +94,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 7;
+constexpr uint32_t kVersion = 8;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -115,6 +120,10 @@ struct ImageHeader {
 };
 static_assert(sizeof(ImageHeader) == 256, "header must be 256 bytes");
 
+// Offset of the aux section (it follows the node section).
+PFAC_HD inline uint64_t aux_offset(uint64_t off_node, uint64_t n_nodes) {
+    return (off_node + 4 * (n_nodes + 1) + 255) / 256 * 256;
+}
 // Kind 0: filter bit index of a little-endian packed d-gram key (d < 4).
 PFAC_HD inline uint32_t filter_index(uint32_t key, uint32_t log2_bits, uint32_t exact) {
     return exact ? key : (key * kFilterMul) >> (32u - log2_bits);

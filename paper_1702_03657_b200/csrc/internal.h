@@ -31,6 +31,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err);
 // Device-side view of an uploaded image (pointers into device memory).
 struct DevTrie {
     const uint32_t *node;
+    const uint32_t *aux;  // per node: record index or packed labels (image.h)
     const uint8_t *label;
     const uint32_t *term_node;
     const uint32_t *out_ptr;

@@ -107,9 +107,9 @@ struct ScanArgs {
     // shared-memory layout (bytes from the dynamic smem base; filter at 0)
     uint32_t filter_words;          // words of the (unreplicated) filter
     uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
-    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_defer, off_pair;
-    uint32_t off_tbits, off_trank, off_tails, off_tbytes;
-    uint32_t hot_tails, hot_tail_bytes, hot_words;  // tails of nodes < H; bitmap words ceil(H/32)
+    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_defer, off_pair, off_aux;
+    uint32_t off_tails, off_tbytes;
+    uint32_t hot_tails, hot_tail_bytes;  // records (and their bytes) of the record nodes < H
     uint32_t off_terms;             // out_ptr[T+1] + term_node[TK] in smem (0 = in global memory)
     uint32_t n_level1;              // B: the root's children are nodes [1, B]
     uint32_t hot_nodes;             // H: node words [0, H] resident
@@ -215,9 +215,8 @@ struct Smem {
     const uint32_t *root;       // level-1 table: child of the root per byte
     const uint32_t *bm;         // level-1 bitmapped nodes, 10 words each (see below)
     const uint32_t *node;       // node words [0, H]
+    const uint32_t *aux;        // aux words [0, H]
     const uint8_t *label;       // labels [0, hot_edges)
-    const uint32_t *tail_bits;  // tail-start bitmap / rank words for nodes [0, H)
-    const uint32_t *tail_rank;
     const uint4 *tails;         // tail records [0, hot_tails)
     const uint8_t *tail_bytes;  // their bytes [0, hot_tail_bytes)
     const uint32_t *out_ptr;    // pid-list offsets by terminal index (smem or global)
@@ -226,6 +225,9 @@ struct Smem {
 
 __device__ __forceinline__ uint32_t node_word(const ScanArgs &a, const Smem &s, uint32_t v) {
     return v <= a.hot_nodes ? s.node[v] : __ldg(a.t.node + v);
+}
+__device__ __forceinline__ uint32_t aux_word(const ScanArgs &a, const Smem &s, uint32_t v) {
+    return v <= a.hot_nodes ? s.aux[v] : __ldg(a.t.aux + v);
 }
 __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, uint32_t e) {
     return e < a.hot_edges ? (uint32_t)s.label[e] : (uint32_t)__ldg(a.t.label + e);
@@ -281,9 +283,7 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
                                          uint32_t last, uint32_t &nv, uint32_t &len) {
     nv = kNone;
     const bool hot = v < a.hot_nodes;  // hot records + bytes are in shared memory
-    const uint32_t below = (1u << (v & 31)) - 1u;
-    const uint32_t idx = hot ? s.tail_rank[v >> 5] + __popc(s.tail_bits[v >> 5] & below)
-                             : __ldg(a.t.tail_rank + (v >> 5)) + __popc(__ldg(a.t.tail_bits + (v >> 5)) & below);
+    const uint32_t idx = aux_word(a, s, v);  // the record's index (= rank among the record nodes)
     const uint4 rec = hot ? s.tails[idx] : __ldg(a.t.tails + idx);
     if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(last);
     const uint32_t *pw = reinterpret_cast<const uint32_t *>((hot ? s.tail_bytes : a.t.tail_bytes) + rec.x);
@@ -314,8 +314,12 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
         const uint32_t lo0 = w & kEdgeMask;
         const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
         const uint32_t deg = hi0 - lo0;
-        if (deg == 1) {
-            if (label_at(a, s, lo0) == c) nv = lo0 + 1;
+        if (deg <= 4) {  // the labels are packed in the node's aux word (loaded beside the node words)
+            if (deg != 0) {
+                const uint32_t x = (aux_word(a, s, v) ^ (c * 0x01010101u)) | (0xFFFFFFFFu << (8 * deg - 1) << 1);
+                const uint32_t f = (x - 0x01010101u) & ~x & 0x80808080u;
+                if (f) nv = lo0 + ((__ffs(f) - 1) >> 3) + 1;  // the child through edge e is node e+1
+            }
         } else if (deg <= 16) {
             // labels[lo0, hi0) lie in <= 5 aligned words: load them at once and
             // find the byte equal to c with the zero-byte test on (word ^ c),
@@ -557,16 +561,13 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         const uint64_t pl = evict_last_policy();
         const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
                        nb_l1 = align16(40 * a.n_level1);
-        const uint32_t nb_w = align16(4 * a.hot_words), nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
-        mbar_arrive_expect_tx(sbar, 1024 + nb_node + nb_label + nb_l1 + 2 * nb_w + nb_t + nb_tb);
+        const uint32_t nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
+        mbar_arrive_expect_tx(sbar, 1024 + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb);
         bulk_g2s(s_root, a.t.root, 1024, sbar, pl);
         bulk_g2s(s_node, a.t.node, nb_node, sbar, pl);
+        bulk_g2s(smem + a.off_aux, a.t.aux, nb_node, sbar, pl);  // aux words [0, H] (same size)
         if (nb_label) bulk_g2s(s_label, a.t.label, nb_label, sbar, pl);
         bulk_g2s(s_bm, a.t.level1, nb_l1, sbar, pl);
-        if (nb_w) {
-            bulk_g2s(smem + a.off_tbits, a.t.tail_bits, nb_w, sbar, pl);
-            bulk_g2s(smem + a.off_trank, a.t.tail_rank, nb_w, sbar, pl);
-        }
         if (nb_t) bulk_g2s(smem + a.off_tails, a.t.tails, nb_t, sbar, pl);
         if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, pl);
     }
@@ -584,9 +585,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     s.root = s_root;
     s.bm = s_bm;
     s.node = s_node;
+    s.aux = reinterpret_cast<const uint32_t *>(smem + a.off_aux);
     s.label = s_label;
-    s.tail_bits = reinterpret_cast<const uint32_t *>(smem + a.off_tbits);
-    s.tail_rank = reinterpret_cast<const uint32_t *>(smem + a.off_trank);
     s.tails = reinterpret_cast<const uint4 *>(smem + a.off_tails);
     s.tail_bytes = smem + a.off_tbytes;
     // filter addressing: copies interleaved at the unit the kernel loads
@@ -1125,6 +1125,7 @@ Geometry geometry(uint64_t n_starts, int sms) {
 DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     DevTrie t;
     t.node = reinterpret_cast<const uint32_t *>(d + h.off_node);
+    t.aux = reinterpret_cast<const uint32_t *>(d + aux_offset(h.off_node, h.n_nodes));
     t.label = d + h.off_label;
     t.term_node = reinterpret_cast<const uint32_t *>(d + h.off_term_node);
     t.out_ptr = reinterpret_cast<const uint32_t *>(d + h.off_out_ptr);
@@ -1230,7 +1231,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     };
     auto hot_bytes = [&](uint32_t H) -> uint64_t {
         const uint32_t nt = tails_below(H);
-        return align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) + 2ull * align16(4 * ((H + 31) / 32)) +
+        return 2ull * align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) +
                16ull * nt + align16(tbytes_below(nt));
     };
     // Whole trie in shared memory when it fits; otherwise its upper levels
@@ -1267,23 +1268,21 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.off_pair = o;   o += 8192;                          // 2-gram prefix table [256][8] words
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
+    a.off_aux = o;    o += align16(4 * (H + 1));
     a.off_label = o;  o += align16(EH);
     {   // terminal tables in smem when small and they fit what is left
         const uint32_t tb = align16(4 * (uint32_t)(hh.n_terminals + 1 + hh.n_kept_terminals));
         a.off_terms = 0;
-        if (hh.n_terminals + 1 + hh.n_kept_terminals < 8192 && o + align16(4 * (H + 1)) + align16(EH) + tb +
-            2 * align16(4 * ((H + 31) / 32)) + 16 * TH + align16(TBH) <= (uint32_t)di.max_smem_optin) {
+        if (hh.n_terminals + 1 + hh.n_kept_terminals < 8192 &&
+            o + tb + 16 * TH + align16(TBH) <= (uint32_t)di.max_smem_optin) {
             a.off_terms = o;
             o += tb;
         }
     }
-    a.off_tbits = o;  o += align16(4 * ((H + 31) / 32));
-    a.off_trank = o;  o += align16(4 * ((H + 31) / 32));
     a.off_tails = o;  o += 16 * TH;
     a.off_tbytes = o; o += align16(TBH);
     a.hot_tails = TH;
     a.hot_tail_bytes = TBH;
-    a.hot_words = (H + 31) / 32;
     const size_t smem = o;
     if (smem > (size_t)di.max_smem_optin) {
         err = "pfac_match_device: internal shared-memory plan error";

@@ -25,6 +25,8 @@ def parse(image: bytes) -> dict:
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
     h["node"] = buf[h["off_node"]:h["off_node"] + 4 * (N + 1)].view(np.uint32)
+    off_aux = (h["off_node"] + 4 * (N + 1) + 255) // 256 * 256  # image.h: aux follows node
+    h["aux"] = buf[off_aux:off_aux + 4 * N].view(np.uint32)
     h["label"] = buf[h["off_label"]:h["off_label"] + E]
     h["term_node"] = buf[h["off_term_node"]:h["off_term_node"] + 4 * h["n_kept_terminals"]].view(np.uint32)
     h["out_ptr"] = buf[h["off_out_ptr"]:h["off_out_ptr"] + 4 * (T + 1)].view(np.uint32)

@@ -93,6 +93,26 @@ def test_image_layout_toy():
     outs = [h["out_pid"][h["out_ptr"][k]:h["out_ptr"][k + 1]].tolist() for k in range(4)]
     assert outs == [[0], [2], [1], [0, 3]]  # he, his, she, hers (+ its prefix he)
     assert h["filter_gram"] == 2 and h["filter_exact"] == 1
+    # aux words: labels of nodes with 1..4 children packed little-endian, the
+    # record index of tail/chain starts, 0 for leaves
+    assert [int(x) for x in h["aux"]] == [0x7368, 0x6965, 0, 1, 0x73, 0]
+
+
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_aux_words(cid):
+    """aux[v] = record rank (tail/chain start) or packed labels (1..4 children)."""
+    h = image_walker.parse(pf.Trie(gen.patterns(cid)).image())
+    node, aux, label = h["node"].astype(np.int64), h["aux"], h["label"]
+    rank = 0
+    for v in range(len(aux)):
+        e0, e1 = int(node[v]) & image_walker.MASK, int(node[v + 1]) & image_walker.MASK
+        if node[v] & image_walker.TAIL:
+            assert aux[v] == rank == image_walker.tail_index(h, v)
+            rank += 1
+        elif 1 <= e1 - e0 <= 4:
+            assert aux[v] == int.from_bytes(bytes(label[e0:e1]), "little"), v
+        else:
+            assert aux[v] == 0
 
 
 def test_image_interpreter_random_vs_oracle():
