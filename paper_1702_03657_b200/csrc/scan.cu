@@ -76,6 +76,8 @@ constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to wa
 #define PFAC_HOTCAP 0xFFFFFFFFu
 #endif
 constexpr uint32_t kHotCap = PFAC_HOTCAP;  // cap on hot-trie smem when the trie does not fit
+constexpr uint64_t kSmallTrie = 160u << 10;  // a trie this small fits shared memory whole
+constexpr uint64_t kBigL1Trie = 1u << 20;    // "big L1" plan up to this trie size (see launch_scan)
 
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
@@ -1202,7 +1204,29 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
     const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
     const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
-    const uint32_t kSlots = filter_words * 4 > 65536u ? 2u : (uint32_t)kSlotsMax;  // ring depth
+    const uint32_t *h_tbits = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_bits);
+    const uint32_t *h_trank = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_rank);
+    const uint32_t *h_tails = reinterpret_cast<const uint32_t *>(host_image + hh.off_tails);
+    auto tails_below = [&](uint32_t H) -> uint32_t {  // rank(H)
+        return h_trank[H >> 5] + (uint32_t)__builtin_popcount(h_tbits[H >> 5] & ((1u << (H & 31)) - 1u));
+    };
+    auto tbytes_below = [&](uint32_t nt) -> uint32_t {
+        return nt < hh.n_tails ? h_tails[4 * nt] : (uint32_t)hh.n_tail_bytes;
+    };
+    auto hot_bytes = [&](uint32_t H) -> uint64_t {
+        const uint32_t nt = tails_below(H);
+        return 2ull * align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) +
+               16ull * nt + align16(tbytes_below(nt));
+    };
+    // "Big L1" plan: a trie too big for shared memory but within a few L1s
+    // (kBigL1Trie) gets no hot levels, a 2-slot ring and one filter copy, so the
+    // L1/shared split leaves the largest L1 for the nodes the walks actually
+    // visit (measured with tools/placement.py: C3 -19%; a multi-MB trie (C5)
+    // is faster with its dense upper levels in shared memory instead)
+    const uint64_t whole = hot_bytes(t.n_nodes - 1);
+    const bool big_l1 = (t.kind == 1 || t.kind == 3) && whole > kSmallTrie && whole <= kBigL1Trie;
+    uint32_t kSlots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
+    if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3)) kSlots = 2;  // placement ablation only
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
                            kWarps * kDefer * 4 + 8192 +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;
@@ -1220,25 +1244,16 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // H = largest BFS prefix whose node words [0, H], labels [0, row_ptr[H]),
     // tail bitmap/rank words and tail records + bytes (tails of nodes < H)
     // all fit the budget
-    const uint32_t *h_tbits = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_bits);
-    const uint32_t *h_trank = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_rank);
-    const uint32_t *h_tails = reinterpret_cast<const uint32_t *>(host_image + hh.off_tails);
-    auto tails_below = [&](uint32_t H) -> uint32_t {  // rank(H)
-        return h_trank[H >> 5] + (uint32_t)__builtin_popcount(h_tbits[H >> 5] & ((1u << (H & 31)) - 1u));
-    };
-    auto tbytes_below = [&](uint32_t nt) -> uint32_t {
-        return nt < hh.n_tails ? h_tails[4 * nt] : (uint32_t)hh.n_tail_bytes;
-    };
-    auto hot_bytes = [&](uint32_t H) -> uint64_t {
-        const uint32_t nt = tails_below(H);
-        return 2ull * align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) +
-               16ull * nt + align16(tbytes_below(nt));
-    };
     // Whole trie in shared memory when it fits; otherwise its upper levels
     // (the BFS prefix) in all that is left (measured: more hot levels beat a
     // larger L1 for the deeper ones; kHotCap is a tuning knob, default off).
-    const uint32_t budget =
+    uint32_t budget =
         hot_bytes(t.n_nodes - 1) <= trie_budget ? trie_budget : (trie_budget < kHotCap ? trie_budget : kHotCap);
+    if (big_l1) budget = 64;  // root table and level-1 bitmaps only
+    if (const char *cap = std::getenv("PFAC_HOT_BYTES")) {  // placement ablation (tools/placement.py) only
+        const uint32_t c = (uint32_t)std::strtoul(cap, nullptr, 10);
+        if (c < budget) budget = c;
+    }
     uint32_t lo = 1, hi = t.n_nodes - 1;
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
@@ -1251,6 +1266,11 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const uint32_t left = rest - (uint32_t)hot_bytes(H);  // >= filter_words * 4 << rep0
     uint32_t rep_log2 = rep0;
     while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= (left < kFilterCap ? left : kFilterCap)) rep_log2++;
+    if (big_l1) rep_log2 = 0;
+    if (const char *r = std::getenv("PFAC_MAX_REP_LOG2")) {  // placement ablation only
+        const uint32_t m = (uint32_t)std::strtoul(r, nullptr, 10);
+        if (rep_log2 > m) rep_log2 = m;
+    }
     const uint32_t filter_bytes = filter_words * 4 << rep_log2;
 
     ScanArgs a;
@@ -1325,6 +1345,17 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
     const void *fn = kernel_for(t.kind, kSlots);
+    if (std::getenv("PFAC_L2_PERSIST")) {  // placement ablation only: the device image as an L2 persisting window
+        static std::once_flag once;
+        std::call_once(once, [&] { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 64u << 20); });
+        cudaStreamAttrValue v = {};
+        v.accessPolicyWindow.base_ptr = const_cast<uint32_t *>(t.node);
+        v.accessPolicyWindow.num_bytes = (size_t)hh.image_bytes - hh.off_node;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)geo.grid), dim3(kThreads), args, smem, stream);
     if (e != cudaSuccess) {
         {   // the kernel did not run: the barrier counter in use is unchanged
