@@ -321,16 +321,45 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
         if (force && force[0] != '3') dna = false;
     }
-    const uint32_t gram = dna ? kDnaGram : std::min<uint32_t>(4, min_len);
+    // 8-byte prefixes (kind 4) for big sets whose patterns are all >= 8 bytes:
+    // text that shares 4-byte prefixes with many patterns (tokens, protocol
+    // words) is filtered at 8 bytes
+    bool g8 = false;
+    if (!dna && min_len >= kGram8) {
+        std::vector<uint64_t> k8(m);
+        for (uint32_t k = 0; k < m; k++) {
+            uint64_t x = 0;
+            for (uint32_t b = 0; b < kGram8; b++) x |= (uint64_t)pats[k][b] << (8 * b);
+            k8[k] = x;
+        }
+        std::sort(k8.begin(), k8.end());
+        g8 = (uint64_t)(std::unique(k8.begin(), k8.end()) - k8.begin()) > 2048;
+    }
+    {
+        const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
+        if (force && force[0] != '4') g8 = false;
+    }
+    const uint32_t gram = dna ? kDnaGram : g8 ? kGram8 : std::min<uint32_t>(4, min_len);
     uint32_t exact = gram <= 2 ? 1u : 0u;
     uint32_t log2_bits;
-    uint32_t kind = dna ? 3u : gram == 4 ? 1u : 0u;
+    uint32_t kind = dna ? 3u : g8 ? 4u : gram == 4 ? 1u : 0u;
     auto dna_key = [&](const uint8_t *pt) {
         uint32_t key = 0;
         for (uint32_t b = 0; b < kDnaGram; b++) key |= dna_code(pt[b]) << (2 * b);
         return key;
     };
-    if (dna) {
+    if (g8) {
+        std::vector<uint64_t> k8(m);
+        for (uint32_t k = 0; k < m; k++) {
+            uint64_t x = 0;
+            for (uint32_t b = 0; b < kGram8; b++) x |= (uint64_t)pats[k][b] << (8 * b);
+            k8[k] = x;
+        }
+        std::sort(k8.begin(), k8.end());
+        const uint64_t distinct = std::unique(k8.begin(), k8.end()) - k8.begin();
+        log2_bits = 10;  // ~32 bits per key, at most 2^20 bits (128 KiB)
+        while (log2_bits < 20 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+    } else if (dna) {
         std::vector<uint32_t> keys(m);
         for (uint32_t k = 0; k < m; k++) keys[k] = dna_key(pats[k]);
         std::sort(keys.begin(), keys.end());
@@ -369,7 +398,15 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     for (uint32_t k = 0; k < m; k++) {
         uint32_t x = 0;
         for (uint32_t b = 0; b < gram; b++) x |= (uint32_t)pats[k][b] << (8 * b);
-        if (kind == 3) {
+        if (kind == 4) {
+            const uint32_t x0 = (uint32_t)pats[k][0] | (uint32_t)pats[k][1] << 8 | (uint32_t)pats[k][2] << 16 |
+                                (uint32_t)pats[k][3] << 24;
+            const uint32_t x1 = (uint32_t)pats[k][4] | (uint32_t)pats[k][5] << 8 | (uint32_t)pats[k][6] << 16 |
+                                (uint32_t)pats[k][7] << 24;
+            const uint32_t b = gram8_block(x0, x1, log2_bits);
+            filter[2 * b] |= 1u << (31u - (x0 & 31u));
+            filter[2 * b + 1] |= 1u << (31u - (x1 & 31u));
+        } else if (kind == 3) {
             const uint32_t key = dna_key(pats[k]);
             const uint32_t b = dna_block(key, log2_bits);
             filter[2 * b] |= 1u << dna_bit_lo(key);
@@ -476,10 +513,13 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
               h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails >= T && h.n_nodes_full >= N &&
               in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
-              in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 && (h.filter_gram <= 4 || (h.filter_kind == 3 && h.filter_gram == kDnaGram)) &&
+              in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 &&
+              (h.filter_gram <= 4 || (h.filter_kind == 3 && h.filter_gram == kDnaGram) ||
+               (h.filter_kind == 4 && h.filter_gram == kGram8)) &&
               h.filter_gram <= h.min_len && h.min_len <= h.max_len && h.max_len <= kMaxPatternLen &&
               h.filter_mul == kFilterMul && (h.filter_gram == kDnaGram ? h.filter_kind == 3
-                                          : h.filter_gram == 4 ? (h.filter_kind == 1 || h.filter_kind == 2) : h.filter_kind == 0) &&
+               : h.filter_gram == kGram8 ? h.filter_kind == 4
+               : h.filter_gram == 4 ? (h.filter_kind == 1 || h.filter_kind == 2) : h.filter_kind == 0) &&
               (h.filter_kind == 0 || h.filter_log2_bits >= 10) && in(h.off_tail_bits, 4 * ((N + 31) / 32)) &&
               in(h.off_tail_rank, 4 * ((N + 31) / 32)) && in(h.off_tails, 16 * h.n_tails) &&
               in(h.off_tail_bytes, h.n_tail_bytes) && in(h.off_level1, 40 * h.n_level1);

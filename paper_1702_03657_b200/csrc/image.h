@@ -94,7 +94,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 8;
+constexpr uint32_t kVersion = 9;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -102,6 +102,7 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kFilterMul = 0x9E3779B1u;  // Fibonacci hashing multiplier (odd)
 constexpr uint32_t kFilterMul2 = 0x85EBCA6Bu; // second multiplier (kind 3 bit index)
 constexpr uint32_t kDnaGram = 16;             // kind 3: bases per key
+constexpr uint32_t kGram8 = 8;                // kind 4: bytes per key
 
 struct ImageHeader {
     char magic[8];  // "PFACIMG1"
@@ -123,6 +124,10 @@ static_assert(sizeof(ImageHeader) == 256, "header must be 256 bytes");
 // Offset of the aux section (it follows the node section).
 PFAC_HD inline uint64_t aux_offset(uint64_t off_node, uint64_t n_nodes) {
     return (off_node + 4 * (n_nodes + 1) + 255) / 256 * 256;
+}
+// Kind 4: block of the 8-byte key (x0 = bytes 0..3, x1 = bytes 4..7).
+PFAC_HD inline uint32_t gram8_block(uint32_t x0, uint32_t x1, uint32_t log2_bits) {
+    return (x0 * kFilterMul + x1 * kFilterMul2) >> (32u - (log2_bits - 6u));
 }
 // Kind 0: filter bit index of a little-endian packed d-gram key (d < 4).
 PFAC_HD inline uint32_t filter_index(uint32_t key, uint32_t log2_bits, uint32_t exact) {

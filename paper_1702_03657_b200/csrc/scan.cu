@@ -451,6 +451,28 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
             acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);  // acc << 1 | bit
         }
         surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
+    } else if (Kind == 4) {
+        // 8-gram blocked two-bit filter: block = top bits of the 32-bit hash
+        // x(k) * M + x(k+4) * M2 of bytes k..k+7; bits 31-(byte k & 31) and
+        // 31-(byte k+4 & 31) (rotate by the bytes: amounts are mod 32)
+        uint32_t x[kPerLane + 5];
+#pragma unroll
+        for (int k = 0; k < kPerLane + 5; ++k) {
+            const int j = k >> 2;
+            const uint32_t w0 = j < kWv ? wv[j] : ext[j - kWv];
+            const uint32_t w1 = j + 1 < kWv ? wv[j + 1] : ext[j + 1 - kWv];
+            x[k] = (k & 3) ? __funnelshift_r(w0, w1, 8 * (k & 3)) : w0;
+        }
+        uint32_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int k = kPerLane - 1; k >= 0; --k) {
+            const uint32_t h = x[k] * kFilterMul + x[k + 4] * kFilterMul2;
+            const uint32_t blk = __umulhi(h, sWmul);
+            const uint2 w2 = lds64_abs(blk * stride + base_lane);
+            const uint32_t r = __funnelshift_l(w2.x, w2.x, x[k]) & __funnelshift_l(w2.y, w2.y, x[k + 4]);
+            acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);
+        }
+        surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
     } else if (Kind == 2) {
         // pair filter: one 32-bit word per start pair (k, k+1), chosen by the
         // three shared bytes k+1..k+3 (x[k+1] * (M << 8) drops byte k+4)
@@ -596,8 +618,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // and 2: word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
     // so the lanes of a phase spread over the banks
     const uint32_t rep = 1u << a.rep_log2;
-    const uint32_t unit = (Kind == 1 || Kind == 3) ? 8u : 4u;
-    const uint32_t sW = 32u - (a.t.log2_bits - ((Kind == 1 || Kind == 3) ? 6u : 5u));  // block index = hash >> sW
+    constexpr bool kBlock64 = Kind == 1 || Kind == 3 || Kind == 4;  // 64-bit two-bit blocks
+    const uint32_t unit = kBlock64 ? 8u : 4u;
+    const uint32_t sW = 32u - (a.t.log2_bits - (kBlock64 ? 6u : 5u));  // block index = hash >> sW
     const uint32_t sWmul = 1u << (32u - sW);                              // (hash * sWmul) >> 32 == hash >> sW
     const uint32_t stride = rep * unit;
     const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
@@ -698,8 +721,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
         // (8-16 loads in flight per thread: the image is cold in L2 here)
-        const uint32_t nu = ((Kind == 1 || Kind == 3) ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
-        if (Kind == 1 || Kind == 3) {
+        const uint32_t nu = (kBlock64 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
+        if (kBlock64) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
             for (uint32_t j0 = 0; j0 < nu; j0 += 8 * kThreads) {
@@ -815,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
             wv[kWv - 1] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound) : w8;
             uint32_t ext[3] = {0, 0, 0};  // kind 3: the next 12 bytes (the slot holds 16 past the round)
-            if (Kind == 3) {
+            if (Kind == 3 || Kind == 4) {
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const uint32_t e = __shfl_down_sync(0xffffffffu, wv[q + 1], 1);
@@ -1046,13 +1069,17 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 // Kernel instance for a filter kind and ring depth (2 slots only where the
 // filter can exceed 64 KiB: kinds 1 and 3).
 const void *kernel_for(uint32_t kind, uint32_t slots) {
-    if (slots == 2) return kind == 1 ? (const void *)pfac_scan_kernel<1, 2> : kind == 3 ? (const void *)pfac_scan_kernel<3, 2>
-                                                                                         : nullptr;
+    if (slots == 2)
+        return kind == 1   ? (const void *)pfac_scan_kernel<1, 2>
+               : kind == 3 ? (const void *)pfac_scan_kernel<3, 2>
+               : kind == 4 ? (const void *)pfac_scan_kernel<4, 2>
+                           : nullptr;
     switch (kind) {
         case 0: return (const void *)pfac_scan_kernel<0, 3>;
         case 1: return (const void *)pfac_scan_kernel<1, 3>;
         case 2: return (const void *)pfac_scan_kernel<2, 3>;
         case 3: return (const void *)pfac_scan_kernel<3, 3>;
+        case 4: return (const void *)pfac_scan_kernel<4, 3>;
         default: return nullptr;
     }
 }
@@ -1077,7 +1104,7 @@ int device_info(int device, DeviceInfo &out, std::string &err) {
         cudaError_t e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, device);
         if (e == cudaSuccess)
             e = cudaDeviceGetAttribute(&di.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-        for (uint32_t kind = 0; kind < 4 && e == cudaSuccess; ++kind)
+        for (uint32_t kind = 0; kind < 5 && e == cudaSuccess; ++kind)
             for (uint32_t slots = 2; slots <= 3 && e == cudaSuccess; ++slots)
                 if (const void *fn = kernel_for(kind, slots))
                     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, di.max_smem_optin);
@@ -1224,9 +1251,9 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // visit (measured with tools/placement.py: C3 -19%; a multi-MB trie (C5)
     // is faster with its dense upper levels in shared memory instead)
     const uint64_t whole = hot_bytes(t.n_nodes - 1);
-    const bool big_l1 = (t.kind == 1 || t.kind == 3) && whole > kSmallTrie && whole <= kBigL1Trie;
+    const bool big_l1 = (t.kind == 1 || t.kind == 3 || t.kind == 4) && whole > kSmallTrie && whole <= kBigL1Trie;
     uint32_t kSlots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
-    if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3)) kSlots = 2;  // placement ablation only
+    if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
                            kWarps * kDefer * 4 + 8192 +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;

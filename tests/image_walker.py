@@ -76,6 +76,12 @@ def filter_pass(h, key, start=0):
     """Does the start whose first d bytes are `key` pass the filter?  Kind 2
     (pair filter) depends on the start's parity (image.h).  Kind 3 takes the
     DNA key (dna_key of the start's 16 bytes)."""
+    if h["filter_kind"] == 4:  # key = the 8 bytes, little-endian (an int)
+        f = h["filter"]
+        x0, x1 = key & 0xFFFFFFFF, key >> 32
+        hh = (x0 * 0x9E3779B1 + x1 * 0x85EBCA6B) & 0xFFFFFFFF
+        b = hh >> (32 - (h["filter_log2_bits"] - 6))
+        return bool((int(f[2 * b]) >> (31 - (x0 & 31))) & 1) and bool((int(f[2 * b + 1]) >> (31 - (x1 & 31))) & 1)
     if h["filter_kind"] == 3:
         f = h["filter"]
         b = ((key * 0x9E3779B1) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))

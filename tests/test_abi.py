@@ -149,7 +149,7 @@ def test_filter_is_complete():
         ps = gen.patterns(cid)
         h = image_walker.parse(pf.Trie(ps).image())
         d = h["filter_gram"]
-        assert (h["filter_kind"] == 3) == (cid == 5)  # DNA k-mer filter for C5 only
+        assert h["filter_kind"] == {2: 2, 3: 4, 4: 1, 5: 3}[cid]  # pair / 8-gram / blocked / DNA k-mer filters
         for k in range(len(ps)):
             key = image_walker.dna_key(ps[k]) if h["filter_kind"] == 3 else int.from_bytes(ps[k][:d], "little")
             assert image_walker.filter_pass(h, key, 0) and image_walker.filter_pass(h, key, 1)
