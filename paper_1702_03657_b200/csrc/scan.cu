@@ -445,9 +445,10 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
             const uint32_t key = (k & 15) ? __funnelshift_r(c[k >> 4], c[(k >> 4) + 1], 2 * (k & 15)) : c[k >> 4];
             const uint32_t blk = __umulhi(key * kFilterMul, sWmul);
             const uint2 w2 = lds64_abs(blk * stride + base_lane);
-            const uint32_t h2 = __umulhi(key, kFilterMul2);
-            // rotate by key / h2 (funnel amounts are mod 32): tested bits -> 31
-            const uint32_t r = __funnelshift_l(w2.x, w2.x, key) & __funnelshift_l(w2.y, w2.y, h2);
+            const uint32_t h2 = __umulhi(key, kFilterMul2), h3 = __umulhi(key, kFilterMul3);
+            // rotate by key / h2 / h3 (funnel amounts are mod 32): tested bits -> 31
+            const uint32_t r = __funnelshift_l(w2.x, w2.x, key) & __funnelshift_l(w2.x, w2.x, h2) &
+                               __funnelshift_l(w2.y, w2.y, h3);
             acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);  // acc << 1 | bit
         }
         surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);

@@ -86,8 +86,9 @@ def filter_pass(h, key, start=0):
         f = h["filter"]
         b = ((key * 0x9E3779B1) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
         lo = 31 - (key & 31)
-        hi = 31 - (((key * 0x85EBCA6B) >> 32) & 31)
-        return bool((int(f[2 * b]) >> lo) & 1) and bool((int(f[2 * b + 1]) >> hi) & 1)
+        mid = 31 - (((key * 0x85EBCA6B) >> 32) & 31)
+        hi = 31 - (((key * 0xC2B2AE35) >> 32) & 31)
+        return bool((int(f[2 * b]) >> lo) & (int(f[2 * b]) >> mid) & (int(f[2 * b + 1]) >> hi) & 1)
     if h["filter_kind"] == 2:
         f = h["filter"]
         if start % 2 == 0:  # first of the pair: shared bytes 1..3, own byte 0
