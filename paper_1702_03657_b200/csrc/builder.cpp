@@ -426,6 +426,38 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         }
     }
 
+    // ---- exact key set (kinds 1, 3: large sets): the distinct filter keys of
+    // the patterns (kind 2 sets are small and their tries fit shared memory,
+    // where a walk is cheaper than a probe)
+    std::vector<uint32_t> kset;
+    uint32_t kset_log2 = 0, kset_empty = 0;
+    if (kind == 1 || kind == 3) {
+        std::vector<uint32_t> keys(m);
+        for (uint32_t k = 0; k < m; k++) {
+            if (kind == 3) {
+                keys[k] = dna_key(pats[k]);
+            } else {
+                keys[k] = (uint32_t)pats[k][0] | (uint32_t)pats[k][1] << 8 | (uint32_t)pats[k][2] << 16 |
+                          (uint32_t)pats[k][3] << 24;
+            }
+        }
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        for (uint32_t x : keys) {  // smallest value that is not a key
+            if (x != kset_empty) break;
+            kset_empty++;
+        }
+        kset_log2 = 6;  // load <= 1/2: a miss probes ~2.5 slots, mostly in one 128-byte line
+        while ((1ull << kset_log2) < 2ull * keys.size()) kset_log2++;
+        kset.assign((size_t)1 << kset_log2, kset_empty);
+        const uint32_t mask = (1u << kset_log2) - 1u;
+        for (uint32_t x : keys) {
+            uint32_t i = kset_slot(x, kset_log2);
+            while (kset[i] != kset_empty) i = (i + 1) & mask;
+            kset[i] = x;
+        }
+    }
+
     // ---- assemble the image
     ImageHeader h;
     std::memset(&h, 0, sizeof h);
@@ -460,6 +492,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     h.off_tails = o;     o = align256(o + 16 * NT);
     h.off_tail_bytes = o; o = align256(o + tail_bytes.size() + 16);
     h.off_level1 = o;    o = align256(o + 40ull * B);
+    h.off_kset = kset.empty() ? 0 : o;
+    o = align256(o + 4 * kset.size());
+    h.kset_log2 = kset_log2;
+    h.kset_empty = kset_empty;
     h.n_level1 = B;
     h.n_tails = NT;
     h.n_tail_bytes = tail_bytes.size();
@@ -490,6 +526,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     if (NT) std::memcpy(p + h.off_tails, tails.data(), 16 * NT);
     if (!tail_bytes.empty()) std::memcpy(p + h.off_tail_bytes, tail_bytes.data(), tail_bytes.size());
     std::memcpy(p + h.off_level1, level1.data(), 40ull * B);
+    if (!kset.empty()) std::memcpy(p + h.off_kset, kset.data(), 4 * kset.size());
     return kStatusOk;
 }
 
@@ -510,6 +547,9 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
     const uint64_t off_aux = aux_offset(h.off_node, N);  // image.h: aux follows node
     bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
               in(off_aux, 4 * N) && off_aux + 4 * N <= h.off_label &&
+              (h.off_kset == 0 ? h.kset_log2 == 0
+                               : ((h.filter_kind == 1 || h.filter_kind == 3) && h.kset_log2 >= 6 &&
+                                  h.kset_log2 <= 30 && in(h.off_kset, 4ull << h.kset_log2))) &&
               h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails >= T && h.n_nodes_full >= N &&
               in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&

@@ -86,6 +86,13 @@
 //                         hi32(key * kFilterMul2), h3 = hi32(key * kFilterMul3)
 //                         (~0.3% false positives at 2^20 bits for 50,000 keys,
 //                         ~1.1% with two bits).
+//   kset   u32[2^kset_log2]  (filter kinds 1 and 3) the exact set of the
+//                     patterns' filter keys (first 4 bytes little-endian; kind
+//                     3: the 16-base DNA key): open addressing, slot =
+//                     (key * kFilterMul) >> (32 - kset_log2), linear probing,
+//                     empty slots hold kset_empty (a value that is no key),
+//                     load <= 1/2.  A start whose key is absent cannot match:
+//                     the walk is skipped (the filter's false positives).
 #pragma once
 #include <cstdint>
 
@@ -97,7 +104,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 10;
+constexpr uint32_t kVersion = 11;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -121,10 +128,14 @@ struct ImageHeader {
     uint64_t n_tails, n_tail_bytes, off_tail_bits, off_tail_rank, off_tails, off_tail_bytes;
     uint64_t n_level1, off_level1;
     uint64_t n_kept_terminals, n_nodes_full;
-    uint8_t pad[256 - 8 - 8 - 8 - 32 - 16 - 16 - 56 - 32 - 48 - 16 - 16];
+    uint64_t off_kset;                 // exact key set (0: none), see below
+    uint32_t kset_log2, kset_empty;    // log2 of its slots; the empty-slot marker
+    uint8_t pad[512 - 256 - 16];
 };
-static_assert(sizeof(ImageHeader) == 256, "header must be 256 bytes");
+static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 
+// First slot of a key in the exact key set.
+PFAC_HD inline uint32_t kset_slot(uint32_t key, uint32_t log2) { return (key * kFilterMul) >> (32u - log2); }
 // Offset of the aux section (it follows the node section).
 PFAC_HD inline uint64_t aux_offset(uint64_t off_node, uint64_t n_nodes) {
     return (off_node + 4 * (n_nodes + 1) + 255) / 256 * 256;

@@ -117,6 +117,7 @@ struct ScanArgs {
     uint32_t hot_nodes;             // H: node words [0, H] resident
     uint32_t hot_edges;             // row_ptr[H]: labels [0, hot_edges) resident
     uint32_t aligned;               // text pointer is 16-byte aligned (bulk-copy path)
+    uint32_t use_kset;              // probe the exact key set before walks (trie not wholly in smem)
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -534,6 +535,28 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
 // streamed moments ago); hits are appended to the warp's hit list in the same
 // order and their pid counts added to their rounds' counts.  Returns the new
 // hit count.
+// Is the start's filter key in the image's exact key set (image.h)?  Kind 3:
+// the 16-base DNA key; kinds 1, 2: the first 4 bytes.
+template <int Kind>
+__device__ __forceinline__ bool kset_has(const ScanArgs &a, const GlobalText &gt) {
+    uint32_t key;
+    if (Kind == 3) {
+        key = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            key |= __umulhi((gt.at4(4 * q) & 0x06060606u) * 0x820820u, 1u << 8) << (8 * q);
+    } else {
+        key = gt.at4(0);
+    }
+    const uint32_t mask = (1u << a.t.kset_log2) - 1u;
+    for (uint32_t i = kset_slot(key, a.t.kset_log2);; i = (i + 1) & mask) {
+        const uint32_t x = __ldg(a.t.kset + i);
+        if (x == key) return true;
+        if (x == a.t.kset_empty) return false;
+    }
+}
+
+template <int Kind>
 __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem s, uint64_t cta_lo, uint64_t cta_round0,
                                                   const uint32_t *dpos, uint32_t n, uint2 *hits, uint32_t n_hits) {
     const ScanArgs &a = *ap;
@@ -546,7 +569,9 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
             p = dpos[j];
             const uint64_t gp = cta_lo + p;
             const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
-            tn = walk(a, s, gt, 0u);
+            // the exact key set rejects the filter's false positives before the walk
+            if ((Kind == 1 || Kind == 3) && a.use_kset ? kset_has<Kind>(a, gt) : true)
+                tn = walk(a, s, gt, 0u);
             if (tn != kNone)
                 atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2),
                           (unsigned long long)(s.out_ptr[tn + 1] - s.out_ptr[tn]));
@@ -893,7 +918,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #if defined(PFAC_EXP) && PFAC_EXP == 2
                 if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
-                n_hits = walk_deferred(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits);
+                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits);
 #endif
                 dcount = 0;
             }
@@ -1167,6 +1192,9 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.tails = reinterpret_cast<const uint4 *>(d + h.off_tails);
     t.tail_bytes = d + h.off_tail_bytes;
     t.level1 = reinterpret_cast<const uint32_t *>(d + h.off_level1);
+    t.kset = h.off_kset ? reinterpret_cast<const uint32_t *>(d + h.off_kset) : nullptr;
+    t.kset_log2 = h.kset_log2;
+    t.kset_empty = h.kset_empty;
     t.n_terminals = (uint32_t)h.n_terminals;
     t.n_kept_terminals = (uint32_t)h.n_kept_terminals;
     t.max_len = h.max_len;
@@ -1338,6 +1366,9 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     }
     a.n_level1 = B;
     a.hot_nodes = H;
+    // walks through a shared-memory trie are cheaper than an L2 probe of the
+    // exact key set: probe only when the trie is not wholly staged
+    a.use_kset = t.kset != nullptr && H < t.n_nodes - 1;
     a.hot_edges = EH;
     if (std::getenv("PFAC_DEBUG_PLAN")) {  // tools only
         std::fprintf(stderr,

@@ -165,7 +165,7 @@ def test_attach_roundtrip_and_validation():
     with pytest.raises(pf.PfacError):
         pf.Trie.attach(bytes(bad), device=-1)
     bad = bytearray(img)
-    bad[256 + 4 * 3] = 0xFF  # corrupt row_ptr monotonicity
+    bad[image_walker.parse(img)["off_node"] + 4 * 3] = 0xFF  # corrupt row_ptr monotonicity
     with pytest.raises(pf.PfacError):
         pf.Trie.attach(bytes(bad), device=-1)
     with pytest.raises(pf.PfacError):
