@@ -378,16 +378,24 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         std::sort(keys.begin(), keys.end());
         const uint64_t distinct = std::unique(keys.begin(), keys.end()) - keys.begin();
         // kind 2 (pair filter, d = 4): one bit per key and role, 2 bits set
-        // per 4-gram -> ~128 bits per 4-gram keeps the fill near 1.6%; used
-        // while that fits 2^18 bits.  Else kind 1 (blocked two-bit, ~32 bits
-        // per key, ~0.5% false positives) or kind 0 (d < 4, ~3%), capped at
-        // 2^20 bits (kind 1, 128 KiB) or 2^19 bits (kind 0).
+        // per 4-gram (sizing below), for sets of <= 2,048 distinct 4-grams.
+        // Else kind 1 (blocked two-bit, ~32 bits per key) or kind 0 (d < 4),
+        // capped at 2^20 bits (kind 1, 128 KiB) or 2^19 bits (kind 0).
         const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
         const bool allow2 = !force || force[0] != '1';
         if (kind == 1 && allow2 && distinct * 128 <= (1ull << 18)) {
             kind = 2;
             log2_bits = 12;
-            while ((1ull << log2_bits) < 128 * distinct) log2_bits++;
+            // 512 filter bits per distinct 4-gram (two set: fill ~0.4%), at
+            // most 2^19 bits (64 KiB, one copy).  Measured on C2 (tools/ab.py):
+            // 128 bits/key with 4 bank-spread copies 54.1 us, 256 with 2
+            // copies 51.3, 512 with 1 copy 47.6, 1024 (128 KiB: 2-slot ring,
+            // trie no longer whole in shared memory) 51.0: fewer survivors
+            // beat fewer bank conflicts.
+            uint64_t per_key = 512;
+            if (const char *e = std::getenv("PFAC_PAIR_BITS"))  // experiments only (tools/)
+                per_key = std::strtoull(e, nullptr, 10);
+            while ((1ull << log2_bits) < per_key * distinct && log2_bits < 19) log2_bits++;
         } else {
             log2_bits = 10;  // at most 2^20 bits (128 KiB; the kernel then keeps 2 text rounds per warp)
             while (log2_bits < (kind == 1 ? 20u : 19u) && (1ull << log2_bits) < 32 * distinct) log2_bits++;

@@ -1097,6 +1097,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 const void *kernel_for(uint32_t kind, uint32_t slots) {
     if (slots == 2)
         return kind == 1   ? (const void *)pfac_scan_kernel<1, 2>
+               : kind == 2 ? (const void *)pfac_scan_kernel<2, 2>
                : kind == 3 ? (const void *)pfac_scan_kernel<3, 2>
                : kind == 4 ? (const void *)pfac_scan_kernel<4, 2>
                            : nullptr;

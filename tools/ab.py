@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""A/B kernel timing: alternates processes running the working-tree library
+"""A/B kernel timing (ENVS: a library name may carry +VAR=value suffixes): alternates processes running the working-tree library
 (libpfac.so) and a reference build (libpfac_ref.so, tools/ab_build.sh) on one
 config; bench-style timing (L2 flush outside CUDA events).
 usage: python tools/ab.py [config] [rounds]"""
@@ -38,7 +38,10 @@ res = {lib: [] for lib in libs}
 for r in range(rounds):
     for lib in libs:
         name = lib
-        env = dict(os.environ, PFAC_LIB=os.path.join(HERE, "paper_1702_03657_b200", lib))
+        env = dict(os.environ, PFAC_LIB=os.path.join(HERE, "paper_1702_03657_b200", lib.split("+")[0]))
+        for kv in lib.split("+")[1:]:  # lib+VAR=value: an environment variant of a library
+            k, v = kv.split("=", 1)
+            env[k] = v
         out = subprocess.run([sys.executable, "-c", CHILD, cid, reps], env=env, capture_output=True, text=True)
         if out.returncode:
             print(out.stderr[-2000:])
