@@ -75,6 +75,8 @@ $(PKG)/libpfac_st0.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=0 -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_st4.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=4 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_st3.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=3 -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_d32.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=32 -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_hot200.so: $(CSRC) $(CHDR)
