@@ -87,3 +87,7 @@ $(PKG)/libpfac_hot8.so: $(CSRC) $(CHDR)
 # KB0 read-stream probe (bench.py reports its bandwidth next to the scan)
 tools/probe/libkb0.so: tools/probe/kb0.cu
 	$(NVCC) $(NVFLAGS) -shared -o $@ $< -lcudart
+$(PKG)/libpfac_w28.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=28 -shared -o $@ $(CSRC) -lcudart
+$(PKG)/libpfac_w30.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=30 -shared -o $@ $(CSRC) -lcudart
