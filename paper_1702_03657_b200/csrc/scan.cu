@@ -613,7 +613,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         const uint32_t nb_node = align16(4 * (a.hot_nodes + 1)), nb_label = align16(a.hot_edges),
                        nb_l1 = align16(40 * a.n_level1);
         const uint32_t nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
-        mbar_arrive_expect_tx(sbar, 1024 + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb);
+        const uint32_t nb_f = a.rep_log2 == 0 ? align16(4 * a.filter_words) : 0u;  // one copy: a bulk copy too
+        mbar_arrive_expect_tx(sbar, 1024 + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb + nb_f);
+        if (nb_f) bulk_g2s(s_filter, a.t.filter, nb_f, sbar, pl);
         bulk_g2s(s_root, a.t.root, 1024, sbar, pl);
         bulk_g2s(s_node, a.t.node, nb_node, sbar, pl);
         bulk_g2s(smem + a.off_aux, a.t.aux, nb_node, sbar, pl);  // aux words [0, H] (same size)
@@ -748,7 +750,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     {   // replicate the filter: destination unit j holds source unit j >> rep_log2
         // (consecutive threads write consecutive units: no bank conflicts)
         // (8-16 loads in flight per thread: the image is cold in L2 here)
-        const uint32_t nu = (kBlock64 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
+        const uint32_t nu = a.rep_log2 == 0 ? 0u : (kBlock64 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
         if (kBlock64) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
