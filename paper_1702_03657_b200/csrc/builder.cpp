@@ -500,6 +500,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     h.off_tails = o;     o = align256(o + 16 * NT);
     h.off_tail_bytes = o; o = align256(o + tail_bytes.size() + 16);
     h.off_level1 = o;    o = align256(o + 40ull * B);
+    h.off_pair = o;      o = align256(o + 8192);
     h.off_kset = kset.empty() ? 0 : o;
     o = align256(o + 4 * kset.size());
     h.kset_log2 = kset_log2;
@@ -534,6 +535,16 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     if (NT) std::memcpy(p + h.off_tails, tails.data(), 16 * NT);
     if (!tail_bytes.empty()) std::memcpy(p + h.off_tail_bytes, tail_bytes.data(), tail_bytes.size());
     std::memcpy(p + h.off_level1, level1.data(), 40ull * B);
+    {   // 2-gram prefix table (image.h)
+        uint32_t *pair = reinterpret_cast<uint32_t *>(p + h.off_pair);
+        for (uint32_t j = 0; j < 2048; j++) {
+            const uint32_t v = root[j >> 3];
+            uint32_t wd = 0;
+            if (v != 0)
+                wd = (node_word[v] & (kTermBit | kTailBit)) ? 0xFFFFFFFFu : level1[(size_t)(v - 1) * 10 + (j & 7)];
+            pair[j] = wd;
+        }
+    }
     if (!kset.empty()) std::memcpy(p + h.off_kset, kset.data(), 4 * kset.size());
     return kStatusOk;
 }
@@ -554,7 +565,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
     auto in = [&](uint64_t off, uint64_t bytes) { return off >= sizeof(ImageHeader) && off + bytes <= size; };
     const uint64_t off_aux = aux_offset(h.off_node, N);  // image.h: aux follows node
     bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
-              in(off_aux, 4 * N) && off_aux + 4 * N <= h.off_label &&
+              in(off_aux, 4 * N) && off_aux + 4 * N <= h.off_label && in(h.off_pair, 8192) &&
               (h.off_kset == 0 ? h.kset_log2 == 0
                                : ((h.filter_kind == 1 || h.filter_kind == 3) && h.kset_log2 >= 6 &&
                                   h.kset_log2 <= 30 && in(h.off_kset, 4ull << h.kset_log2))) &&

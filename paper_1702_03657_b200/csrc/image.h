@@ -86,6 +86,11 @@
 //                         hi32(key * kFilterMul2), h3 = hi32(key * kFilterMul3)
 //                         (~0.3% false positives at 2^20 bits for 50,000 keys,
 //                         ~1.1% with two bits).
+//   pair   u32[256][8]  the 2-gram prefix table: word (b0, q) bit j set iff
+//                     the walk from a start with bytes (b0, 32q + j) gets past
+//                     level 1, or b0's level-1 node already is a terminal or a
+//                     tail/chain start (then every b1 is set).  Derived from
+//                     root + level1; the kernel tests survivors with it.
 //   kset   u32[2^kset_log2]  (filter kinds 1 and 3) the exact set of the
 //                     patterns' filter keys (first 4 bytes little-endian; kind
 //                     3: the 16-base DNA key): open addressing, slot =
@@ -104,7 +109,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 11;
+constexpr uint32_t kVersion = 12;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -130,7 +135,8 @@ struct ImageHeader {
     uint64_t n_kept_terminals, n_nodes_full;
     uint64_t off_kset;                 // exact key set (0: none), see below
     uint32_t kset_log2, kset_empty;    // log2 of its slots; the empty-slot marker
-    uint8_t pad[512 - 256 - 16];
+    uint64_t off_pair;                 // 2-gram prefix table u32[256][8]
+    uint8_t pad[512 - 256 - 24];
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 

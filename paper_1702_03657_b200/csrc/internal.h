@@ -43,6 +43,7 @@ struct DevTrie {
     const uint4 *tails;
     const uint8_t *tail_bytes;
     const uint32_t *level1;
+    const uint32_t *pair;  // 2-gram prefix table [256][8]
     const uint32_t *kset;  // exact key set (nullptr: none)
     uint32_t kset_log2, kset_empty;
     uint32_t n_terminals;

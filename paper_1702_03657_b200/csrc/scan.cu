@@ -614,7 +614,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                        nb_l1 = align16(40 * a.n_level1);
         const uint32_t nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
         const uint32_t nb_f = a.rep_log2 == 0 ? align16(4 * a.filter_words) : 0u;  // one copy: a bulk copy too
-        mbar_arrive_expect_tx(sbar, 1024 + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb + nb_f);
+        mbar_arrive_expect_tx(sbar, 1024 + 8192 + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb + nb_f);
+        bulk_g2s(smem + a.off_pair, a.t.pair, 8192, sbar, pl);
         if (nb_f) bulk_g2s(s_filter, a.t.filter, nb_f, sbar, pl);
         bulk_g2s(s_root, a.t.root, 1024, sbar, pl);
         bulk_g2s(s_node, a.t.node, nb_node, sbar, pl);
@@ -805,14 +806,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // 2-gram prefix table: word (b0, q) bit j <=> the walk from a start with
     // bytes (b0, 32q + j) gets past level 1 (or b0's node already is a
     // terminal / tail start, where every b1 is kept)
-    uint32_t *s_pair = reinterpret_cast<uint32_t *>(smem + a.off_pair);
-    for (uint32_t j = tid; j < 2048; j += kThreads) {
-        const uint32_t v = s_root[j >> 3];
-        uint32_t wd = 0;
-        if (v != 0) wd = (node_word(a, s, v) & (kTermBit | kTailBit)) ? 0xFFFFFFFFu : s_bm[(v - 1) * 10 + (j & 7)];
-        s_pair[j] = wd;
-    }
-    __syncthreads();
+    const uint32_t *s_pair = reinterpret_cast<const uint32_t *>(smem + a.off_pair);  // (arrived with the tables)
     STAMP(1);
 
     // ================================================= phase 1: scan
@@ -1196,6 +1190,7 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.tails = reinterpret_cast<const uint4 *>(d + h.off_tails);
     t.tail_bytes = d + h.off_tail_bytes;
     t.level1 = reinterpret_cast<const uint32_t *>(d + h.off_level1);
+    t.pair = reinterpret_cast<const uint32_t *>(d + h.off_pair);
     t.kset = h.off_kset ? reinterpret_cast<const uint32_t *>(d + h.off_kset) : nullptr;
     t.kset_log2 = h.kset_log2;
     t.kset_empty = h.kset_empty;

@@ -10,7 +10,7 @@ TERM = 0x80000000
 TAIL = 0x40000000
 MASK = 0x3FFFFFFF
 
-_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II")
+_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q")
 
 
 def parse(image: bytes) -> dict:
@@ -20,7 +20,7 @@ def parse(image: bytes) -> dict:
             "filter_kind", "off_node", "off_label", "off_term_node", "off_out_ptr", "off_out_pid", "off_root",
             "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core",
             "n_tails", "n_tail_bytes", "off_tail_bits", "off_tail_rank", "off_tails", "off_tail_bytes",
-            "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full", "off_kset", "kset_log2", "kset_empty"]
+            "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full", "off_kset", "kset_log2", "kset_empty", "off_pair"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
@@ -40,6 +40,7 @@ def parse(image: bytes) -> dict:
     h["tails"] = buf[h["off_tails"]:h["off_tails"] + 16 * h["n_tails"]].view(np.uint32).reshape(-1, 4)
     h["tail_bytes"] = buf[h["off_tail_bytes"]:h["off_tail_bytes"] + h["n_tail_bytes"]]
     h["level1"] = buf[h["off_level1"]:h["off_level1"] + 40 * h["n_level1"]].view(np.uint32).reshape(-1, 10)
+    h["pair"] = buf[h["off_pair"]:h["off_pair"] + 8192].view(np.uint32).reshape(256, 8)
     if h["off_kset"]:
         h["kset"] = buf[h["off_kset"]:h["off_kset"] + (4 << h["kset_log2"])].view(np.uint32)
     return h

@@ -98,6 +98,19 @@ def test_image_layout_toy():
     assert [int(x) for x in h["aux"]] == [0x7368, 0x6965, 0, 1, 0x73, 0]
 
 
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_pair_table(cid):
+    """2-gram prefix table = bit (b0, b1) set iff a pattern path continues
+    with b1 after b0, or b0 alone reaches a terminal / tail / chain start."""
+    h = image_walker.parse(pf.Trie(gen.patterns(cid)).image())
+    node, root, l1 = h["node"], h["root"], h["level1"]
+    for b0 in range(256):
+        v = int(root[b0])
+        want = [0] * 8 if v == 0 else ([0xFFFFFFFF] * 8 if int(node[v]) & (image_walker.TERM | image_walker.TAIL)
+                                       else [int(x) for x in l1[v - 1][:8]])
+        assert [int(x) for x in h["pair"][b0]] == want, b0
+
+
 @pytest.mark.parametrize("cid", [2, 3, 4, 5])
 def test_aux_words(cid):
     """aux[v] = record rank (tail/chain start) or packed labels (1..4 children)."""
