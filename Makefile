@@ -91,3 +91,10 @@ $(PKG)/libpfac_w28.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=28 -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_w30.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=30 -shared -o $@ $(CSRC) -lcudart
+
+# latency / launch-overhead probes (tools/probe; measurement only)
+probes: tools/probe/lat_probe tools/probe/launch_probe
+tools/probe/lat_probe: tools/probe/lat_probe.cu
+	$(NVCC) -O2 $(ARCH) -o $@ $<
+tools/probe/launch_probe: tools/probe/launch_probe.cu
+	$(NVCC) -O2 $(ARCH) -o $@ $<
