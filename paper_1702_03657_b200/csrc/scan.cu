@@ -119,6 +119,7 @@ struct ScanArgs {
     uint32_t aligned;               // text pointer is 16-byte aligned (bulk-copy path)
     uint32_t use_kset;              // probe the exact key set before walks (trie not wholly in smem)
     uint32_t static_quarters;       // share of a CTA's rounds assigned statically, in quarters
+    uint32_t contig;                // warps own contiguous round blocks: output order = (CTA, warp, position)
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -559,7 +560,8 @@ __device__ __forceinline__ bool kset_has(const ScanArgs &a, const GlobalText &gt
 
 template <int Kind>
 __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem s, uint64_t cta_lo, uint64_t cta_round0,
-                                                  const uint32_t *dpos, uint32_t n, uint2 *hits, uint32_t n_hits) {
+                                                  const uint32_t *dpos, uint32_t n, uint2 *hits, uint32_t n_hits,
+                                                  unsigned long long &rows) {
     const ScanArgs &a = *ap;
     const int lane = threadIdx.x & 31;
     __syncwarp();
@@ -573,9 +575,11 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
             // the exact key set rejects the filter's false positives before the walk
             if ((Kind == 1 || Kind == 3) && a.use_kset ? kset_has<Kind>(a, gt) : true)
                 tn = walk(a, s, gt, 0u);
-            if (tn != kNone)
-                atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2),
-                          (unsigned long long)(s.out_ptr[tn + 1] - s.out_ptr[tn]));
+            if (tn != kNone) {
+                const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
+                if (a.contig) rows += cnt;  // the lane's rows (contiguous mode: per-warp totals)
+                else atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2), (unsigned long long)cnt);
+            }
         }
         const bool hit = tn != kNone;
         const uint32_t hb = __ballot_sync(0xffffffffu, hit);
@@ -683,8 +687,16 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     const uint32_t n_static = max((uint32_t)(kSlots - 1), (n_local * a.static_quarters / 4) / kWarps);  // the first
                                                                        // kSlots-1 takes never touch the counter
     uint32_t taken = 0;
+    // contiguous mode: warp w owns rounds [wbeg, wend) (balanced split)
+    const uint32_t wq = n_local / kWarps, wrem = n_local % kWarps;
+    const uint32_t wbeg = warp * wq + min((uint32_t)warp, wrem), wend = wbeg + wq + ((uint32_t)warp < wrem ? 1u : 0u);
     auto take = [&]() -> uint32_t {
         uint32_t r;
+        if (a.contig) {
+            r = wbeg + taken < wend ? wbeg + taken : n_local;
+            ++taken;
+            return r;
+        }
         if (taken < n_static) {
             r = warp + kWarps * taken;
         } else {
@@ -788,7 +800,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         }
     }
     STAMP(8);
-    for (uint32_t r = tid; r < n_local; r += kThreads) a.round_val[cta_round0 + r] = 0ull;  // pid counts
+    if (!a.contig)
+        for (uint32_t r = tid; r < n_local; r += kThreads) a.round_val[cta_round0 + r] = 0ull;  // pid counts
     __syncthreads();  // the round counter and counts are initialised
     STAMP(9);
     // the first kSlots-1 rounds of this warp (static ones) start streaming
@@ -820,6 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // two, else a warp scan) and walked in full-warp batches to their first
     // mismatch whenever the queue may not take another 32.
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
+    unsigned long long lane_rows = 0;  // contiguous mode: rows of this lane's hits
     uint32_t dcount = 0;  // queued starts (warp-uniform)
     uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * kDefer;
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
@@ -915,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #if defined(PFAC_EXP) && PFAC_EXP == 2
                 if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
-                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits);
+                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits, lane_rows);
 #endif
                 dcount = 0;
             }
@@ -947,8 +961,31 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // round's first row relative to the CTA), CTA total -> grid barrier ->
     // prefix over the CTA totals.
     __syncthreads();  // every round of the CTA is done (round_val complete)
-    unsigned long long run = 0;
-    for (uint32_t b = 0; b < n_local; b += kThreads) {
+    unsigned long long run = 0, warp_base = 0;
+    if (a.contig) {  // per-warp totals: the CTA's rows are the warps' rows in warp order
+        unsigned long long wt = lane_rows;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, d);
+        if (lane == 0) s_wtot[warp] = wt;
+        __syncthreads();
+        if (warp == 0) {
+            const unsigned long long wv0 = lane < kWarps ? s_wtot[lane] : 0ull;
+            unsigned long long wi = wv0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, d);
+                if (lane >= d) wi += y;
+            }
+            if (lane < kWarps) s_wtot[lane] = wi - wv0;
+            __syncwarp();
+            if (lane == 31) s_wtot[kWarps] = wi;
+        }
+        __syncthreads();
+        warp_base = s_wtot[warp];
+        run = s_wtot[kWarps];
+        __syncthreads();
+    }
+    for (uint32_t b = 0; !a.contig && b < n_local; b += kThreads) {
         const uint32_t r = b + tid;
         const unsigned long long v = r < n_local ? a.round_val[cta_round0 + r] : 0ull;
         unsigned long long incl = v;
@@ -1001,7 +1038,33 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     STAMP(3);
 
     // ================================================= phase 3: emit
-    if (n_hits <= a.hit_cap) {
+    if (a.contig && n_hits <= a.hit_cap) {
+        // the warp's hits are in position order and its rows follow the
+        // CTA's earlier warps' rows
+        uint64_t run_rows = cta_off + warp_base;
+        for (uint32_t b = 0; b < n_hits; b += 32) {
+            const uint32_t i = b + lane;
+            uint32_t ti = 0, cnt = 0, p = 0;
+            if (i < n_hits) {
+                const uint2 h = hits[i];
+                p = h.x;
+                ti = h.y;
+                cnt = s.out_ptr[ti + 1] - s.out_ptr[ti];
+            }
+            uint32_t ctot;
+            uint64_t o = run_rows + warp_excl_scan(cnt, lane, &ctot);
+            if (cnt) {
+                const uint32_t r0 = s.out_ptr[ti];
+                for (uint32_t e = 0; e < cnt; ++e, ++o) {
+                    if (o < a.capacity) {
+                        a.out_pos[o] = a.pos_base + cta_lo + p;
+                        a.out_pid[o] = __ldg(a.t.out_pid + r0 + e);
+                    }
+                }
+            }
+            run_rows += ctot;
+        }
+    } else if (!a.contig && n_hits <= a.hit_cap) {
         // hits are in position order; a round's hits are consecutive, so a
         // row's index = its round's first row + rows of the round's earlier hits
         uint64_t carry_run = 0, carry_seg = 0;  // warp-running rows before the batch / before its first round
@@ -1041,11 +1104,14 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     } else {
         // hit list overflowed: scan this warp's rounds again (text from global
         // memory), writing rows directly in position order
-        for (uint32_t r = 0; r < n_local; ++r) {
-            const uint32_t owner = r < kWarps * n_static ? blockIdx.x * kWarps + r % kWarps
-                                                         : __ldcg(a.round_owner + cta_round0 + r);
-            if (owner != gw) continue;
-            uint64_t off = cta_off + a.round_val[cta_round0 + r];
+        uint64_t contig_off = cta_off + warp_base;  // contiguous mode: the warp's running row
+        for (uint32_t r = a.contig ? wbeg : 0; r < (a.contig ? wend : n_local); ++r) {
+            if (!a.contig) {
+                const uint32_t owner = r < kWarps * n_static ? blockIdx.x * kWarps + r % kWarps
+                                                             : __ldcg(a.round_owner + cta_round0 + r);
+                if (owner != gw) continue;
+            }
+            uint64_t off = a.contig ? contig_off : cta_off + a.round_val[cta_round0 + r];
             const uint64_t lbase = cta_lo + (uint64_t)r * kRound + (uint64_t)lane * kPerLane;
             uint32_t wv[kWv], ext[3];
 #pragma unroll
@@ -1084,6 +1150,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     }
                 }
             }
+            contig_off += ctot;
         }
     }
     STAMP(4);
@@ -1372,6 +1439,9 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // rounds static; else the last quarter is handed out dynamically
     // (measured: C2 -1% static; C3 -11% dynamic)
     a.static_quarters = PFAC_STATIC_NUM >= 0 ? (uint32_t)PFAC_STATIC_NUM : (H >= t.n_nodes - 1 ? 4u : 3u);
+    // all-static: contiguous blocks per warp (per-warp totals replace the
+    // per-round counts: no round zeroing, atomics or round scan)
+    a.contig = a.static_quarters == 4 && !std::getenv("PFAC_NO_CONTIG");
     a.hot_edges = EH;
     if (std::getenv("PFAC_DEBUG_PLAN")) {  // tools only
         std::fprintf(stderr,
