@@ -537,6 +537,34 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
 // streamed moments ago); hits are appended to the warp's hit list in the same
 // order and their pid counts added to their rounds' counts.  Returns the new
 // hit count.
+// The filter key of the start at slot offset off (the slot holds 16 bytes
+// past the round, so the 16 DNA bytes are always in it): kind 3 the 16-base
+// DNA key, else the first 4 bytes.
+template <int Kind>
+__device__ __forceinline__ uint32_t slot_key(const uint8_t *slot, uint32_t off) {
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(slot + (off & ~3u));
+    const uint32_t sh = 8 * (off & 3);
+    if (Kind == 3) {
+        uint32_t key = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t x = __funnelshift_r(w[q], w[q + 1], sh);
+            key |= __umulhi((x & 0x06060606u) * 0x820820u, 1u << 8) << (8 * q);
+        }
+        return key;
+    }
+    return __funnelshift_r(w[0], w[1], sh);
+}
+// Probe the exact key set for a key.
+__device__ __forceinline__ bool kset_probe(const ScanArgs &a, uint32_t key) {
+    const uint32_t mask = (1u << a.t.kset_log2) - 1u;
+    for (uint32_t i = kset_slot(key, a.t.kset_log2);; i = (i + 1) & mask) {
+        const uint32_t x = __ldg(a.t.kset + i);
+        if (x == key) return true;
+        if (x == a.t.kset_empty) return false;
+    }
+}
+
 // Is the start's filter key in the image's exact key set (image.h)?  Kind 3:
 // the 16-base DNA key; kinds 1, 2: the first 4 bytes.
 template <int Kind>
@@ -560,8 +588,8 @@ __device__ __forceinline__ bool kset_has(const ScanArgs &a, const GlobalText &gt
 
 template <int Kind>
 __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem s, uint64_t cta_lo, uint64_t cta_round0,
-                                                  const uint32_t *dpos, uint32_t n, uint2 *hits, uint32_t n_hits,
-                                                  unsigned long long &rows) {
+                                                  const uint32_t *dpos, const uint32_t *dkey, uint32_t n, uint2 *hits,
+                                                  uint32_t n_hits, unsigned long long &rows) {
     const ScanArgs &a = *ap;
     const int lane = threadIdx.x & 31;
     __syncwarp();
@@ -573,7 +601,10 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
             const uint64_t gp = cta_lo + p;
             const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
             // the exact key set rejects the filter's false positives before the walk
-            if ((Kind == 1 || Kind == 3) && a.use_kset ? kset_has<Kind>(a, gt) : true)
+            // (kind 1: the key was taken from the ring when queued; kind 3 reads
+            // it from the text: most of its probes hit and the walk follows)
+            if (Kind == 1 && a.use_kset ? kset_probe(a, dkey[j])
+                                        : (Kind == 3 && a.use_kset ? kset_has<Kind>(a, gt) : true))
                 tn = walk(a, s, gt, 0u);
             if (tn != kNone) {
                 const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
@@ -836,6 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     unsigned long long lane_rows = 0;  // contiguous mode: rows of this lane's hits
     uint32_t dcount = 0;  // queued starts (warp-uniform)
     uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * kDefer;
+    uint32_t *dkey = reinterpret_cast<uint32_t *>(smem + a.off_defer) + (kWarps + warp) * kDefer;  // kind 1
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
     for (;;) {
         const bool done = rid[0] >= n_local;
@@ -929,19 +961,26 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #if defined(PFAC_EXP) && PFAC_EXP == 2
                 if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
-                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, dpos, dcount, hits, n_hits, lane_rows);
+                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, dpos, dkey, dcount, hits, n_hits, lane_rows);
 #endif
                 dcount = 0;
             }
             if (cb >= tot) break;
             if (single) {  // append by ballot (the queue has room for 32)
                 const uint32_t kb = __ballot_sync(0xffffffffu, pending != 0);
-                if (pending) dpos[dcount + __popc(kb & ((1u << lane) - 1u))] = rel + lane * kPerLane + (__ffs(pending) - 1);
+                if (pending) {
+                    const uint32_t e = dcount + __popc(kb & ((1u << lane) - 1u));
+                    const uint32_t off = lane * kPerLane + (__ffs(pending) - 1);
+                    dpos[e] = rel + off;
+                    if (Kind == 1 && a.use_kset) dkey[e] = slot_key<Kind>(p0, off);
+                }
                 dcount += __popc(kb);
                 break;
             }
             while (pending && r < cb + 32) {  // the next 32 in position order (the queue has room for 32)
-                dpos[dcount + r - cb] = rel + lane * kPerLane + (__ffs(pending) - 1);
+                const uint32_t off = lane * kPerLane + (__ffs(pending) - 1);
+                dpos[dcount + r - cb] = rel + off;
+                if (Kind == 1 && a.use_kset) dkey[dcount + r - cb] = slot_key<Kind>(p0, off);
                 pending &= pending - 1;
                 ++r;
             }
@@ -1350,7 +1389,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     uint32_t kSlots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
     if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
-                           kWarps * kDefer * 4 + 8192 +
+                           kWarps * kDefer * (t.kind == 1 ? 8 : 4) + 8192 +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
@@ -1406,7 +1445,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 1] + the CTA's round counter
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
-    a.off_defer = o;  o += kWarps * kDefer * 4;  // per warp: queue u32[kDefer]
+    a.off_defer = o;  o += kWarps * kDefer * (t.kind == 1 ? 8 : 4);  // queue u32[kDefer] (+ kind-1 keys)
     a.off_pair = o;   o += 8192;                          // 2-gram prefix table [256][8] words
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
