@@ -957,7 +957,19 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         }
         // ---- queue the kept starts, 32 per pass; the single batch-walk site at its top
         for (uint32_t cb = 0;; cb += 32) {
-            if (dcount != 0 && (done || dcount > (uint32_t)(kDefer - 32))) {
+            // kinds 1 and 3 (large sets: walks and key-set probes cost L2 round
+            // trips) flush only when this pass would not fit, for fuller
+            // batches (C4/C5 -2%); kind 2 flushes once fewer than 32 slots are
+            // left (C2: +1% the other way)
+            bool flush_now;
+            if (Kind == 1 || Kind == 3) {
+                const uint32_t kb0 = single ? __ballot_sync(0xffffffffu, pending != 0) : 0u;
+                const uint32_t need = cb >= tot ? 0u : (single ? __popc(kb0) : min(32u, tot - cb));
+                flush_now = dcount != 0 && (done || dcount + need > (uint32_t)kDefer);
+            } else {
+                flush_now = dcount != 0 && (done || dcount > (uint32_t)(kDefer - 32));
+            }
+            if (flush_now) {
 #if defined(PFAC_EXP) && PFAC_EXP == 2
                 if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
