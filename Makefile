@@ -98,3 +98,5 @@ tools/probe/lat_probe: tools/probe/lat_probe.cu
 	$(NVCC) -O2 $(ARCH) -o $@ $<
 tools/probe/launch_probe: tools/probe/launch_probe.cu
 	$(NVCC) -O2 $(ARCH) -o $@ $<
+$(PKG)/libpfac_d96.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=96 -shared -o $@ $(CSRC) -lcudart

@@ -71,7 +71,7 @@ constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated f
 #ifndef PFAC_DEFER
 #define PFAC_DEFER 48
 #endif
-constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to walk
+constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to walk (kinds 1, 2; see defer_for)
 #ifndef PFAC_HOTCAP
 #define PFAC_HOTCAP 0xFFFFFFFFu
 #endif
@@ -120,6 +120,7 @@ struct ScanArgs {
     uint32_t use_kset;              // probe the exact key set before walks (trie not wholly in smem)
     uint32_t static_quarters;       // share of a CTA's rounds assigned statically, in quarters
     uint32_t contig;                // warps own contiguous round blocks: output order = (CTA, warp, position)
+    uint32_t defer;                 // walk-queue capacity per warp (>= 33)
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -866,8 +867,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
     unsigned long long lane_rows = 0;  // contiguous mode: rows of this lane's hits
     uint32_t dcount = 0;  // queued starts (warp-uniform)
-    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * kDefer;
-    uint32_t *dkey = reinterpret_cast<uint32_t *>(smem + a.off_defer) + (kWarps + warp) * kDefer;  // kind 1
+    const uint32_t qcap = (Kind == 1 || Kind == 2) ? (uint32_t)kDefer : a.defer;  // queue capacity (per plan)
+    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * qcap;
+    uint32_t *dkey = reinterpret_cast<uint32_t *>(smem + a.off_defer) + (kWarps + warp) * qcap;  // kind 1
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
     for (;;) {
         const bool done = rid[0] >= n_local;
@@ -965,9 +967,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             if (Kind == 1 || Kind == 3) {
                 const uint32_t kb0 = single ? __ballot_sync(0xffffffffu, pending != 0) : 0u;
                 const uint32_t need = cb >= tot ? 0u : (single ? __popc(kb0) : min(32u, tot - cb));
-                flush_now = dcount != 0 && (done || dcount + need > (uint32_t)kDefer);
+                flush_now = dcount != 0 && (done || dcount + need > qcap);
             } else {
-                flush_now = dcount != 0 && (done || dcount > (uint32_t)(kDefer - 32));
+                flush_now = dcount != 0 && (done || dcount > qcap - 32);
             }
             if (flush_now) {
 #if defined(PFAC_EXP) && PFAC_EXP == 2
@@ -1398,10 +1400,13 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // is faster with its dense upper levels in shared memory instead)
     const uint64_t whole = hot_bytes(t.n_nodes - 1);
     const bool big_l1 = (t.kind == 1 || t.kind == 3 || t.kind == 4) && whole > kSmallTrie && whole <= kBigL1Trie;
+    // walk-queue capacity: deeper for DNA (kind 3) and 8-byte-prefix (kind 4)
+    // sets, whose walks are long (measured: C5 64 -4%, C3 96 -2.5%)
+    const uint32_t defer = t.kind == 3 ? 64u : t.kind == 4 ? 96u : (uint32_t)kDefer;  // (kernel: kDefer for kinds 1, 2)
     uint32_t kSlots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
     if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
-                           kWarps * kDefer * (t.kind == 1 ? 8 : 4) + 8192 +
+                           kWarps * defer * (t.kind == 1 ? 8 : 4) + 8192 +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
@@ -1457,7 +1462,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 1] + the CTA's round counter
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
-    a.off_defer = o;  o += kWarps * kDefer * (t.kind == 1 ? 8 : 4);  // queue u32[kDefer] (+ kind-1 keys)
+    a.off_defer = o;  o += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
+    a.defer = defer;
     a.off_pair = o;   o += 8192;                          // 2-gram prefix table [256][8] words
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
