@@ -357,8 +357,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         }
         std::sort(k8.begin(), k8.end());
         const uint64_t distinct = std::unique(k8.begin(), k8.end()) - k8.begin();
-        log2_bits = 10;  // ~32 bits per key, at most 2^20 bits (128 KiB)
-        while (log2_bits < 20 && (1ull << log2_bits) < 32 * distinct) log2_bits++;
+        uint64_t per_key = 32;  // ~32 bits per key, at most 2^20 bits (128 KiB)
+        if (const char *e = std::getenv("PFAC_G8_BITS")) per_key = std::strtoull(e, nullptr, 10);  // experiments
+        log2_bits = 10;
+        while (log2_bits < 20 && (1ull << log2_bits) < per_key * distinct) log2_bits++;
     } else if (dna) {
         std::vector<uint32_t> keys(m);
         for (uint32_t k = 0; k < m; k++) keys[k] = dna_key(pats[k]);

@@ -121,6 +121,7 @@ struct ScanArgs {
     uint32_t static_quarters;       // share of a CTA's rounds assigned statically, in quarters
     uint32_t contig;                // warps own contiguous round blocks: output order = (CTA, warp, position)
     uint32_t defer;                 // walk-queue capacity per warp (>= 33)
+    uint32_t use_pair;              // the 2-gram prefix table is staged and tested
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -650,8 +651,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                        nb_l1 = align16(40 * a.n_level1);
         const uint32_t nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
         const uint32_t nb_f = a.rep_log2 == 0 ? align16(4 * a.filter_words) : 0u;  // one copy: a bulk copy too
-        mbar_arrive_expect_tx(sbar, 1024 + 8192 + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb + nb_f);
-        bulk_g2s(smem + a.off_pair, a.t.pair, 8192, sbar, pl);
+        const uint32_t nb_pair = a.use_pair ? 8192u : 0u;
+        mbar_arrive_expect_tx(sbar, 1024 + nb_pair + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb + nb_f);
+        if (nb_pair) bulk_g2s(smem + a.off_pair, a.t.pair, nb_pair, sbar, pl);
         if (nb_f) bulk_g2s(s_filter, a.t.filter, nb_f, sbar, pl);
         bulk_g2s(s_root, a.t.root, 1024, sbar, pl);
         bulk_g2s(s_node, a.t.node, nb_node, sbar, pl);
@@ -929,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #endif
             // ---- stage 2 in the lane: 2-gram prefix test of each survivor;
             // `pending` becomes the kept set (sparse: appended by ballot)
-            if (Kind != 3) {
+            if (Kind != 3 && (Kind != 4 || a.use_pair)) {
                 const uint32_t rl = rid[0] < n_fast ? (uint32_t)kSlotBytes  // readable bytes from rbase
                                                     : (a.readable > rbase ? clamp32(a.readable - rbase) : 0u);
                 uint32_t km = 0;
@@ -1403,10 +1405,13 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // walk-queue capacity: deeper for DNA (kind 3) and 8-byte-prefix (kind 4)
     // sets, whose walks are long (measured: C5 64 -4%, C3 96 -2.5%)
     const uint32_t defer = t.kind == 3 ? 64u : t.kind == 4 ? 96u : (uint32_t)kDefer;  // (kernel: kDefer for kinds 1, 2)
+    // the 2-gram test (and its 8 KiB table): not for DNA (every 2-gram begins a
+    // pattern); optional for 8-byte prefixes (tuning knob)
+    const bool use_pair = t.kind != 3 && !(t.kind == 4 && std::getenv("PFAC_K4_NOPAIR"));
     uint32_t kSlots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
     if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
-                           kWarps * defer * (t.kind == 1 ? 8 : 4) + 8192 +
+                           kWarps * defer * (t.kind == 1 ? 8 : 4) + (use_pair ? 8192 : 0) +
                            align16(40 * B) + 8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
@@ -1427,7 +1432,10 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // larger L1 for the deeper ones; kHotCap is a tuning knob, default off).
     uint32_t budget =
         hot_bytes(t.n_nodes - 1) <= trie_budget ? trie_budget : (trie_budget < kHotCap ? trie_budget : kHotCap);
-    if (big_l1) budget = 64;  // root table and level-1 bitmaps only
+    if (big_l1) {  // root table and level-1 bitmaps only (+ a tuning knob)
+        budget = 64;
+        if (const char *h = std::getenv("PFAC_BIGL1_HOT")) budget = (uint32_t)std::strtoul(h, nullptr, 10);
+    }
     if (const char *cap = std::getenv("PFAC_HOT_BYTES")) {  // placement ablation (tools/placement.py) only
         const uint32_t c = (uint32_t)std::strtoul(cap, nullptr, 10);
         if (c < budget) budget = c;
@@ -1464,7 +1472,8 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.off_root = o;   o += 1024;
     a.off_defer = o;  o += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
     a.defer = defer;
-    a.off_pair = o;   o += 8192;                          // 2-gram prefix table [256][8] words
+    a.off_pair = o;   o += use_pair ? 8192 : 0;           // 2-gram prefix table [256][8] words
+    a.use_pair = use_pair;
     a.off_bm = o;     o += align16(40 * B);
     a.off_node = o;   o += align16(4 * (H + 1));
     a.off_aux = o;    o += align16(4 * (H + 1));
