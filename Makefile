@@ -44,16 +44,6 @@ clean:
 
 .PHONY: all clean
 
-# layout variants for A/B timing (tools/variants.sh)
-VARLIBS := $(PKG)/libpfac_v_s0.so $(PKG)/libpfac_v_e0.so $(PKG)/libpfac_v_s0e0.so
-$(PKG)/libpfac_v_s0.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_STATIC_NUM=0 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_v_e0.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_SLOT_EXTRA=0 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_v_s0e0.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_STATIC_NUM=0 -DPFAC_SLOT_EXTRA=0 -shared -o $@ $(CSRC) -lcudart
-variants: $(VARLIBS)
-
 # A/B variants of the production build (tools/ab.py)
 ABLIBS := $(PKG)/libpfac_nosw.so $(PKG)/libpfac_d64.so $(PKG)/libpfac_w24.so $(PKG)/libpfac_w16.so
 $(PKG)/libpfac_nosw.so: $(CSRC) $(CHDR)
@@ -69,14 +59,6 @@ $(PKG)/libpfac_s2l.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_s2l_nosw.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -DPFAC_NO_SWIZZLE -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_st2.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=2 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_st0.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=0 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_st4.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=4 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_st3.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_STATIC_NUM=3 -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_d32.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=32 -shared -o $@ $(CSRC) -lcudart
 $(PKG)/libpfac_hot200.so: $(CSRC) $(CHDR)

@@ -16,8 +16,8 @@
 //    first H nodes are the hot upper levels; PAPER.md:89 kept row_ptr on chip
 //    for the same reason).
 //  * phase 1 (scan): CTA b owns a contiguous range of 1024-start rounds; its
-//    warps take them statically interleaved, the last quarter from a shared
-//    counter.  A per-warp ring of kSlots slots (1 KiB + 16-byte overhang) is
+//    warps own contiguous blocks of the range's first part and take the rest
+//    (the last quarter, or a plan's share) from a shared counter.  A per-warp ring of kSlots slots (1 KiB + 16-byte overhang) is
 //    filled by TMA bulk copies (cp.async.bulk + mbarrier, evict-first in L2)
 //    kSlots-1 rounds ahead.  Per round each lane tests its 32 consecutive
 //    starts against the filter (a clear bit means no pattern can start there:
@@ -26,8 +26,9 @@
 //    nodes); the few kept are queued in position order and walked in
 //    full-warp batches to the first mismatch.  A start that passed a terminal
 //    is appended, in position order, to the warp's hit list (offset, terminal
-//    index), its pid count to the round's count.
-//  * phase 2 (offsets): CTA exclusive scan of the round counts -> one grid
+//    index), its pid count to the lane's rows (block) or the round's count.
+//  * phase 2 (offsets): CTA exclusive scan of the warp totals and the dynamic
+//    rounds' counts -> one grid
 //    barrier -> exclusive prefix over CTA totals.  Ranges are contiguous and
 //    ordered, so the concatenation is globally sorted by (pos, pid).
 //  * phase 3 (emit): each warp expands its hit list into (pos, pid) rows (a
@@ -60,9 +61,6 @@ constexpr int kSlotsMax = 3;           // text ring depth per warp (kSlots-1 rou
                                        // takes more than 64 KiB of shared memory
 #ifndef PFAC_SLOT_EXTRA
 #define PFAC_SLOT_EXTRA 16
-#endif
-#ifndef PFAC_STATIC_NUM
-#define PFAC_STATIC_NUM (-1)  // share of a CTA's rounds assigned statically, in quarters (-1: per plan)
 #endif
 constexpr int kSlotBytes = kRound + PFAC_SLOT_EXTRA;  // one round of text (+ the next 16 bytes: the last windows)
 static_assert(kSlotsMax >= 2, "ring");
@@ -118,8 +116,8 @@ struct ScanArgs {
     uint32_t hot_edges;             // row_ptr[H]: labels [0, hot_edges) resident
     uint32_t aligned;               // text pointer is 16-byte aligned (bulk-copy path)
     uint32_t use_kset;              // probe the exact key set before walks (trie not wholly in smem)
-    uint32_t static_quarters;       // share of a CTA's rounds assigned statically, in quarters
-    uint32_t contig;                // warps own contiguous round blocks: output order = (CTA, warp, position)
+    uint32_t ctg64;                 // share of a CTA's rounds in contiguous per-warp blocks, in 64ths
+                                    // (the rest, the range's end, is handed out dynamically)
     uint32_t defer;                 // walk-queue capacity per warp (>= 33)
     uint32_t use_pair;              // the 2-gram prefix table is staged and tested
 };
@@ -590,8 +588,8 @@ __device__ __forceinline__ bool kset_has(const ScanArgs &a, const GlobalText &gt
 
 template <int Kind>
 __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem s, uint64_t cta_lo, uint64_t cta_round0,
-                                                  const uint32_t *dpos, const uint32_t *dkey, uint32_t n, uint2 *hits,
-                                                  uint32_t n_hits, unsigned long long &rows) {
+                                                  uint32_t ctg_bytes, const uint32_t *dpos, const uint32_t *dkey,
+                                                  uint32_t n, uint2 *hits, uint32_t n_hits, unsigned long long &rows) {
     const ScanArgs &a = *ap;
     const int lane = threadIdx.x & 31;
     __syncwarp();
@@ -610,8 +608,8 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
                 tn = walk(a, s, gt, 0u);
             if (tn != kNone) {
                 const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
-                if (a.contig) rows += cnt;  // the lane's rows (contiguous mode: per-warp totals)
-                else atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2), (unsigned long long)cnt);
+                if (p < ctg_bytes) rows += cnt;  // the lane's rows in its warp's block (per-warp totals)
+                else atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2), (unsigned long long)cnt);  // dynamic round
             }
         }
         const bool hit = tn != kNone;
@@ -698,9 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     const uint32_t gram = a.t.gram;
     const uint64_t lim = (a.readable + 1 >= gram && a.readable + 1 - gram < a.n_starts) ? a.readable + 1 - gram
                                                                                         : a.n_starts;
-    // ---- this CTA's contiguous range of rounds; its warps take rounds from
-    // a shared counter (dynamic within the CTA: warps whose walks run long
-    // take fewer rounds), in increasing order per warp
+    // ---- this CTA's contiguous range of rounds
     const uint32_t gw = blockIdx.x * kWarps + warp;
     const uint64_t n_rounds = (a.n_starts + kRound - 1) / kRound;
     const uint64_t cta_round0 = (uint64_t)blockIdx.x * a.rounds_per_cta < n_rounds
@@ -714,35 +710,29 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     const uint32_t n_fast = !a.aligned || a.readable < cta_lo + kSlotBytes
                                 ? 0u
                                 : (uint32_t)min((uint64_t)n_local, (a.readable - cta_lo - kSlotBytes) / kRound + 1);
-    // The warp's j-th round: rounds warp + 32j while j < n_static (static,
-    // interleaved), then from the CTA's shared counter (dynamic: warps whose
-    // walks ran long take fewer of the last rounds).  Increasing per warp;
-    // warp-uniform; >= n_local when none is left.
-    const uint32_t n_static = max((uint32_t)(kSlots - 1), (n_local * a.static_quarters / 4) / kWarps);  // the first
-                                                                       // kSlots-1 takes never touch the counter
+    // The CTA's first n_ctg rounds are split into contiguous per-warp blocks
+    // (warp w owns [wbeg, wend); its rows follow the CTA's earlier warps'
+    // rows, so per-warp totals order them); the rest are handed out from the
+    // CTA's shared counter (dynamic: warps whose walks ran long take fewer;
+    // those rounds keep per-round counts and record their owner).  The warp's
+    // rounds increase; warp-uniform; >= n_local when none is left.
+    const uint32_t n_ctg = (uint32_t)(((uint64_t)n_local * a.ctg64) >> 6);
     uint32_t taken = 0;
-    // contiguous mode: warp w owns rounds [wbeg, wend) (balanced split)
-    const uint32_t wq = n_local / kWarps, wrem = n_local % kWarps;
+    const uint32_t wq = n_ctg / kWarps, wrem = n_ctg % kWarps;
     const uint32_t wbeg = warp * wq + min((uint32_t)warp, wrem), wend = wbeg + wq + ((uint32_t)warp < wrem ? 1u : 0u);
     auto take = [&]() -> uint32_t {
         uint32_t r;
-        if (a.contig) {
-            r = wbeg + taken < wend ? wbeg + taken : n_local;
-            ++taken;
-            return r;
-        }
-        if (taken < n_static) {
-            r = warp + kWarps * taken;
+        if (wbeg + taken < wend) {
+            r = wbeg + taken;
         } else {
             r = 0;
             if (lane == 0) {
                 asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(s_next)) : "memory");
             }
-            r = kWarps * n_static + __shfl_sync(0xffffffffu, r, 0);
+            r = n_ctg + __shfl_sync(0xffffffffu, r, 0);
+            // the owner of a dynamic round is recorded (phase 3's re-scan fallback)
+            if (lane == 0 && r < n_local) a.round_owner[cta_round0 + r] = gw;
         }
-        // the owner of a dynamic round is recorded (phase 3's re-scan
-        // fallback); a static round r < kWarps * n_static belongs to warp r % kWarps
-        if (taken >= n_static && lane == 0 && r < n_local) a.round_owner[cta_round0 + r] = gw;
         ++taken;
         return r;
     };
@@ -834,8 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         }
     }
     STAMP(8);
-    if (!a.contig)
-        for (uint32_t r = tid; r < n_local; r += kThreads) a.round_val[cta_round0 + r] = 0ull;  // pid counts
+    for (uint32_t r = n_ctg + tid; r < n_local; r += kThreads) a.round_val[cta_round0 + r] = 0ull;  // pid counts
     __syncthreads();  // the round counter and counts are initialised
     STAMP(9);
     // the first kSlots-1 rounds of this warp (static ones) start streaming
@@ -867,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // two, else a warp scan) and walked in full-warp batches to their first
     // mismatch whenever the queue may not take another 32.
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
-    unsigned long long lane_rows = 0;  // contiguous mode: rows of this lane's hits
+    unsigned long long lane_rows = 0;  // rows of this lane's hits in the warp's block
     uint32_t dcount = 0;  // queued starts (warp-uniform)
     const uint32_t qcap = (Kind == 1 || Kind == 2) ? (uint32_t)kDefer : a.defer;  // queue capacity (per plan)
     uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * qcap;
@@ -977,7 +966,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #if defined(PFAC_EXP) && PFAC_EXP == 2
                 if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
-                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, dpos, dkey, dcount, hits, n_hits, lane_rows);
+                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey, dcount, hits, n_hits,
+                                             lane_rows);
 #endif
                 dcount = 0;
             }
@@ -1012,12 +1002,13 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     STAMP(2);
 
     // ================================================= phase 2: offsets
-    // Exclusive scan of the CTA's round counts in place (round_val becomes the
-    // round's first row relative to the CTA), CTA total -> grid barrier ->
-    // prefix over the CTA totals.
+    // Exclusive scan of the warps' block totals (a warp's first row relative
+    // to the CTA) and of the dynamic rounds' counts after them, in place
+    // (round_val becomes the round's first row relative to the CTA), CTA
+    // total -> grid barrier -> prefix over the CTA totals.
     __syncthreads();  // every round of the CTA is done (round_val complete)
     unsigned long long run = 0, warp_base = 0;
-    if (a.contig) {  // per-warp totals: the CTA's rows are the warps' rows in warp order
+    {   // per-warp totals: the rows of the CTA's blocks are the warps' rows in warp order
         unsigned long long wt = lane_rows;
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) wt += __shfl_xor_sync(0xffffffffu, wt, d);
@@ -1040,7 +1031,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         run = s_wtot[kWarps];
         __syncthreads();
     }
-    for (uint32_t b = 0; !a.contig && b < n_local; b += kThreads) {
+    for (uint32_t b = n_ctg; b < n_local; b += kThreads) {  // the dynamic rounds follow the blocks
         const uint32_t r = b + tid;
         const unsigned long long v = r < n_local ? a.round_val[cta_round0 + r] : 0ull;
         unsigned long long incl = v;
@@ -1093,9 +1084,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     STAMP(3);
 
     // ================================================= phase 3: emit
-    if (a.contig && n_hits <= a.hit_cap) {
-        // the warp's hits are in position order and its rows follow the
-        // CTA's earlier warps' rows
+    if (n_ctg == n_local && n_hits <= a.hit_cap) {
+        // blocks only: the warp's hits are in position order and its rows
+        // follow the CTA's earlier warps' rows
         uint64_t run_rows = cta_off + warp_base;
         for (uint32_t b = 0; b < n_hits; b += 32) {
             const uint32_t i = b + lane;
@@ -1119,11 +1110,16 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             }
             run_rows += ctot;
         }
-    } else if (!a.contig && n_hits <= a.hit_cap) {
-        // hits are in position order; a round's hits are consecutive, so a
-        // row's index = its round's first row + rows of the round's earlier hits
-        uint64_t carry_run = 0, carry_seg = 0;  // warp-running rows before the batch / before its first round
+    } else if (n_hits <= a.hit_cap) {
+        // the warp's hits are in position order: first those of its block
+        // (rows from the warp's base on), then those of its dynamic rounds; a
+        // round's hits are consecutive, so a row's index = its segment's first
+        // row + rows of the segment's earlier hits (segment = the block, or one
+        // dynamic round)
+        constexpr uint32_t kBlockSeg = 0xFFFFFFF0u;
+        uint64_t carry_run = 0, carry_seg = 0;  // warp-running rows before the batch / before its first segment
         uint32_t carry_round = 0xFFFFFFFFu;
+        const uint32_t ctg_bytes = n_ctg * kRound;
         for (uint32_t b = 0; b < n_hits; b += 32) {
             const uint32_t i = b + lane;
             uint32_t ti = 0, cnt = 0, rnd = 0xFFFFFFFEu, p = 0;
@@ -1131,7 +1127,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 const uint2 h = hits[i];
                 p = h.x;
                 ti = h.y;
-                rnd = p >> kRoundLog2;
+                rnd = p < ctg_bytes ? kBlockSeg : p >> kRoundLog2;
                 cnt = s.out_ptr[ti + 1] - s.out_ptr[ti];
             }
             uint32_t ctot;
@@ -1143,7 +1139,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             const uint64_t seg_h = __shfl_sync(0xffffffffu, ex, hl < 0 ? 0 : hl);
             const uint64_t seg = hl < 0 ? carry_seg : seg_h;
             if (cnt) {
-                uint64_t o = cta_off + a.round_val[cta_round0 + rnd] + (ex - seg);
+                uint64_t o = cta_off + (rnd == kBlockSeg ? warp_base : a.round_val[cta_round0 + rnd]) + (ex - seg);
                 const uint32_t r0 = s.out_ptr[ti];
                 for (uint32_t e = 0; e < cnt; ++e, ++o) {
                     if (o < a.capacity) {
@@ -1159,14 +1155,11 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     } else {
         // hit list overflowed: scan this warp's rounds again (text from global
         // memory), writing rows directly in position order
-        uint64_t contig_off = cta_off + warp_base;  // contiguous mode: the warp's running row
-        for (uint32_t r = a.contig ? wbeg : 0; r < (a.contig ? wend : n_local); ++r) {
-            if (!a.contig) {
-                const uint32_t owner = r < kWarps * n_static ? blockIdx.x * kWarps + r % kWarps
-                                                             : __ldcg(a.round_owner + cta_round0 + r);
-                if (owner != gw) continue;
-            }
-            uint64_t off = a.contig ? contig_off : cta_off + a.round_val[cta_round0 + r];
+        uint64_t contig_off = cta_off + warp_base;  // the warp's running row in its block
+        for (uint32_t r = wbeg < wend ? wbeg : n_ctg; r < n_local; r = r + 1 == wend ? n_ctg : r + 1) {
+            const bool dyn = r >= n_ctg;  // the block's rounds, then the dynamic rounds the warp took
+            if (dyn && __ldcg(a.round_owner + cta_round0 + r) != gw) continue;
+            uint64_t off = dyn ? cta_off + a.round_val[cta_round0 + r] : contig_off;
             const uint64_t lbase = cta_lo + (uint64_t)r * kRound + (uint64_t)lane * kPerLane;
             uint32_t wv[kWv], ext[3];
 #pragma unroll
@@ -1502,12 +1495,12 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // exact key set: probe only when the trie is not wholly staged
     a.use_kset = t.kset != nullptr && H < t.n_nodes - 1;
     // walks through a wholly staged trie are short and even: (almost) all
-    // rounds static; else the last quarter is handed out dynamically
-    // (measured: C2 -1% static; C3 -11% dynamic)
-    a.static_quarters = PFAC_STATIC_NUM >= 0 ? (uint32_t)PFAC_STATIC_NUM : (H >= t.n_nodes - 1 ? 4u : 3u);
-    // all-static: contiguous blocks per warp (per-warp totals replace the
-    // per-round counts: no round zeroing, atomics or round scan)
-    a.contig = a.static_quarters == 4 && !std::getenv("PFAC_NO_CONTIG");
+    // rounds in per-warp blocks; else the last quarter is handed out
+    // dynamically (measured: C3 -11% dynamic)
+    {
+        const char *e = std::getenv("PFAC_CTG64");  // tools only
+        a.ctg64 = e ? (uint32_t)std::min(64l, std::max(0l, std::atol(e))) : (H >= t.n_nodes - 1 ? 64u : 48u);
+    }
     a.hot_edges = EH;
     if (std::getenv("PFAC_DEBUG_PLAN")) {  // tools only
         std::fprintf(stderr,
