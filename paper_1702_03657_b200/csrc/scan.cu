@@ -80,11 +80,15 @@ constexpr uint64_t kBigL1Trie = 1u << 20;    // "big L1" plan up to this trie si
 // Workspace: header (two grid-barrier counters, used alternately so that a
 // launch clears the other one for the next launch) + CTA totals + hit lists.
 struct WsHeader {
-    unsigned int barrier[2];
-    unsigned int pad[62];
+    unsigned int barrier[2];    // grid barrier after phase 1 (alternating per launch)
+    unsigned int barrier2[2];   // grid barrier after the pool scan
+    unsigned int pool_next[2];  // next pool round
+    unsigned int pad[58];
 };
 static_assert(sizeof(WsHeader) == 256, "");
-constexpr uint64_t kWsFixed = sizeof(WsHeader) + 8ull * kMaxCtas;
+// fixed part: header | cta_total[kMaxCtas] u64 | pool_total[kMaxCtas] u64
+constexpr uint64_t kWsFixed = sizeof(WsHeader) + 16ull * kMaxCtas;
+constexpr uint32_t kNoRound = 0xFFFFFFFFu;  // take(): no round left
 
 struct ScanArgs {
     DevTrie t;
@@ -101,7 +105,10 @@ struct ScanArgs {
     uint2 *hits;                    // [warps][hit_cap] (start offset within the warp's range, terminal index)
     uint32_t hit_cap;
     uint32_t parity;                // barrier counter used by this launch
-    uint64_t rounds_per_cta;
+    uint64_t rounds_per_cta;        // of the first n_main rounds (the CTA ranges)
+    uint64_t n_main;                // rounds in CTA ranges; rounds [n_main, n_rounds) are the shared pool
+    uint32_t pool_seg;              // pool rounds per CTA in the pool's scan (0: no pool)
+    unsigned long long *pool_total; // [grid] row totals of the pool segments
     unsigned long long *round_val;  // [n_rounds] pid count of the round, then its first row within the CTA
     uint32_t *round_owner;          // [n_rounds] global warp that scanned the round
     // shared-memory layout (bytes from the dynamic smem base; filter at 0)
@@ -634,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint8_t *s_label = smem + a.off_label;
     uint8_t *ring = smem + a.off_ring + (uint32_t)warp * (kSlots * kSlotBytes);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.off_bar) + warp * kSlots;
-    unsigned long long *s_wtot = reinterpret_cast<unsigned long long *>(smem + a.off_warp);  // [kWarps + 1]
+    unsigned long long *s_wtot = reinterpret_cast<unsigned long long *>(smem + a.off_warp);  // [kWarps + 2]
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
 
     STAMP(0);
@@ -662,10 +669,14 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, pl);
     }
     if (lane < kSlots) mbar_init(&bars[lane], 1);
-    uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 1);  // round counter of the CTA
+    uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 2);  // round counter of the CTA
     if (tid == 32) *s_next = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (blockIdx.x == 0 && tid == 0) a.ws->barrier[a.parity ^ 1u] = 0u;  // for the next launch
+    if (blockIdx.x == 0 && tid == 0) {  // for the next launch
+        a.ws->barrier[a.parity ^ 1u] = 0u;
+        a.ws->barrier2[a.parity ^ 1u] = 0u;
+        a.ws->pool_next[a.parity ^ 1u] = 0u;
+    }
     __syncthreads();  // barriers initialised
     STAMP(11);
     Smem s;
@@ -699,10 +710,14 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // ---- this CTA's contiguous range of rounds
     const uint32_t gw = blockIdx.x * kWarps + warp;
     const uint64_t n_rounds = (a.n_starts + kRound - 1) / kRound;
-    const uint64_t cta_round0 = (uint64_t)blockIdx.x * a.rounds_per_cta < n_rounds
-                                    ? (uint64_t)blockIdx.x * a.rounds_per_cta : n_rounds;
-    const uint32_t n_local = (uint32_t)((cta_round0 + a.rounds_per_cta < n_rounds ? cta_round0 + a.rounds_per_cta
-                                                                                    : n_rounds) - cta_round0);
+    const uint64_t cta_round0 = (uint64_t)blockIdx.x * a.rounds_per_cta < a.n_main
+                                    ? (uint64_t)blockIdx.x * a.rounds_per_cta : a.n_main;
+    const uint32_t n_local = (uint32_t)((cta_round0 + a.rounds_per_cta < a.n_main ? cta_round0 + a.rounds_per_cta
+                                                                                  : a.n_main) - cta_round0);
+    // the shared pool (the text's last rounds, taken by any warp once its
+    // CTA's range is done: cross-CTA balance) in the CTA's local round
+    // numbering: [pool_lo, pool_hi) (start offsets stay 32-bit: planned so)
+    const uint32_t pool_lo = (uint32_t)(a.n_main - cta_round0), pool_hi = (uint32_t)(n_rounds - cta_round0);
     const uint64_t cta_lo = cta_round0 * kRound;
     uint2 *hits = a.hits + (uint64_t)gw * a.hit_cap;
 
@@ -715,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // rows, so per-warp totals order them); the rest are handed out from the
     // CTA's shared counter (dynamic: warps whose walks ran long take fewer;
     // those rounds keep per-round counts and record their owner).  The warp's
-    // rounds increase; warp-uniform; >= n_local when none is left.
+    // rounds increase; warp-uniform; kNoRound when none is left.
     const uint32_t n_ctg = (uint32_t)(((uint64_t)n_local * a.ctg64) >> 6);
     uint32_t taken = 0;
     const uint32_t wq = n_ctg / kWarps, wrem = n_ctg % kWarps;
@@ -730,8 +745,22 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(s_next)) : "memory");
             }
             r = n_ctg + __shfl_sync(0xffffffffu, r, 0);
+            if (r >= n_local) {  // the CTA's range is done: a pool round, if any is left
+                r = kNoRound;
+                if (a.pool_seg) {
+                    if (lane == 0) {
+                        const uint32_t q = atomicAdd(&a.ws->pool_next[a.parity], 1u);
+                        if (q < pool_hi - pool_lo) {
+                            r = pool_lo + q;
+                            a.round_val[cta_round0 + r] = 0ull;  // its count (ordered before the warp's
+                                                                 // walks by their __syncwarp)
+                        }
+                    }
+                    r = __shfl_sync(0xffffffffu, r, 0);
+                }
+            }
             // the owner of a dynamic round is recorded (phase 3's re-scan fallback)
-            if (lane == 0 && r < n_local) a.round_owner[cta_round0 + r] = gw;
+            if (lane == 0 && r != kNoRound) a.round_owner[cta_round0 + r] = gw;
         }
         ++taken;
         return r;
@@ -833,7 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #pragma unroll
     for (int q = 0; q < kSlots - 1; ++q) {
         rid[q] = take();
-        if (rid[q] < n_local) issue(rid[q], q);
+        if (rid[q] != kNoRound) issue(rid[q], q);
     }
     STAMP(10);
     mbar_wait(sbar, 0);
@@ -863,7 +892,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t *dkey = reinterpret_cast<uint32_t *>(smem + a.off_defer) + (kWarps + warp) * qcap;  // kind 1
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
     for (;;) {
-        const bool done = rid[0] >= n_local;
+        const bool done = rid[0] == kNoRound;
         const uint32_t rel = rid[0] * (uint32_t)kRound;  // round start relative to cta_lo
         const uint64_t rbase = cta_lo + rel;
         const uint8_t *p0 = ring + slot * kSlotBytes;
@@ -873,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             // refill the slot of the previous round with the next round taken
             __syncwarp();  // every lane's reads of that slot precede its refill
             rid[kSlots - 1] = take();
-            if (rid[kSlots - 1] < n_local) issue(rid[kSlots - 1], slot == 0 ? kSlots - 1 : slot - 1);
+            if (rid[kSlots - 1] != kNoRound) issue(rid[kSlots - 1], slot == 0 ? kSlots - 1 : slot - 1);
             mbar_wait(&bars[slot], phase);
 #ifdef PFAC_TIMING
             if (taken == kSlots) STAMP(6);  // the first round's text is in
@@ -1031,9 +1060,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         run = s_wtot[kWarps];
         __syncthreads();
     }
-    for (uint32_t b = n_ctg; b < n_local; b += kThreads) {  // the dynamic rounds follow the blocks
-        const uint32_t r = b + tid;
-        const unsigned long long v = r < n_local ? a.round_val[cta_round0 + r] : 0ull;
+    // block-wide exclusive scan of one value per thread (kThreads values)
+    auto block_excl = [&](unsigned long long v, unsigned long long &total) -> unsigned long long {
         unsigned long long incl = v;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -1055,10 +1083,24 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             if (lane == 31) s_wtot[kWarps] = wi;
         }
         __syncthreads();
-        if (r < n_local) a.round_val[cta_round0 + r] = run + s_wtot[warp] + incl - v;
-        run += s_wtot[kWarps];
+        const unsigned long long ex = s_wtot[warp] + incl - v;
+        total = s_wtot[kWarps];
         __syncthreads();
-    }
+        return ex;
+    };
+    // in place: counts of rounds [g0, g0 + n) -> run0 + their exclusive prefix; returns the end
+    auto scan_rounds = [&](uint64_t g0, uint32_t n, unsigned long long run0) -> unsigned long long {
+        for (uint32_t b = 0; b < n; b += kThreads) {
+            const uint32_t r = b + tid;
+            unsigned long long tot;
+            const unsigned long long v = r < n ? a.round_val[g0 + r] : 0ull;
+            const unsigned long long ex = block_excl(v, tot);
+            if (r < n) a.round_val[g0 + r] = run0 + ex;
+            run0 += tot;
+        }
+        return run0;
+    };
+    run = scan_rounds(cta_round0 + n_ctg, n_local - n_ctg, run);  // the dynamic rounds follow the blocks
     if (tid == 0) a.cta_total[blockIdx.x] = run;
     STAMP(7);
     grid_barrier(&a.ws->barrier[a.parity]);
@@ -1076,15 +1118,35 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         }
         if (lane == 0) {
             s_wtot[kWarps] = pre;
-            if (blockIdx.x == 0) *a.out_count = all;
+            s_wtot[kWarps + 1] = all;
+            if (blockIdx.x == 0 && !a.pool_seg) *a.out_count = all;
         }
     }
     __syncthreads();
     const uint64_t cta_off = s_wtot[kWarps];  // this CTA's first output row
+    // The pool's rows follow every range's: its counts are complete only now.
+    // CTA b scans pool segment b in place, a second grid barrier, then every
+    // CTA holds each segment's first row (s_pool, in the idle ring).
+    unsigned long long *s_pool = reinterpret_cast<unsigned long long *>(smem + a.off_ring);
+    if (a.pool_seg) {
+        const unsigned long long all_main = s_wtot[kWarps + 1];
+        __syncthreads();
+        const uint64_t g0 = a.n_main + (uint64_t)blockIdx.x * a.pool_seg;
+        const uint32_t n = g0 < n_rounds ? (uint32_t)min((uint64_t)a.pool_seg, n_rounds - g0) : 0u;
+        const unsigned long long seg_total = scan_rounds(g0, n, 0ull);
+        if (tid == 0) a.pool_total[blockIdx.x] = seg_total;
+        grid_barrier(&a.ws->barrier2[a.parity]);
+        unsigned long long pool_all;
+        const unsigned long long v = (uint32_t)tid < gridDim.x ? __ldcg(a.pool_total + tid) : 0ull;
+        const unsigned long long ex = block_excl(v, pool_all);
+        if ((uint32_t)tid < gridDim.x) s_pool[tid] = all_main + ex;
+        if (blockIdx.x == 0 && tid == 0) *a.out_count = all_main + pool_all;
+        __syncthreads();
+    }
     STAMP(3);
 
     // ================================================= phase 3: emit
-    if (n_ctg == n_local && n_hits <= a.hit_cap) {
+    if (n_ctg == n_local && !a.pool_seg && n_hits <= a.hit_cap) {
         // blocks only: the warp's hits are in position order and its rows
         // follow the CTA's earlier warps' rows
         uint64_t run_rows = cta_off + warp_base;
@@ -1139,7 +1201,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             const uint64_t seg_h = __shfl_sync(0xffffffffu, ex, hl < 0 ? 0 : hl);
             const uint64_t seg = hl < 0 ? carry_seg : seg_h;
             if (cnt) {
-                uint64_t o = cta_off + (rnd == kBlockSeg ? warp_base : a.round_val[cta_round0 + rnd]) + (ex - seg);
+                uint64_t o = (rnd == kBlockSeg ? cta_off + warp_base
+                                               : (rnd >= pool_lo ? s_pool[(rnd - pool_lo) / a.pool_seg] : cta_off) +
+                                                     a.round_val[cta_round0 + rnd]) +
+                             (ex - seg);
                 const uint32_t r0 = s.out_ptr[ti];
                 for (uint32_t e = 0; e < cnt; ++e, ++o) {
                     if (o < a.capacity) {
@@ -1156,10 +1221,19 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         // hit list overflowed: scan this warp's rounds again (text from global
         // memory), writing rows directly in position order
         uint64_t contig_off = cta_off + warp_base;  // the warp's running row in its block
-        for (uint32_t r = wbeg < wend ? wbeg : n_ctg; r < n_local; r = r + 1 == wend ? n_ctg : r + 1) {
-            const bool dyn = r >= n_ctg;  // the block's rounds, then the dynamic rounds the warp took
+        // the block's rounds, then the CTA's dynamic rounds and the pool's the warp took
+        auto next_round = [&](uint32_t r) -> uint32_t {
+            if (r == wend) r = n_ctg;
+            if (r == n_local && a.pool_seg) r = pool_lo;
+            return r;
+        };
+        const uint32_t r_end = a.pool_seg ? pool_hi : n_local;
+        for (uint32_t r = next_round(wbeg); r < r_end; r = next_round(r + 1)) {
+            const bool dyn = r >= n_ctg;
             if (dyn && __ldcg(a.round_owner + cta_round0 + r) != gw) continue;
-            uint64_t off = dyn ? cta_off + a.round_val[cta_round0 + r] : contig_off;
+            uint64_t off = dyn ? (r >= pool_lo ? s_pool[(r - pool_lo) / a.pool_seg] : cta_off) +
+                                     a.round_val[cta_round0 + r]
+                               : contig_off;
             const uint64_t lbase = cta_lo + (uint64_t)r * kRound + (uint64_t)lane * kPerLane;
             uint32_t wv[kWv], ext[3];
 #pragma unroll
@@ -1405,7 +1479,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
                            kWarps * defer * (t.kind == 1 ? 8 : 4) + (use_pair ? 8192 : 0) +
-                           align16(40 * B) + 8 * (kWarps + 2) + 512;
+                           align16(40 * B) + 8 * (kWarps + 3) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
         return kStatusLimit;
@@ -1460,7 +1534,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     o = align_up(o, 128);
     a.off_ring = o;   o += kWarps * kSlots * kSlotBytes;
     a.off_bar = o;    o += (kWarps * kSlots + 1) * 8;
-    a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 1] + the CTA's round counter
+    a.off_warp = o;   o += 8 * (kWarps + 3);  // warp totals [kWarps + 2] + the CTA's round counter
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
     a.off_defer = o;  o += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
@@ -1527,12 +1601,25 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.out_count = d_count;
     a.ws = reinterpret_cast<WsHeader *>(d_ws);
     a.cta_total = reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(d_ws) + sizeof(WsHeader));
+    a.pool_total = a.cta_total + kMaxCtas;
     a.round_val = reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(d_ws) + kWsFixed);
     a.round_owner = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_ws) + geo.off_owner);
     a.hits = reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(d_ws) + geo.off_hits);
     a.hit_cap = geo.hit_cap;
     a.parity = parity;
-    a.rounds_per_cta = geo.rounds_per_cta;
+    // the shared pool: the text's last rounds, taken by any warp whose CTA's
+    // range is done (cross-CTA balance where walks leave the SM: content
+    // skew between ranges, e.g. C5's first ranges hold twice the matches);
+    // planned when start offsets from a CTA's first round stay 32-bit
+    {
+        const char *e = std::getenv("PFAC_POOL64");  // tools only: pool share in 64ths
+        const uint64_t pool64 = e ? (uint64_t)std::min(32l, std::max(0l, std::atol(e))) : (a.ctg64 < 64 ? 4u : 0u);
+        const uint64_t n_pool = geo.n_rounds * pool64 / 64;
+        const bool pool = n_pool >= geo.grid && geo.n_rounds * (uint64_t)kRound < (1ull << 32);
+        a.n_main = pool ? geo.n_rounds - n_pool : geo.n_rounds;
+        a.rounds_per_cta = pool ? (a.n_main + geo.grid - 1) / geo.grid : geo.rounds_per_cta;
+        a.pool_seg = pool ? (uint32_t)((n_pool + geo.grid - 1) / geo.grid) : 0u;
+    }
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
     const void *fn = kernel_for(t.kind, kSlots);

@@ -1,0 +1,6 @@
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
+timeout 900 python tools/ab.py 5 3 libpfac_ref.so libpfac.so libpfac.so+PFAC_POOL64=8 libpfac.so+PFAC_POOL64=2 > gpurun_out/ab_c5.log 2>&1; cat gpurun_out/ab_c5.log
+timeout 900 python tools/ab.py 3 3 libpfac_ref.so libpfac.so libpfac.so+PFAC_POOL64=8 > gpurun_out/ab_c3.log 2>&1; cat gpurun_out/ab_c3.log
+timeout 900 python tools/ab.py 4 3 libpfac_ref.so libpfac.so libpfac.so+PFAC_POOL64=8 > gpurun_out/ab_c4.log 2>&1; cat gpurun_out/ab_c4.log
+timeout 600 python tools/ab.py 2 4 libpfac_ref.so libpfac.so > gpurun_out/ab_c2.log 2>&1; cat gpurun_out/ab_c2.log
