@@ -633,6 +633,10 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
 
 template <int Kind, int kSlots>
 __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a) {
+    // the shared round pool (cross-CTA balance) is planned only for kinds
+    // whose tries may live outside shared memory; the pair-filter kernel
+    // (small sets, staged tries) is built without it
+    constexpr bool kPool = Kind != 2;
     extern __shared__ __align__(128) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t *s_filter = reinterpret_cast<uint32_t *>(smem);
@@ -669,7 +673,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, pl);
     }
     if (lane < kSlots) mbar_init(&bars[lane], 1);
-    uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 2);  // round counter of the CTA
+    uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 1);  // round counter of the CTA (phase 1;
+                                                                            // then s_wtot[kWarps + 1])
     if (tid == 32) *s_next = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (blockIdx.x == 0 && tid == 0) {  // for the next launch
@@ -716,8 +721,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                                                                                   : a.n_main) - cta_round0);
     // the shared pool (the text's last rounds, taken by any warp once its
     // CTA's range is done: cross-CTA balance) in the CTA's local round
-    // numbering: [pool_lo, pool_hi) (start offsets stay 32-bit: planned so)
-    const uint32_t pool_lo = (uint32_t)(a.n_main - cta_round0), pool_hi = (uint32_t)(n_rounds - cta_round0);
+    // numbering: [pool_lo, pool_hi) (start offsets stay 32-bit: planned so;
+    // recomputed where used: no registers held through phase 1)
     const uint64_t cta_lo = cta_round0 * kRound;
     uint2 *hits = a.hits + (uint64_t)gw * a.hit_cap;
 
@@ -747,11 +752,11 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             r = n_ctg + __shfl_sync(0xffffffffu, r, 0);
             if (r >= n_local) {  // the CTA's range is done: a pool round, if any is left
                 r = kNoRound;
-                if (a.pool_seg) {
+                if (kPool && a.pool_seg) {
                     if (lane == 0) {
                         const uint32_t q = atomicAdd(&a.ws->pool_next[a.parity], 1u);
-                        if (q < pool_hi - pool_lo) {
-                            r = pool_lo + q;
+                        if (q < (uint32_t)((a.n_starts + kRound - 1) / kRound - a.n_main)) {
+                            r = (uint32_t)(a.n_main - cta_round0) + q;
                             a.round_val[cta_round0 + r] = 0ull;  // its count (ordered before the warp's
                                                                  // walks by their __syncwarp)
                         }
@@ -1119,7 +1124,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         if (lane == 0) {
             s_wtot[kWarps] = pre;
             s_wtot[kWarps + 1] = all;
-            if (blockIdx.x == 0 && !a.pool_seg) *a.out_count = all;
+            if (blockIdx.x == 0 && !(kPool && a.pool_seg)) *a.out_count = all;
         }
     }
     __syncthreads();
@@ -1128,7 +1133,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // CTA b scans pool segment b in place, a second grid barrier, then every
     // CTA holds each segment's first row (s_pool, in the idle ring).
     unsigned long long *s_pool = reinterpret_cast<unsigned long long *>(smem + a.off_ring);
-    if (a.pool_seg) {
+    const uint32_t pool_lo = (uint32_t)(a.n_main - cta_round0), pool_hi = (uint32_t)(n_rounds - cta_round0);
+    if (kPool && a.pool_seg) {
         const unsigned long long all_main = s_wtot[kWarps + 1];
         __syncthreads();
         const uint64_t g0 = a.n_main + (uint64_t)blockIdx.x * a.pool_seg;
@@ -1146,7 +1152,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     STAMP(3);
 
     // ================================================= phase 3: emit
-    if (n_ctg == n_local && !a.pool_seg && n_hits <= a.hit_cap) {
+    if (n_ctg == n_local && !(kPool && a.pool_seg) && n_hits <= a.hit_cap) {
         // blocks only: the warp's hits are in position order and its rows
         // follow the CTA's earlier warps' rows
         uint64_t run_rows = cta_off + warp_base;
@@ -1224,10 +1230,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         // the block's rounds, then the CTA's dynamic rounds and the pool's the warp took
         auto next_round = [&](uint32_t r) -> uint32_t {
             if (r == wend) r = n_ctg;
-            if (r == n_local && a.pool_seg) r = pool_lo;
+            if (r == n_local && kPool && a.pool_seg) r = pool_lo;
             return r;
         };
-        const uint32_t r_end = a.pool_seg ? pool_hi : n_local;
+        const uint32_t r_end = kPool && a.pool_seg ? pool_hi : n_local;
         for (uint32_t r = next_round(wbeg); r < r_end; r = next_round(r + 1)) {
             const bool dyn = r >= n_ctg;
             if (dyn && __ldcg(a.round_owner + cta_round0 + r) != gw) continue;
@@ -1411,6 +1417,29 @@ int debug_timing(unsigned long long *host, uint64_t n) {
 }
 #endif
 
+// Environment knobs of the tools (ablations, plan dumps), read once per
+// process: a launch costs no environment scans.
+struct Knobs {
+    bool k4_nopair, slots2, debug_plan, l2_persist;
+    const char *bigl1_hot, *hot_bytes, *max_rep_log2, *ctg64, *pool64;
+};
+const Knobs &knobs() {
+    static const Knobs k = [] {
+        Knobs v;
+        v.k4_nopair = std::getenv("PFAC_K4_NOPAIR") != nullptr;
+        v.slots2 = std::getenv("PFAC_SLOTS2") != nullptr;
+        v.debug_plan = std::getenv("PFAC_DEBUG_PLAN") != nullptr;
+        v.l2_persist = std::getenv("PFAC_L2_PERSIST") != nullptr;
+        v.bigl1_hot = std::getenv("PFAC_BIGL1_HOT");
+        v.hot_bytes = std::getenv("PFAC_HOT_BYTES");
+        v.max_rep_log2 = std::getenv("PFAC_MAX_REP_LOG2");
+        v.ctg64 = std::getenv("PFAC_CTG64");
+        v.pool64 = std::getenv("PFAC_POOL64");
+        return v;
+    }();
+    return k;
+}
+
 int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const uint8_t *d_text,
                 uint64_t readable_len, uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                 uint64_t capacity, uint64_t *d_count, void *d_ws, uint64_t ws_bytes, CUstream_st *stream_,
@@ -1474,12 +1503,12 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     const uint32_t defer = t.kind == 3 ? 64u : t.kind == 4 ? 96u : (uint32_t)kDefer;  // (kernel: kDefer for kinds 1, 2)
     // the 2-gram test (and its 8 KiB table): not for DNA (every 2-gram begins a
     // pattern); optional for 8-byte prefixes (tuning knob)
-    const bool use_pair = t.kind != 3 && !(t.kind == 4 && std::getenv("PFAC_K4_NOPAIR"));
+    const bool use_pair = t.kind != 3 && !(t.kind == 4 && knobs().k4_nopair);
     uint32_t kSlots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
-    if (std::getenv("PFAC_SLOTS2") && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
+    if (knobs().slots2 && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
     const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
                            kWarps * defer * (t.kind == 1 ? 8 : 4) + (use_pair ? 8192 : 0) +
-                           align16(40 * B) + 8 * (kWarps + 3) + 512;
+                           align16(40 * B) + 8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac_match_device: filter does not fit shared memory";
         return kStatusLimit;
@@ -1501,9 +1530,9 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
         hot_bytes(t.n_nodes - 1) <= trie_budget ? trie_budget : (trie_budget < kHotCap ? trie_budget : kHotCap);
     if (big_l1) {  // root table and level-1 bitmaps only (+ a tuning knob)
         budget = 64;
-        if (const char *h = std::getenv("PFAC_BIGL1_HOT")) budget = (uint32_t)std::strtoul(h, nullptr, 10);
+        if (const char *h = knobs().bigl1_hot) budget = (uint32_t)std::strtoul(h, nullptr, 10);
     }
-    if (const char *cap = std::getenv("PFAC_HOT_BYTES")) {  // placement ablation (tools/placement.py) only
+    if (const char *cap = knobs().hot_bytes) {  // placement ablation (tools/placement.py) only
         const uint32_t c = (uint32_t)std::strtoul(cap, nullptr, 10);
         if (c < budget) budget = c;
     }
@@ -1520,7 +1549,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     uint32_t rep_log2 = rep0;
     while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= (left < kFilterCap ? left : kFilterCap)) rep_log2++;
     if (big_l1) rep_log2 = 0;
-    if (const char *r = std::getenv("PFAC_MAX_REP_LOG2")) {  // placement ablation only
+    if (const char *r = knobs().max_rep_log2) {  // placement ablation only
         const uint32_t m = (uint32_t)std::strtoul(r, nullptr, 10);
         if (rep_log2 > m) rep_log2 = m;
     }
@@ -1534,7 +1563,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     o = align_up(o, 128);
     a.off_ring = o;   o += kWarps * kSlots * kSlotBytes;
     a.off_bar = o;    o += (kWarps * kSlots + 1) * 8;
-    a.off_warp = o;   o += 8 * (kWarps + 3);  // warp totals [kWarps + 2] + the CTA's round counter
+    a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 2] (the last: the CTA's round counter first)
     o = align_up(o, 16);
     a.off_root = o;   o += 1024;
     a.off_defer = o;  o += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
@@ -1572,11 +1601,11 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // rounds in per-warp blocks; else the last quarter is handed out
     // dynamically (measured: C3 -11% dynamic)
     {
-        const char *e = std::getenv("PFAC_CTG64");  // tools only
+        const char *e = knobs().ctg64;  // tools only
         a.ctg64 = e ? (uint32_t)std::min(64l, std::max(0l, std::atol(e))) : (H >= t.n_nodes - 1 ? 64u : 48u);
     }
     a.hot_edges = EH;
-    if (std::getenv("PFAC_DEBUG_PLAN")) {  // tools only
+    if (knobs().debug_plan) {  // tools only
         std::fprintf(stderr,
                          "pfac plan: kind %u smem %zu of %d; filter %u B x%u; hot nodes %u of %u (edges %u, tails %u, "
                          "tail bytes %u); terms in smem %d; grid %llu x %d warps, %llu rounds/CTA, hit cap %u\n",
@@ -1612,10 +1641,10 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // skew between ranges, e.g. C5's first ranges hold twice the matches);
     // planned when start offsets from a CTA's first round stay 32-bit
     {
-        const char *e = std::getenv("PFAC_POOL64");  // tools only: pool share in 64ths
+        const char *e = knobs().pool64;  // tools only: pool share in 64ths
         const uint64_t pool64 = e ? (uint64_t)std::min(32l, std::max(0l, std::atol(e))) : (a.ctg64 < 64 ? 4u : 0u);
         const uint64_t n_pool = geo.n_rounds * pool64 / 64;
-        const bool pool = n_pool >= geo.grid && geo.n_rounds * (uint64_t)kRound < (1ull << 32);
+        const bool pool = t.kind != 2 && n_pool >= geo.grid && geo.n_rounds * (uint64_t)kRound < (1ull << 32);
         a.n_main = pool ? geo.n_rounds - n_pool : geo.n_rounds;
         a.rounds_per_cta = pool ? (a.n_main + geo.grid - 1) / geo.grid : geo.rounds_per_cta;
         a.pool_seg = pool ? (uint32_t)((n_pool + geo.grid - 1) / geo.grid) : 0u;
@@ -1623,7 +1652,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
     const void *fn = kernel_for(t.kind, kSlots);
-    if (std::getenv("PFAC_L2_PERSIST")) {  // placement ablation only: the device image as an L2 persisting window
+    if (knobs().l2_persist) {  // placement ablation only: the device image as an L2 persisting window
         static std::once_flag once;
         std::call_once(once, [&] { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 64u << 20); });
         cudaStreamAttrValue v = {};
