@@ -125,6 +125,22 @@ def test_capacity_overflow_and_count():
     assert np.array_equal(sc.pid[:100].cpu().numpy().astype(np.uint32), want_q[:100])
 
 
+def test_round_pool_and_overflow():
+    """A trie too large for shared memory (C4's 100,000 patterns) plans
+    dynamic rounds and the shared round pool (the text's last 1/16); dense
+    'a' runs in a CTA range and in the pool overflow the warps' hit lists,
+    so the re-scan fallback runs over block, dynamic and pool rounds."""
+    ps = gen.patterns(4).to_list() + [b"a" * k for k in range(4, 9)]
+    n = 4 << 20
+    text = gen.text(4, 0, n).copy()
+    text[n // 3:n // 3 + (64 << 10)] = ord("a")
+    text[n - (256 << 10):n - 1000] = ord("a")
+    t = pf.Trie(ps)
+    want = oracle.Trie(ps).match(text)
+    assert_same(gpu_rows(t, text), want, "pool + overflow")
+    assert_same(gpu_rows(t, text, offset=3), want, "pool + overflow, unaligned")
+
+
 @pytest.mark.parametrize("kind", ["nested", "zero_bytes", "long", "len1", "len2", "dups"])
 def test_adversarial(kind):
     rng = np.random.default_rng(["nested", "zero_bytes", "long", "len1", "len2", "dups"].index(kind))
