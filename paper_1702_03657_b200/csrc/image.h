@@ -98,6 +98,19 @@
 //                     empty slots hold kset_empty (a value that is no key),
 //                     load <= 1/2.  A start whose key is absent cannot match:
 //                     the walk is skipped (the filter's false positives).
+//   entry8 u32[2^entry8_log2][4]  (filter kind 4: every pattern has >= 8
+//                     bytes) the depth-8 entry table: one entry {x0, x1,
+//                     node, depth} per distinct 8-byte pattern prefix (x0 =
+//                     bytes 0..3, x1 = bytes 4..7, little-endian); node =
+//                     the deepest image node on the prefix's path at depth
+//                     <= 8 (a node inside a tail or chain record is not in the
+//                     image: its record's start is), depth = its depth.  Open
+//                     addressing, slot = entry8_slot(x0, x1), linear probing,
+//                     empty slots hold node = kNone, load <= 1/2.  A start
+//                     whose 8 bytes are absent cannot match (no pattern is
+//                     shorter than 8); else the walk from (node, depth) equals
+//                     the walk from the root, as no pattern ends
+//                     above depth 8.
 #pragma once
 #include <cstdint>
 
@@ -109,7 +122,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 12;
+constexpr uint32_t kVersion = 13;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -136,12 +149,18 @@ struct ImageHeader {
     uint64_t off_kset;                 // exact key set (0: none), see below
     uint32_t kset_log2, kset_empty;    // log2 of its slots; the empty-slot marker
     uint64_t off_pair;                 // 2-gram prefix table u32[256][8]
-    uint8_t pad[512 - 256 - 24];
+    uint64_t off_entry8;               // depth-8 entry table (0: none), see above
+    uint32_t entry8_log2, entry8_pad;  // log2 of its slots; 0
+    uint8_t pad[512 - 256 - 40];
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 
 // First slot of a key in the exact key set.
 PFAC_HD inline uint32_t kset_slot(uint32_t key, uint32_t log2) { return (key * kFilterMul) >> (32u - log2); }
+// First slot of an 8-byte prefix (x0 = bytes 0..3, x1 = bytes 4..7) in the depth-8 entry table.
+PFAC_HD inline uint32_t entry8_slot(uint32_t x0, uint32_t x1, uint32_t log2) {
+    return (x0 * kFilterMul + x1 * kFilterMul2) >> (32u - log2);
+}
 // Offset of the aux section (it follows the node section).
 PFAC_HD inline uint64_t aux_offset(uint64_t off_node, uint64_t n_nodes) {
     return (off_node + 4 * (n_nodes + 1) + 255) / 256 * 256;

@@ -127,6 +127,7 @@ struct ScanArgs {
                                     // (the rest, the range's end, is handed out dynamically)
     uint32_t defer;                 // walk-queue capacity per warp (>= 33)
     uint32_t use_pair;              // the 2-gram prefix table is staged and tested
+    uint32_t use_entry8;            // kind 4: walks enter through the depth-8 entry table
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -379,13 +380,16 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
 // set bits); deeper nodes use the CSR label list of the image; tail and chain
 // starts compare their path's bytes at once.
 template <class Text>
-__device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0) {
-    uint32_t v = s.root[tx.at(r0)];
+__device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0, uint32_t v0 = 0,
+                         uint32_t d0 = 1) {
+    // (v0, d0): enter at image node v0 of depth d0 whose path the start's
+    // first d0 bytes spell (the depth-8 entry table); else from the root
+    uint32_t v = v0 ? v0 : s.root[tx.at(r0)];
     if (v == 0) return kNone;
     uint32_t w = node_word(a, s, v);
     uint32_t last = (w & kTermBit) ? v : kNone;
-    uint32_t j = r0 + 1;
-    bool l1 = true;  // v is a level-1 node: the next step uses its bitmap
+    uint32_t j = r0 + d0;
+    bool l1 = d0 == 1;  // v is a level-1 node: the next step uses its bitmap
     while (j < tx.end) {
         uint32_t nv = kNone;
         if (w & kTailBit) {
@@ -572,6 +576,17 @@ __device__ __forceinline__ bool kset_probe(const ScanArgs &a, uint32_t key) {
     }
 }
 
+// Kind 4: the depth-8 entry of the start's first 8 bytes (image.h): its
+// node and depth, or node 0 when no pattern begins with them.
+__device__ __forceinline__ uint2 entry8_find(const ScanArgs &a, uint32_t x0, uint32_t x1) {
+    const uint32_t mask = (1u << a.t.entry8_log2) - 1u;
+    for (uint32_t i = entry8_slot(x0, x1, a.t.entry8_log2);; i = (i + 1) & mask) {
+        const uint4 e = __ldg(a.t.entry8 + i);
+        if (e.z == kNone) return make_uint2(0u, 0u);
+        if (e.x == x0 && e.y == x1) return make_uint2(e.z, e.w);
+    }
+}
+
 // Is the start's filter key in the image's exact key set (image.h)?  Kind 3:
 // the 16-base DNA key; kinds 1, 2: the first 4 bytes.
 template <int Kind>
@@ -610,9 +625,16 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
             // the exact key set rejects the filter's false positives before the walk
             // (kind 1: the key was taken from the ring when queued; kind 3 reads
             // it from the text: most of its probes hit and the walk follows)
-            if (Kind == 1 && a.use_kset ? kset_probe(a, dkey[j])
-                                        : (Kind == 3 && a.use_kset ? kset_has<Kind>(a, gt) : true))
+            if (Kind == 4 && a.use_entry8) {
+                // enter at depth <= 8 through the entry table (a miss: no pattern starts here)
+                if (gt.end >= kGram8) {
+                    const uint2 en = entry8_find(a, gt.at4(0), gt.at4(4));
+                    if (en.x) tn = walk(a, s, gt, 0u, en.x, en.y);
+                }
+            } else if (Kind == 1 && a.use_kset ? kset_probe(a, dkey[j])
+                                               : (Kind == 3 && a.use_kset ? kset_has<Kind>(a, gt) : true)) {
                 tn = walk(a, s, gt, 0u);
+            }
             if (tn != kNone) {
                 const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
                 if (p < ctg_bytes) rows += cnt;  // the lane's rows in its warp's block (per-warp totals)
@@ -1389,6 +1411,8 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.kset = h.off_kset ? reinterpret_cast<const uint32_t *>(d + h.off_kset) : nullptr;
     t.kset_log2 = h.kset_log2;
     t.kset_empty = h.kset_empty;
+    t.entry8 = h.off_entry8 ? reinterpret_cast<const uint4 *>(d + h.off_entry8) : nullptr;
+    t.entry8_log2 = h.entry8_log2;
     t.n_terminals = (uint32_t)h.n_terminals;
     t.n_kept_terminals = (uint32_t)h.n_kept_terminals;
     t.max_len = h.max_len;
@@ -1420,7 +1444,7 @@ int debug_timing(unsigned long long *host, uint64_t n) {
 // Environment knobs of the tools (ablations, plan dumps), read once per
 // process: a launch costs no environment scans.
 struct Knobs {
-    bool k4_nopair, slots2, debug_plan, l2_persist;
+    bool k4_nopair, slots2, debug_plan, l2_persist, no_entry8;
     const char *bigl1_hot, *hot_bytes, *max_rep_log2, *ctg64, *pool64;
 };
 const Knobs &knobs() {
@@ -1430,6 +1454,7 @@ const Knobs &knobs() {
         v.slots2 = std::getenv("PFAC_SLOTS2") != nullptr;
         v.debug_plan = std::getenv("PFAC_DEBUG_PLAN") != nullptr;
         v.l2_persist = std::getenv("PFAC_L2_PERSIST") != nullptr;
+        v.no_entry8 = std::getenv("PFAC_NO_ENTRY8") != nullptr;
         v.bigl1_hot = std::getenv("PFAC_BIGL1_HOT");
         v.hot_bytes = std::getenv("PFAC_HOT_BYTES");
         v.max_rep_log2 = std::getenv("PFAC_MAX_REP_LOG2");
@@ -1597,6 +1622,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // walks through a shared-memory trie are cheaper than an L2 probe of the
     // exact key set: probe only when the trie is not wholly staged
     a.use_kset = t.kset != nullptr && H < t.n_nodes - 1;
+    a.use_entry8 = t.entry8 != nullptr && !knobs().no_entry8;
     // walks through a wholly staged trie are short and even: (almost) all
     // rounds in per-warp blocks; else the last quarter is handed out
     // dynamically (measured: C3 -11% dynamic)

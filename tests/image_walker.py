@@ -10,7 +10,7 @@ TERM = 0x80000000
 TAIL = 0x40000000
 MASK = 0x3FFFFFFF
 
-_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q")
+_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II")
 
 
 def parse(image: bytes) -> dict:
@@ -20,7 +20,8 @@ def parse(image: bytes) -> dict:
             "filter_kind", "off_node", "off_label", "off_term_node", "off_out_ptr", "off_out_pid", "off_root",
             "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core",
             "n_tails", "n_tail_bytes", "off_tail_bits", "off_tail_rank", "off_tails", "off_tail_bytes",
-            "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full", "off_kset", "kset_log2", "kset_empty", "off_pair"]
+            "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full", "off_kset", "kset_log2", "kset_empty", "off_pair",
+            "off_entry8", "entry8_log2", "entry8_pad"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
@@ -43,7 +44,20 @@ def parse(image: bytes) -> dict:
     h["pair"] = buf[h["off_pair"]:h["off_pair"] + 8192].view(np.uint32).reshape(256, 8)
     if h["off_kset"]:
         h["kset"] = buf[h["off_kset"]:h["off_kset"] + (4 << h["kset_log2"])].view(np.uint32)
+    if h["off_entry8"]:
+        h["entry8"] = buf[h["off_entry8"]:h["off_entry8"] + (16 << h["entry8_log2"])].view(np.uint32).reshape(-1, 4)
     return h
+
+
+def entry8_find(h, x0, x1):
+    """Depth-8 entry table probe (image.h): (node, depth) or None."""
+    t, lg = h["entry8"], h["entry8_log2"]
+    i = ((x0 * 0x9E3779B1 + x1 * 0x85EBCA6B) & 0xFFFFFFFF) >> (32 - lg)
+    while int(t[i][2]) != 0xFFFFFFFF:
+        if int(t[i][0]) == x0 and int(t[i][1]) == x1:
+            return int(t[i][2]), int(t[i][3])
+        i = (i + 1) & ((1 << lg) - 1)
+    return None
 
 
 def tail_index(h, v):
@@ -116,17 +130,18 @@ def term_of(h, last):
     return k
 
 
-def walk(h, text, i, L):
-    """Terminal index of the deepest terminal passed by the walk from start i.
-    Bit 30 marks a tail start (record ends at a terminal: compare and stop) or
-    a chain start (record ends at node x: compare, continue at x)."""
+def walk(h, text, i, L, v0=None, d0=1):
+    """Terminal index of the deepest terminal passed by the walk from start i
+    (entered at node v0 of depth d0 when given).  Bit 30 marks a tail start
+    (record ends at a terminal: compare and stop) or a chain start (record
+    ends at node x: compare, continue at x)."""
     node, label = h["node"], h["label"]
-    v = int(h["root"][text[i]])
+    v = int(h["root"][text[i]]) if v0 is None else v0
     if v == 0:
         return None
     last = v if node[v] & TERM else None
-    j = i + 1
-    l1 = True
+    j = i + d0
+    l1 = d0 == 1
     while j < L:
         if node[v] & TAIL:
             off, ln, ti, x = (int(y) for y in h["tails"][tail_index(h, v)])
@@ -182,7 +197,11 @@ def match(h, text: bytes, readable=None, n_starts=None):
             continue
         if h["off_kset"] and not kset_has(h, key):  # the exact key set (image.h)
             continue
-        ti = walk(h, text, i, L)
+        if h["off_entry8"]:  # kind 4: enter through the depth-8 entry table
+            en = entry8_find(h, key & 0xFFFFFFFF, key >> 32)
+            ti = walk(h, text, i, L, *en) if en else None
+        else:
+            ti = walk(h, text, i, L)
         if ti is not None:
             for r in range(int(h["out_ptr"][ti]), int(h["out_ptr"][ti + 1])):
                 rows.append((i, int(h["out_pid"][r])))

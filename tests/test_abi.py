@@ -111,6 +111,52 @@ def test_pair_table(cid):
         assert [int(x) for x in h["pair"][b0]] == want, b0
 
 
+def test_entry8_table():
+    """Kind 4 (C3): one entry per distinct 8-byte pattern prefix; entering the
+    walk at the entry's (node, depth) gives the root walk's result for every
+    pattern, the entry node is the root walk's node after `depth` bytes, and
+    8-byte strings that begin no pattern are absent."""
+    ps = gen.patterns(3).to_list()
+    h = image_walker.parse(pf.Trie(ps).image())
+    assert h["filter_kind"] == 4 and h["off_entry8"]
+    prefixes = {p[:8] for p in ps}
+    assert int((h["entry8"][:, 2] != 0xFFFFFFFF).sum()) == len(prefixes)
+    rng = np.random.default_rng(3)
+    for k in rng.choice(len(ps), 1500, replace=False):
+        p = ps[int(k)]
+        en = image_walker.entry8_find(h, int.from_bytes(p[:4], "little"), int.from_bytes(p[4:8], "little"))
+        assert en is not None and 1 <= en[1] <= 8
+        full = image_walker.walk(h, p, 0, len(p))
+        assert full is not None and image_walker.walk(h, p, 0, len(p), *en) == full
+        # the entry node is on the path: the root walk over the first `depth`
+        # bytes of p (a prefix of length en[1] need not be a pattern, so walk
+        # p itself truncated there and compare the node reached)
+        assert _node_after(h, p, en[1]) == en[0]
+    for _ in range(2000):
+        x = rng.integers(0, 256, 8).astype(np.uint8).tobytes()
+        if x not in prefixes:
+            assert image_walker.entry8_find(h, int.from_bytes(x[:4], "little"), int.from_bytes(x[4:], "little")) is None
+
+
+def _node_after(h, text, d):
+    """Image node reached by consuming text[:d] from the root (a record's
+    start when the path enters a record before depth d)."""
+    node, label = h["node"], h["label"]
+    v, j = int(h["root"][text[0]]), 1
+    while j < d:
+        if int(node[v]) & image_walker.TAIL:
+            off, ln, ti, x = (int(y) for y in h["tails"][image_walker.tail_index(h, v)])
+            if ti != 0xFFFFFFFF or j + ln > d:
+                return v  # the record spans depth d: its start is the deepest image node
+            v, j = x, j + ln
+            continue
+        s_, e_ = int(node[v]) & image_walker.MASK, int(node[v + 1]) & image_walker.MASK
+        k = int(np.searchsorted(label[s_:e_], text[j]))
+        assert k < e_ - s_ and label[s_ + k] == text[j]
+        v, j = s_ + k + 1, j + 1
+    return v
+
+
 @pytest.mark.parametrize("cid", [2, 3, 4, 5])
 def test_aux_words(cid):
     """aux[v] = record rank (tail/chain start) or packed labels (1..4 children)."""
