@@ -198,20 +198,27 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     const uint64_t NK = order.size();
     std::vector<uint32_t> new_id(N, kNone);
     for (uint64_t i = 0; i < NK; i++) new_id[order[i]] = (uint32_t)i;
-    // depth-8 entries (image.h; used by kind 4): per depth-8 node, its 8-byte
-    // path and the deepest kept node at depth <= 8 on it
-    std::vector<uint32_t> e8;  // {x0, x1, node, depth} per distinct 8-byte prefix
-    if (min_len >= kGram8) {
-        for (uint64_t u = 1; u < N; u++) {
-            if (q[u].depth != kGram8) continue;
-            const uint8_t *pt = pats[ord[q[u].lo]];
-            uint64_t a = u;
-            while (removed[a]) a = parent[a];
-            e8.push_back((uint32_t)pt[0] | (uint32_t)pt[1] << 8 | (uint32_t)pt[2] << 16 | (uint32_t)pt[3] << 24);
-            e8.push_back((uint32_t)pt[4] | (uint32_t)pt[5] << 8 | (uint32_t)pt[6] << 16 | (uint32_t)pt[7] << 24);
-            e8.push_back(new_id[a]);
-            e8.push_back(q[a].depth);
+    // entry-table candidates (image.h): per node at depth D (8: kind 4; 16:
+    // kind 3), its key and the deepest kept node at depth <= D on its path
+    std::vector<uint32_t> e8, e16;  // {x0, x1, node, depth} per distinct D-byte prefix
+    for (uint64_t u = 1; u < N; u++) {
+        const uint32_t du = q[u].depth;
+        if (!((du == kGram8 && min_len >= kGram8) || (du == kDnaGram && min_len >= kDnaGram))) continue;
+        const uint8_t *pt = pats[ord[q[u].lo]];
+        uint64_t a = u;
+        while (removed[a]) a = parent[a];
+        std::vector<uint32_t> &ev = du == kGram8 ? e8 : e16;
+        if (du == kGram8) {
+            ev.push_back((uint32_t)pt[0] | (uint32_t)pt[1] << 8 | (uint32_t)pt[2] << 16 | (uint32_t)pt[3] << 24);
+            ev.push_back((uint32_t)pt[4] | (uint32_t)pt[5] << 8 | (uint32_t)pt[6] << 16 | (uint32_t)pt[7] << 24);
+        } else {  // the 16-base DNA key (only used when every pattern byte is A, C, G or T)
+            uint32_t key = 0;
+            for (uint32_t b = 0; b < kDnaGram; b++) key |= dna_code(pt[b]) << (2 * b);
+            ev.push_back(key);
+            ev.push_back(0u);
         }
+        ev.push_back(new_id[a]);
+        ev.push_back(q[a].depth);
     }
 
     // compressed CSR (bit 30 marks a tail or chain start: its record holds the bytes)
@@ -456,7 +463,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     // where a walk is cheaper than a probe)
     std::vector<uint32_t> kset;
     uint32_t kset_log2 = 0, kset_empty = 0;
-    if (kind == 1 || kind == 3) {
+    if (kind == 1) {  // (kind 3 enters through the entry table instead)
         std::vector<uint32_t> keys(m);
         for (uint32_t k = 0; k < m; k++) {
             if (kind == 3) {
@@ -483,24 +490,25 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         }
     }
 
-    // ---- depth-8 entry table (kind 4; image.h)
-    std::vector<uint32_t> entry8;
-    uint32_t entry8_log2 = 0;
-    if (kind == 4) {
+    // ---- entry table (kinds 3 and 4; image.h)
+    std::vector<uint32_t> entry;
+    uint32_t entry_log2 = 0;
+    if (kind == 3) e8.swap(e16);
+    if (kind == 4 || kind == 3) {
         const uint64_t ne = e8.size() / 4;
-        entry8_log2 = 4;
-        while ((1ull << entry8_log2) < 2 * ne) entry8_log2++;
-        if (entry8_log2 > 30) {
-            err = "pfac_build: too many 8-byte prefixes";
+        entry_log2 = 4;
+        while ((1ull << entry_log2) < 2 * ne) entry_log2++;
+        if (entry_log2 > 30) {
+            err = "pfac_build: too many entry-table keys";
             return kStatusLimit;
         }
-        entry8.assign((size_t)4 << entry8_log2, 0u);
-        for (size_t i = 0; i < ((size_t)1 << entry8_log2); i++) entry8[4 * i + 2] = kNone;
-        const uint32_t mask = (1u << entry8_log2) - 1u;
+        entry.assign((size_t)4 << entry_log2, 0u);
+        for (size_t i = 0; i < ((size_t)1 << entry_log2); i++) entry[4 * i + 2] = kNone;
+        const uint32_t mask = (1u << entry_log2) - 1u;
         for (uint64_t k = 0; k < ne; k++) {
-            uint32_t i = entry8_slot(e8[4 * k], e8[4 * k + 1], entry8_log2);
-            while (entry8[4 * i + 2] != kNone) i = (i + 1) & mask;
-            std::memcpy(&entry8[4 * i], &e8[4 * k], 16);
+            uint32_t i = entry_slot(e8[4 * k], e8[4 * k + 1], entry_log2);
+            while (entry[4 * i + 2] != kNone) i = (i + 1) & mask;
+            std::memcpy(&entry[4 * i], &e8[4 * k], 16);
         }
     }
 
@@ -543,9 +551,9 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
     o = align256(o + 4 * kset.size());
     h.kset_log2 = kset_log2;
     h.kset_empty = kset_empty;
-    h.off_entry8 = entry8.empty() ? 0 : o;
-    o = align256(o + 4 * entry8.size());
-    h.entry8_log2 = entry8_log2;
+    h.off_entry = entry.empty() ? 0 : o;
+    o = align256(o + 4 * entry.size());
+    h.entry_log2 = entry_log2;
     h.n_level1 = B;
     h.n_tails = NT;
     h.n_tail_bytes = tail_bytes.size();
@@ -587,7 +595,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         }
     }
     if (!kset.empty()) std::memcpy(p + h.off_kset, kset.data(), 4 * kset.size());
-    if (!entry8.empty()) std::memcpy(p + h.off_entry8, entry8.data(), 4 * entry8.size());
+    if (!entry.empty()) std::memcpy(p + h.off_entry, entry.data(), 4 * entry.size());
     return kStatusOk;
 }
 
@@ -609,11 +617,12 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
     bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
               in(off_aux, 4 * N) && off_aux + 4 * N <= h.off_label && in(h.off_pair, 8192) &&
               (h.off_kset == 0 ? h.kset_log2 == 0
-                               : ((h.filter_kind == 1 || h.filter_kind == 3) && h.kset_log2 >= 6 &&
+                               : (h.filter_kind == 1 && h.kset_log2 >= 6 &&
                                   h.kset_log2 <= 30 && in(h.off_kset, 4ull << h.kset_log2))) &&
-              (h.off_entry8 == 0 ? h.entry8_log2 == 0
-                                 : (h.filter_kind == 4 && h.entry8_log2 >= 4 && h.entry8_log2 <= 30 &&
-                                    in(h.off_entry8, 16ull << h.entry8_log2))) &&
+              (h.off_entry == 0 ? h.entry_log2 == 0
+                                 : ((h.filter_kind == 4 || h.filter_kind == 3) && h.entry_log2 >= 4 &&
+                                    h.entry_log2 <= 30 &&
+                                    in(h.off_entry, 16ull << h.entry_log2))) &&
               h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails >= T && h.n_nodes_full >= N &&
               in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
@@ -643,10 +652,10 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
             n_tail_ends += !chain;
         }
         ok = ok && h.n_kept_terminals + n_tail_ends == T;
-        const uint32_t *e8 = reinterpret_cast<const uint32_t *>(p + h.off_entry8);  // entries: a node and depth <= 8
-        for (uint64_t i = 0; ok && h.off_entry8 && i < (1ull << h.entry8_log2); i++)
-            ok = e8[4 * i + 2] == kNone || (e8[4 * i + 2] > 0 && e8[4 * i + 2] < N && e8[4 * i + 3] >= 1 &&
-                                            e8[4 * i + 3] <= kGram8);
+        const uint32_t *en = reinterpret_cast<const uint32_t *>(p + h.off_entry);  // entries: a node, depth <= D
+        for (uint64_t i = 0; ok && h.off_entry && i < (1ull << h.entry_log2); i++)
+            ok = en[4 * i + 2] == kNone || (en[4 * i + 2] > 0 && en[4 * i + 2] < N && en[4 * i + 3] >= 1 &&
+                                            en[4 * i + 3] <= h.filter_gram);
     }
     if (!ok) {
         err = "pfac_attach: inconsistent image sections";

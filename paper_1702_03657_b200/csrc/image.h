@@ -91,26 +91,28 @@
 //                     level 1, or b0's level-1 node already is a terminal or a
 //                     tail/chain start (then every b1 is set).  Derived from
 //                     root + level1; the kernel tests survivors with it.
-//   kset   u32[2^kset_log2]  (filter kinds 1 and 3) the exact set of the
-//                     patterns' filter keys (first 4 bytes little-endian; kind
-//                     3: the 16-base DNA key): open addressing, slot =
-//                     (key * kFilterMul) >> (32 - kset_log2), linear probing,
-//                     empty slots hold kset_empty (a value that is no key),
-//                     load <= 1/2.  A start whose key is absent cannot match:
-//                     the walk is skipped (the filter's false positives).
-//   entry8 u32[2^entry8_log2][4]  (filter kind 4: every pattern has >= 8
-//                     bytes) the depth-8 entry table: one entry {x0, x1,
-//                     node, depth} per distinct 8-byte pattern prefix (x0 =
-//                     bytes 0..3, x1 = bytes 4..7, little-endian); node =
-//                     the deepest image node on the prefix's path at depth
-//                     <= 8 (a node inside a tail or chain record is not in the
-//                     image: its record's start is), depth = its depth.  Open
-//                     addressing, slot = entry8_slot(x0, x1), linear probing,
-//                     empty slots hold node = kNone, load <= 1/2.  A start
-//                     whose 8 bytes are absent cannot match (no pattern is
-//                     shorter than 8); else the walk from (node, depth) equals
-//                     the walk from the root, as no pattern ends
-//                     above depth 8.
+//   kset   u32[2^kset_log2]  (filter kind 1) the exact set of the patterns'
+//                     filter keys (first 4 bytes little-endian): open
+//                     addressing, slot = (key * kFilterMul) >> (32 -
+//                     kset_log2), linear probing, empty slots hold kset_empty
+//                     (a value that is no key), load <= 1/2.  A start whose
+//                     key is absent cannot match: the walk is skipped (the
+//                     filter's false positives).
+//   entry  u32[2^entry_log2][4]  (filter kinds 4 and 3; D = the filter gram:
+//                     8 bytes, or 16 DNA bases; every pattern has >= D bytes)
+//                     the entry table: one entry {x0, x1, node, depth} per
+//                     distinct D-byte pattern prefix (kind 4: x0 = bytes 0..3,
+//                     x1 = bytes 4..7, little-endian; kind 3: x0 = the 16-base
+//                     DNA key, x1 = 0); node = the deepest image node on the
+//                     prefix's path at depth <= D (a node inside a tail or
+//                     chain record is not in the image: its record's start
+//                     is), depth = its depth.  Open addressing, slot =
+//                     entry_slot(x0, x1), linear probing, empty slots hold
+//                     node = kNone, load <= 1/2.  A start whose D bytes are
+//                     absent (kind 3: or not all A/C/G/T, which the key
+//                     aliases) cannot match; else the walk from (node, depth)
+//                     equals the walk from the root, as no
+//                     pattern ends above depth D.
 #pragma once
 #include <cstdint>
 
@@ -149,16 +151,16 @@ struct ImageHeader {
     uint64_t off_kset;                 // exact key set (0: none), see below
     uint32_t kset_log2, kset_empty;    // log2 of its slots; the empty-slot marker
     uint64_t off_pair;                 // 2-gram prefix table u32[256][8]
-    uint64_t off_entry8;               // depth-8 entry table (0: none), see above
-    uint32_t entry8_log2, entry8_pad;  // log2 of its slots; 0
+    uint64_t off_entry;                // entry table (0: none), see above
+    uint32_t entry_log2, entry_pad;  // log2 of its slots; 0
     uint8_t pad[512 - 256 - 40];
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 
 // First slot of a key in the exact key set.
 PFAC_HD inline uint32_t kset_slot(uint32_t key, uint32_t log2) { return (key * kFilterMul) >> (32u - log2); }
-// First slot of an 8-byte prefix (x0 = bytes 0..3, x1 = bytes 4..7) in the depth-8 entry table.
-PFAC_HD inline uint32_t entry8_slot(uint32_t x0, uint32_t x1, uint32_t log2) {
+// First slot of a key (x0, x1) in the entry table.
+PFAC_HD inline uint32_t entry_slot(uint32_t x0, uint32_t x1, uint32_t log2) {
     return (x0 * kFilterMul + x1 * kFilterMul2) >> (32u - log2);
 }
 // Offset of the aux section (it follows the node section).

@@ -46,8 +46,8 @@ struct DevTrie {
     const uint32_t *pair;  // 2-gram prefix table [256][8]
     const uint32_t *kset;  // exact key set (nullptr: none)
     uint32_t kset_log2, kset_empty;
-    const uint4 *entry8;   // depth-8 entry table (nullptr: none)
-    uint32_t entry8_log2;
+    const uint4 *entry;   // depth-8 entry table (nullptr: none)
+    uint32_t entry_log2;
     uint32_t n_terminals;
     uint32_t n_kept_terminals;
     uint32_t max_len;

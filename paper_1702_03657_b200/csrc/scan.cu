@@ -127,7 +127,7 @@ struct ScanArgs {
                                     // (the rest, the range's end, is handed out dynamically)
     uint32_t defer;                 // walk-queue capacity per warp (>= 33)
     uint32_t use_pair;              // the 2-gram prefix table is staged and tested
-    uint32_t use_entry8;            // kind 4: walks enter through the depth-8 entry table
+    uint32_t use_entry;            // kind 4: walks enter through the depth-8 entry table
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -576,12 +576,13 @@ __device__ __forceinline__ bool kset_probe(const ScanArgs &a, uint32_t key) {
     }
 }
 
-// Kind 4: the depth-8 entry of the start's first 8 bytes (image.h): its
-// node and depth, or node 0 when no pattern begins with them.
-__device__ __forceinline__ uint2 entry8_find(const ScanArgs &a, uint32_t x0, uint32_t x1) {
-    const uint32_t mask = (1u << a.t.entry8_log2) - 1u;
-    for (uint32_t i = entry8_slot(x0, x1, a.t.entry8_log2);; i = (i + 1) & mask) {
-        const uint4 e = __ldg(a.t.entry8 + i);
+// The entry of a start's key (image.h; kind 4: its first 8 bytes, kind 3:
+// its 16-base DNA key): its node and depth, or node 0 when no pattern begins
+// with them.
+__device__ __forceinline__ uint2 entry_find(const ScanArgs &a, uint32_t x0, uint32_t x1) {
+    const uint32_t mask = (1u << a.t.entry_log2) - 1u;
+    for (uint32_t i = entry_slot(x0, x1, a.t.entry_log2);; i = (i + 1) & mask) {
+        const uint4 e = __ldg(a.t.entry + i);
         if (e.z == kNone) return make_uint2(0u, 0u);
         if (e.x == x0 && e.y == x1) return make_uint2(e.z, e.w);
     }
@@ -625,11 +626,30 @@ __device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem
             // the exact key set rejects the filter's false positives before the walk
             // (kind 1: the key was taken from the ring when queued; kind 3 reads
             // it from the text: most of its probes hit and the walk follows)
-            if (Kind == 4 && a.use_entry8) {
+            if (Kind == 4 && a.use_entry) {
                 // enter at depth <= 8 through the entry table (a miss: no pattern starts here)
                 if (gt.end >= kGram8) {
-                    const uint2 en = entry8_find(a, gt.at4(0), gt.at4(4));
+                    const uint2 en = entry_find(a, gt.at4(0), gt.at4(4));
                     if (en.x) tn = walk(a, s, gt, 0u, en.x, en.y);
+                }
+            } else if (Kind == 3 && a.use_entry) {
+                // enter at depth <= 16 when the 16 bytes are A/C/G/T (the key
+                // aliases other bytes, and no DNA pattern can cover those)
+                if (gt.end >= kDnaGram) {
+                    uint32_t key = 0;
+                    bool acgt = true;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t w = gt.at4(4 * q);
+                        const uint32_t c = (w >> 1) & 0x03030303u;  // the four 2-bit codes, one per byte
+                        const uint32_t sel = (c & 0xFu) | ((c >> 4) & 0xF0u) | ((c >> 8) & 0xF00u) | ((c >> 12) & 0xF000u);
+                        acgt &= __byte_perm(0x47544341u, 0u, sel) == w;  // code -> 'A','C','T','G'
+                        key |= __umulhi((w & 0x06060606u) * 0x820820u, 1u << 8) << (8 * q);
+                    }
+                    if (acgt) {
+                        const uint2 en = entry_find(a, key, 0u);
+                        if (en.x) tn = walk(a, s, gt, 0u, en.x, en.y);
+                    }
                 }
             } else if (Kind == 1 && a.use_kset ? kset_probe(a, dkey[j])
                                                : (Kind == 3 && a.use_kset ? kset_has<Kind>(a, gt) : true)) {
@@ -1411,8 +1431,8 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.kset = h.off_kset ? reinterpret_cast<const uint32_t *>(d + h.off_kset) : nullptr;
     t.kset_log2 = h.kset_log2;
     t.kset_empty = h.kset_empty;
-    t.entry8 = h.off_entry8 ? reinterpret_cast<const uint4 *>(d + h.off_entry8) : nullptr;
-    t.entry8_log2 = h.entry8_log2;
+    t.entry = h.off_entry ? reinterpret_cast<const uint4 *>(d + h.off_entry) : nullptr;
+    t.entry_log2 = h.entry_log2;
     t.n_terminals = (uint32_t)h.n_terminals;
     t.n_kept_terminals = (uint32_t)h.n_kept_terminals;
     t.max_len = h.max_len;
@@ -1444,7 +1464,7 @@ int debug_timing(unsigned long long *host, uint64_t n) {
 // Environment knobs of the tools (ablations, plan dumps), read once per
 // process: a launch costs no environment scans.
 struct Knobs {
-    bool k4_nopair, slots2, debug_plan, l2_persist, no_entry8;
+    bool k4_nopair, slots2, debug_plan, l2_persist, no_entry;
     const char *bigl1_hot, *hot_bytes, *max_rep_log2, *ctg64, *pool64;
 };
 const Knobs &knobs() {
@@ -1454,7 +1474,7 @@ const Knobs &knobs() {
         v.slots2 = std::getenv("PFAC_SLOTS2") != nullptr;
         v.debug_plan = std::getenv("PFAC_DEBUG_PLAN") != nullptr;
         v.l2_persist = std::getenv("PFAC_L2_PERSIST") != nullptr;
-        v.no_entry8 = std::getenv("PFAC_NO_ENTRY8") != nullptr;
+        v.no_entry = std::getenv("PFAC_NO_ENTRY") != nullptr;
         v.bigl1_hot = std::getenv("PFAC_BIGL1_HOT");
         v.hot_bytes = std::getenv("PFAC_HOT_BYTES");
         v.max_rep_log2 = std::getenv("PFAC_MAX_REP_LOG2");
@@ -1622,7 +1642,7 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     // walks through a shared-memory trie are cheaper than an L2 probe of the
     // exact key set: probe only when the trie is not wholly staged
     a.use_kset = t.kset != nullptr && H < t.n_nodes - 1;
-    a.use_entry8 = t.entry8 != nullptr && !knobs().no_entry8;
+    a.use_entry = t.entry != nullptr && !knobs().no_entry;
     // walks through a wholly staged trie are short and even: (almost) all
     // rounds in per-warp blocks; else the last quarter is handed out
     // dynamically (measured: C3 -11% dynamic)

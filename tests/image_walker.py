@@ -21,7 +21,7 @@ def parse(image: bytes) -> dict:
             "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core",
             "n_tails", "n_tail_bytes", "off_tail_bits", "off_tail_rank", "off_tails", "off_tail_bytes",
             "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full", "off_kset", "kset_log2", "kset_empty", "off_pair",
-            "off_entry8", "entry8_log2", "entry8_pad"]
+            "off_entry", "entry_log2", "entry_pad"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
@@ -44,14 +44,14 @@ def parse(image: bytes) -> dict:
     h["pair"] = buf[h["off_pair"]:h["off_pair"] + 8192].view(np.uint32).reshape(256, 8)
     if h["off_kset"]:
         h["kset"] = buf[h["off_kset"]:h["off_kset"] + (4 << h["kset_log2"])].view(np.uint32)
-    if h["off_entry8"]:
-        h["entry8"] = buf[h["off_entry8"]:h["off_entry8"] + (16 << h["entry8_log2"])].view(np.uint32).reshape(-1, 4)
+    if h["off_entry"]:
+        h["entry"] = buf[h["off_entry"]:h["off_entry"] + (16 << h["entry_log2"])].view(np.uint32).reshape(-1, 4)
     return h
 
 
-def entry8_find(h, x0, x1):
+def entry_find(h, x0, x1):
     """Depth-8 entry table probe (image.h): (node, depth) or None."""
-    t, lg = h["entry8"], h["entry8_log2"]
+    t, lg = h["entry"], h["entry_log2"]
     i = ((x0 * 0x9E3779B1 + x1 * 0x85EBCA6B) & 0xFFFFFFFF) >> (32 - lg)
     while int(t[i][2]) != 0xFFFFFFFF:
         if int(t[i][0]) == x0 and int(t[i][1]) == x1:
@@ -197,8 +197,12 @@ def match(h, text: bytes, readable=None, n_starts=None):
             continue
         if h["off_kset"] and not kset_has(h, key):  # the exact key set (image.h)
             continue
-        if h["off_entry8"]:  # kind 4: enter through the depth-8 entry table
-            en = entry8_find(h, key & 0xFFFFFFFF, key >> 32)
+        if h["off_entry"]:  # kinds 4 and 3: enter through the entry table (image.h)
+            if h["filter_kind"] == 3:
+                ok = all(b in b"ACGT" for b in bytes(text[i:i + d]))  # the key aliases other bytes
+                en = entry_find(h, key, 0) if ok else None
+            else:
+                en = entry_find(h, key & 0xFFFFFFFF, key >> 32)
             ti = walk(h, text, i, L, *en) if en else None
         else:
             ti = walk(h, text, i, L)

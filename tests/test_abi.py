@@ -111,31 +111,37 @@ def test_pair_table(cid):
         assert [int(x) for x in h["pair"][b0]] == want, b0
 
 
-def test_entry8_table():
-    """Kind 4 (C3): one entry per distinct 8-byte pattern prefix; entering the
-    walk at the entry's (node, depth) gives the root walk's result for every
-    pattern, the entry node is the root walk's node after `depth` bytes, and
-    8-byte strings that begin no pattern are absent."""
-    ps = gen.patterns(3).to_list()
+@pytest.mark.parametrize("cid", [3, 5])
+def test_entry_table(cid):
+    """Kinds 4 (C3: 8-byte prefixes) and 3 (C5: 16-base DNA keys): one entry
+    per distinct D-byte pattern prefix; entering the walk at the entry's
+    (node, depth) gives the root walk's result for every pattern, the entry
+    node is the root walk's node after `depth` bytes, and keys that begin no
+    pattern are absent."""
+    ps = gen.patterns(cid).to_list()
     h = image_walker.parse(pf.Trie(ps).image())
-    assert h["filter_kind"] == 4 and h["off_entry8"]
-    prefixes = {p[:8] for p in ps}
-    assert int((h["entry8"][:, 2] != 0xFFFFFFFF).sum()) == len(prefixes)
+    D = h["filter_gram"]
+    assert (h["filter_kind"], D) in [(4, 8), (3, 16)] and h["off_entry"] and not h["off_kset"]
+
+    def key(x):
+        if h["filter_kind"] == 3:
+            return image_walker.dna_key(x[:D]), 0
+        return int.from_bytes(x[:4], "little"), int.from_bytes(x[4:8], "little")
+    prefixes = {p[:D] for p in ps}
+    assert int((h["entry"][:, 2] != 0xFFFFFFFF).sum()) == len(prefixes)
     rng = np.random.default_rng(3)
     for k in rng.choice(len(ps), 1500, replace=False):
         p = ps[int(k)]
-        en = image_walker.entry8_find(h, int.from_bytes(p[:4], "little"), int.from_bytes(p[4:8], "little"))
-        assert en is not None and 1 <= en[1] <= 8
+        en = image_walker.entry_find(h, *key(p))
+        assert en is not None and 1 <= en[1] <= D
         full = image_walker.walk(h, p, 0, len(p))
         assert full is not None and image_walker.walk(h, p, 0, len(p), *en) == full
-        # the entry node is on the path: the root walk over the first `depth`
-        # bytes of p (a prefix of length en[1] need not be a pattern, so walk
-        # p itself truncated there and compare the node reached)
         assert _node_after(h, p, en[1]) == en[0]
+    alpha = np.frombuffer(b"ACGT", np.uint8) if cid == 5 else np.arange(256, dtype=np.uint8)
     for _ in range(2000):
-        x = rng.integers(0, 256, 8).astype(np.uint8).tobytes()
+        x = rng.choice(alpha, D).astype(np.uint8).tobytes()
         if x not in prefixes:
-            assert image_walker.entry8_find(h, int.from_bytes(x[:4], "little"), int.from_bytes(x[4:], "little")) is None
+            assert image_walker.entry_find(h, *key(x)) is None
 
 
 def _node_after(h, text, d):
