@@ -293,10 +293,10 @@ __device__ __forceinline__ uint32_t term_index(const uint32_t *term_node, uint32
 // with `last`.  *nv = kNone when the walk ends (the result is returned).
 template <class Text>
 __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t v, uint32_t j,
-                                         uint32_t last, uint32_t &nv, uint32_t &len) {
+                                         uint32_t last, uint32_t &nv, uint32_t &len, uint32_t ax) {
     nv = kNone;
     const bool hot = v < a.hot_nodes;  // hot records + bytes are in shared memory
-    const uint32_t idx = aux_word(a, s, v);  // the record's index (= rank among the record nodes)
+    const uint32_t idx = ax;  // aux word: the record's index (= rank among the record nodes)
     const uint4 rec = hot ? s.tails[idx] : __ldg(a.t.tails + idx);
     if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(last);
     const uint32_t *pw = reinterpret_cast<const uint32_t *>((hot ? s.tail_bytes : a.t.tail_bytes) + rec.x);
@@ -315,7 +315,7 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
 // Child of node v (node word w) through byte c, or kNone: level-1 nodes by
 // their bitmap (Fig. 3), deeper nodes by their CSR labels.
 __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, uint32_t v, uint32_t w, uint32_t c,
-                                     bool l1) {
+                                     bool l1, uint32_t wn, uint32_t ax) {
     uint32_t nv = kNone;
     if (l1) {  // level 1 -> 2 through the bitmap
         const uint32_t *bm = s.bm + (v - 1) * 10;
@@ -325,11 +325,11 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
         nv = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
     } else {
         const uint32_t lo0 = w & kEdgeMask;
-        const uint32_t hi0 = node_word(a, s, v + 1) & kEdgeMask;
+        const uint32_t hi0 = wn & kEdgeMask;  // node word v+1 (loaded with w)
         const uint32_t deg = hi0 - lo0;
         if (deg <= 4) {  // the labels are packed in the node's aux word (loaded beside the node words)
             if (deg != 0) {
-                const uint32_t x = (aux_word(a, s, v) ^ (c * 0x01010101u)) | (0xFFFFFFFFu << (8 * deg - 1) << 1);
+                const uint32_t x = (ax ^ (c * 0x01010101u)) | (0xFFFFFFFFu << (8 * deg - 1) << 1);
                 const uint32_t f = (x - 0x01010101u) & ~x & 0x80808080u;
                 if (f) nv = lo0 + ((__ffs(f) - 1) >> 3) + 1;  // the child through edge e is node e+1
             }
@@ -386,7 +386,9 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
     // first d0 bytes spell (the depth-8 entry table); else from the root
     uint32_t v = v0 ? v0 : s.root[tx.at(r0)];
     if (v == 0) return kNone;
-    uint32_t w = node_word(a, s, v);
+    // the node's word, the next node's word (its edge end) and its aux word
+    // are loaded together: no load waits on the branch on the first
+    uint32_t w = node_word(a, s, v), wn = node_word(a, s, v + 1), ax = aux_word(a, s, v);
     uint32_t last = (w & kTermBit) ? v : kNone;
     uint32_t j = r0 + d0;
     bool l1 = d0 == 1;  // v is a level-1 node: the next step uses its bitmap
@@ -394,18 +396,20 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
         uint32_t nv = kNone;
         if (w & kTailBit) {
             uint32_t len = 0;
-            const uint32_t r = jump(a, s, tx, v, j, last, nv, len);
+            const uint32_t r = jump(a, s, tx, v, j, last, nv, len, ax);
             if (nv == kNone) return r;
             j += len;
         } else {
             const uint32_t c = tx.at(j);
-            nv = child_of(a, s, v, w, c, l1);
+            nv = child_of(a, s, v, w, c, l1, wn, ax);
             if (nv == kNone) break;  // mismatch: the thread terminates
             ++j;
         }
         l1 = false;
         v = nv;
         w = node_word(a, s, v);
+        wn = node_word(a, s, v + 1);
+        ax = aux_word(a, s, v);
         if (w & kTermBit) last = v;
     }
     return term_of(last);
