@@ -265,6 +265,28 @@ def test_dna_filter_other_bytes():
     assert_same(gpu_rows(t, text), want, "C5 text with non-ACGT bytes")
 
 
+def test_dna_small_set_aliasing():
+    """Kind 3 with a trie small enough for shared memory: 200 k-mers (16-24
+    bases); the text plants them, plants copies whose bytes are aliases of
+    A/C/G/T in the 2-bit code (lowercase: same key, no match), and sprinkles
+    N.  The entry table may be entered only when the 16 bytes are A/C/G/T."""
+    rng = np.random.default_rng(77)
+    acgt = np.frombuffer(b"ACGT", np.uint8)
+    ps = [rng.choice(acgt, int(rng.integers(16, 25))).tobytes() for _ in range(200)]
+    text = rng.choice(acgt, 3 << 20).astype(np.uint8)
+    for k in range(4000):
+        p = ps[k % len(ps)]
+        o = int(rng.integers(0, len(text) - 32))
+        text[o:o + len(p)] = np.frombuffer(p.lower() if k % 3 == 0 else p, np.uint8)
+    text[rng.choice(len(text), 20000, replace=False)] = ord("N")
+    t = pf.Trie(ps)
+    assert t.stats()["filter_gram"] == 16
+    want = oracle.Trie(ps).match(text)
+    assert len(want[0]) > 1000
+    assert_same(gpu_rows(t, text), want, "small DNA set, aliasing bytes")
+    assert_same(gpu_rows(t, text, offset=7), want, "small DNA set, unaligned")
+
+
 def test_full_c2_exact():
     ps = gen.patterns(2)
     n = gen.config(2)["text_len"]
