@@ -451,6 +451,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         } else if (kind == 1) {
             const uint32_t b = filter4_block(x, log2_bits);
             filter[2 * b] |= 1u << filter4_bit_lo(x);
+            filter[2 * b] |= 1u << filter4_bit_mid(x);
             filter[2 * b + 1] |= 1u << filter4_bit_hi(x);
         } else {
             uint32_t h = filter_index(x, log2_bits, exact);

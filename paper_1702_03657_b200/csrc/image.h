@@ -61,10 +61,11 @@
 //                       kind 1 (d = 4): a blocked two-bit filter.  Block
 //                         (64 bits = words 2b, 2b+1) b = top (F-6) bits of
 //                         x * (kFilterMul << 8) (a hash of bytes 0..2); the
-//                         key sets bit 31-(byte3 & 31) of word 2b and bit
+//                         key sets bits 31-(byte3 & 31) and 31-(h2 & 31) of
+//                         word 2b, h2 = hi32(x * kFilterMul2), and bit
 //                         31-(byte2 & 31) of word 2b+1 (bit-reversed so the
 //                         kernel tests each with one rotate; scan.cu stage 1).
-//                         A start passes iff both bits are set.
+//                         A start passes iff the three bits are set.
 //                       kind 2 (d = 4, small sets): the pair filter.  Starts k
 //                         and k+1 share bytes k+1..k+3, so one 32-bit word
 //                         b = filter_pair_word(bytes k+1..k+3) answers both:
@@ -124,7 +125,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 13;
+constexpr uint32_t kVersion = 14;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -198,5 +199,8 @@ PFAC_HD inline uint32_t dna_bit_hi(uint32_t key) {
 }
 PFAC_HD inline uint32_t filter4_bit_lo(uint32_t x) { return 31u - ((x >> 24) & 31u); }
 PFAC_HD inline uint32_t filter4_bit_hi(uint32_t x) { return 31u - ((x >> 16) & 31u); }
+PFAC_HD inline uint32_t filter4_bit_mid(uint32_t x) {
+    return 31u - (uint32_t)(((uint64_t)x * kFilterMul2) >> 32 & 31u);
+}
 
 }  // namespace pfac

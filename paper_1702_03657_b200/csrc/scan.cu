@@ -529,7 +529,9 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
             const uint32_t blk = __umulhi(x[k] * kMul, sWmul);
             const uint2 w2 = lds64_abs(blk * stride + base_lane);
             // rotate by byte k+3 / byte k+2 (funnel amounts are mod 32): tested bits -> 31
-            const uint32_t r = __funnelshift_l(w2.x, w2.x, x[k + 3]) & __funnelshift_l(w2.y, w2.y, x[k + 2]);
+            // and by hi32(x * M2) (a third bit in word 2b)
+            const uint32_t r = __funnelshift_l(w2.x, w2.x, x[k + 3]) & __funnelshift_l(w2.y, w2.y, x[k + 2]) &
+                               __funnelshift_l(w2.x, w2.x, __umulhi(x[k], kFilterMul2));
             acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);  // acc << 1 | bit
         }
         surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);

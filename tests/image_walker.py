@@ -72,7 +72,8 @@ def filter_bits(h, key):
         raise ValueError("kind 2 tests depend on the start's parity; use filter_pass")
     if h["filter_kind"] == 1:  # d = 4: blocked two-bit filter (image.h)
         b = ((key * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
-        return [2 * b * 32 + (31 - ((key >> 24) & 31)), (2 * b + 1) * 32 + (31 - ((key >> 16) & 31))]
+        h2 = ((key * 0x85EBCA6B) >> 32) & 31
+        return [2 * b * 32 + (31 - ((key >> 24) & 31)), 2 * b * 32 + (31 - h2), (2 * b + 1) * 32 + (31 - ((key >> 16) & 31))]
     return [filter_index(h, key)]
 
 
