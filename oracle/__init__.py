@@ -79,7 +79,8 @@ class Trie:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        # at interpreter exit the module globals (_lib) may already be gone
+        if getattr(self, "_h", None) and _lib is not None:
             _lib().or_free(self._h)
             self._h = None
 
