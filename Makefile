@@ -44,41 +44,12 @@ clean:
 
 .PHONY: all clean
 
-# A/B variants of the production build (tools/ab.py)
-ABLIBS := $(PKG)/libpfac_nosw.so $(PKG)/libpfac_d64.so $(PKG)/libpfac_w24.so $(PKG)/libpfac_w16.so
-$(PKG)/libpfac_nosw.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_NO_SWIZZLE -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_d64.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=64 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_w24.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=24 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_w16.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=16 -shared -o $@ $(CSRC) -lcudart
-ab: $(ABLIBS)
-$(PKG)/libpfac_s2l.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_s2l_nosw.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_STAGE2_INLANE -DPFAC_NO_SWIZZLE -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_d32.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=32 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_hot200.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_HOTCAP=200000 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_hot8.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_HOTCAP=8192 -shared -o $@ $(CSRC) -lcudart
-
 # KB0 read-stream probe (bench.py reports its bandwidth next to the scan)
 tools/probe/libkb0.so: tools/probe/kb0.cu
 	$(NVCC) $(NVFLAGS) -shared -o $@ $< -lcudart
-$(PKG)/libpfac_w28.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=28 -shared -o $@ $(CSRC) -lcudart
-$(PKG)/libpfac_w30.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_WARPS=30 -shared -o $@ $(CSRC) -lcudart
-
 # latency / launch-overhead probes (tools/probe; measurement only)
 probes: tools/probe/lat_probe tools/probe/launch_probe
 tools/probe/lat_probe: tools/probe/lat_probe.cu
 	$(NVCC) -O2 $(ARCH) -o $@ $<
 tools/probe/launch_probe: tools/probe/launch_probe.cu
 	$(NVCC) -O2 $(ARCH) -o $@ $<
-$(PKG)/libpfac_d96.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -DPFAC_DEFER=96 -shared -o $@ $(CSRC) -lcudart

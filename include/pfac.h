@@ -40,7 +40,9 @@ typedef struct CUstream_st *pfac_stream; /* == cudaStream_t; NULL = legacy defau
 typedef enum {
     PFAC_OK = 0,
     PFAC_ERR_INVALID_ARG = 1,  /* NULL pointer, n_patterns == 0, zero-length pattern, length > 65535, bad enum, bad image */
-    PFAC_ERR_LIMIT = 2,        /* trie exceeds 2^30-1 nodes or 2^32-2 pattern-id-list entries */
+    PFAC_ERR_LIMIT = 2,        /* trie exceeds 2^30-1 nodes, or the per-terminal pattern-id lists
+                                  (each terminal lists the ids ending on its root path) exceed
+                                  2^28 entries (e.g. tens of thousands of nested patterns) */
     PFAC_ERR_NOMEM = 3,        /* host or device allocation failed */
     PFAC_ERR_CUDA = 4,         /* no usable device / CUDA runtime error (detail in pfac_last_error) */
     PFAC_ERR_CAPACITY = 5      /* (pfac_match only, never device path) internal retry failed */
@@ -66,6 +68,68 @@ typedef struct {
     uint32_t image_nodes; /* nodes stored in the device image after path compression of single-path tails */
 } pfac_stats;
 
+/* Build options (pfac_build_ex).  NULL means "all defaults"; initialise a
+ * struct with pfac_build_options_init() and change the fields you need.
+ * These select experiments and ablations (tools/, tests/); the default build
+ * is the product configuration. */
+typedef struct {
+    uint32_t struct_bytes;       /* sizeof(pfac_build_options); INVALID_ARG if smaller than the
+                                    library's version of the struct */
+    int32_t filter_kind;         /* -1: automatic.  0..4 force a first-stage filter kind (image.h);
+                                    INVALID_ARG if the pattern set does not admit it (e.g. kind 3
+                                    needs an all-A/C/G/T set with shortest >= 16) */
+    uint32_t pair_bits_per_key;  /* kind 2 sizing: filter bits per distinct 4-gram (0: 512) */
+    uint32_t gram8_bits_per_key; /* kind 4 sizing: filter bits per distinct 8-byte prefix (0: 32) */
+    uint32_t truncate_depth;     /* 0: untruncated trie (default).  d >= 1: PAPER.md:80 step III,
+                                    the trie is cut at level d; a start that reaches a depth-d
+                                    node is verified on the device against the full bytes of
+                                    the patterns below it (exact results either way) */
+    uint32_t reserved[7];        /* must be 0 */
+} pfac_build_options;
+
+/* Shared-memory placement of the trie for one scan (the analog of the paper's
+ * Fig. 6 global vs texture + shared-memory study). */
+typedef enum {
+    PFAC_PLACE_AUTO = 0,    /* planner's choice (below) */
+    PFAC_PLACE_GLOBAL = 1,  /* no trie level staged: root table + level-1 bitmaps only, the rest via L1/L2 */
+    PFAC_PLACE_SMEM = 2,    /* the whole trie, else its BFS prefix (upper levels), in shared memory */
+    PFAC_PLACE_BIG_L1 = 3   /* no trie level staged, 2-slot text ring, one filter copy: the
+                               largest L1 carve-out for the nodes the walks visit */
+} pfac_placement;
+
+/* Scan-plan options (pfac_match_device_ex, pfac_plan_query).  NULL = the
+ * automatic plan; initialise with pfac_plan_options_init() (every field
+ * automatic) and change the fields you need.  -1 in a signed field =
+ * automatic. */
+typedef struct {
+    uint32_t struct_bytes;        /* sizeof(pfac_plan_options) */
+    uint32_t placement;           /* pfac_placement */
+    uint32_t hot_bytes_cap;       /* cap on the staged trie bytes (0: none) */
+    int32_t max_filter_rep_log2;  /* cap on filter copies in shared memory (2^x), -1 auto */
+    int32_t ring_slots;           /* text ring slots per warp: 2, 3, or -1 auto */
+    int32_t ctg64;                /* share of a CTA's rounds in per-warp blocks, in 64ths (0..64) */
+    int32_t pool64;               /* share of all rounds in the cross-CTA pool, in 64ths (0..32) */
+    int32_t stage2;               /* 2-gram prefix test of filter survivors: 0 off, 1 on */
+    int32_t entry;                /* entry table (walks enter below the top levels): 0 off, 1 on */
+    uint32_t l2_persist;          /* 1: the device image is given as an L2 persisting access-policy
+                                     window for this launch (sets the device's persisting-L2 limit
+                                     to min(image, 64 MiB) on first use) */
+    uint32_t reserved[6];         /* must be 0 */
+} pfac_plan_options;
+
+/* Fill *o with the defaults (struct_bytes set, every choice automatic). */
+void pfac_build_options_init(pfac_build_options *o);
+void pfac_plan_options_init(pfac_plan_options *o);
+
+/* What the planner chose for a scan (pfac_plan_query). */
+typedef struct {
+    uint32_t filter_kind, ring_slots, filter_copies, smem_bytes;
+    uint32_t hot_nodes, image_nodes, hot_edges, terms_in_smem;
+    uint32_t grid, warps_per_cta, hit_cap, stage2;
+    uint32_t entry, kset, pool_rounds, placement;
+    uint64_t rounds_per_cta, main_rounds;
+} pfac_plan_info;
+
 /* Host-side result of pfac_match: library-allocated, free with pfac_matches_free.
  * count == 0 => pos == pid == NULL. */
 typedef struct {
@@ -86,6 +150,13 @@ pfac_status pfac_build(const uint8_t *const *patterns, const uint32_t *lengths, 
 /* Same, patterns concatenated in `data` (offset of k = sum of lengths[0..k)). */
 pfac_status pfac_build_concat(const uint8_t *data, const uint32_t *lengths, uint32_t n_patterns,
                               pfac_trie **out);
+
+/* pfac_build_concat with build options (NULL = defaults, identical to
+ * pfac_build_concat).  PAPER.md:80 steps I-III (truncate_depth).  Extra
+ * errors: INVALID_ARG for a bad struct_bytes, a non-zero reserved field or a
+ * filter kind the set does not admit. */
+pfac_status pfac_build_ex(const uint8_t *data, const uint32_t *lengths, uint32_t n_patterns,
+                          const pfac_build_options *opt, pfac_trie **out);
 
 /* Frees the host image and every device copy.  NULL-safe. */
 void pfac_free(pfac_trie *t);
@@ -131,16 +202,33 @@ pfac_status pfac_workspace_bytes(const pfac_trie *t, uint64_t n_starts, uint64_t
  *             nothing past capacity is written: re-run with larger buffers.
  *   d_workspace: >= pfac_workspace_bytes(t, n_starts) bytes, 256-B aligned,
  *             ZERO-FILLED BEFORE ITS FIRST USE; the kernels leave it ready for
- *             the next call.  One workspace must not be used by two calls
- *             that can run concurrently.
- * No host synchronisation inside; kernel faults surface at the caller's next
- * sync.  Launch errors return PFAC_ERR_CUDA.  The device copy of the trie is
- * uploaded on first use per device (synchronously, once). */
+ *             the next call (its grid barrier resets itself in device memory,
+ *             so the call may be captured in a CUDA graph and replayed).  One
+ *             workspace must not be used by two calls that can run
+ *             concurrently.
+ * `device` must be the calling thread's current CUDA device (INVALID_ARG
+ * otherwise).  No host synchronisation inside; kernel faults surface at the
+ * caller's next sync.  Launch errors return PFAC_ERR_CUDA.  The device copy of
+ * the trie is uploaded on first use per device (synchronously, once). */
 pfac_status pfac_match_device(const pfac_trie *t, int device, const uint8_t *d_text,
                               uint64_t readable_len, uint64_t n_starts, uint64_t pos_base,
                               uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
                               uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
                               pfac_stream stream);
+
+/* pfac_match_device with a scan plan (NULL = automatic, identical to
+ * pfac_match_device).  Results do not depend on the plan; only speed does.
+ * INVALID_ARG for a bad struct_bytes, a non-zero reserved field or an
+ * out-of-range value; LIMIT if the requested plan does not fit shared memory. */
+pfac_status pfac_match_device_ex(const pfac_trie *t, int device, const uint8_t *d_text,
+                                 uint64_t readable_len, uint64_t n_starts, uint64_t pos_base,
+                                 uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+                                 uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
+                                 const pfac_plan_options *opt, pfac_stream stream);
+
+/* The plan a scan of n_starts starts on `device` would use (no launch). */
+pfac_status pfac_plan_query(const pfac_trie *t, int device, uint64_t n_starts,
+                            const pfac_plan_options *opt, pfac_plan_info *out);
 
 /* Number of kernel launches one pfac_match_device call makes (for the bench's
  * gpu_launches count). */

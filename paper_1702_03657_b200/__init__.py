@@ -19,7 +19,8 @@ import os
 
 import numpy as np
 
-__all__ = ["Trie", "Scanner", "PfacError", "BYTES_KINDS", "lib_path", "launches_per_call"]
+__all__ = ["Trie", "Scanner", "PfacError", "BYTES_KINDS", "lib_path", "launches_per_call", "build_options",
+           "plan_options", "PLACEMENTS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.environ.get("PFAC_LIB") or os.path.join(_HERE, "libpfac.so")  # PFAC_LIB: instrumented build
@@ -46,6 +47,46 @@ class _Matches(C.Structure):
     _fields_ = [("count", C.c_uint64), ("pos", C.POINTER(C.c_uint64)), ("pid", C.POINTER(C.c_uint32))]
 
 
+class BuildOptions(C.Structure):
+    """pfac_build_options (include/pfac.h); fields set from keyword arguments."""
+    _fields_ = [("struct_bytes", C.c_uint32), ("filter_kind", C.c_int32), ("pair_bits_per_key", C.c_uint32),
+                ("gram8_bits_per_key", C.c_uint32), ("truncate_depth", C.c_uint32), ("reserved", C.c_uint32 * 7)]
+
+
+class PlanOptions(C.Structure):
+    """pfac_plan_options (include/pfac.h); fields set from keyword arguments."""
+    _fields_ = [("struct_bytes", C.c_uint32), ("placement", C.c_uint32), ("hot_bytes_cap", C.c_uint32),
+                ("max_filter_rep_log2", C.c_int32), ("ring_slots", C.c_int32), ("ctg64", C.c_int32),
+                ("pool64", C.c_int32), ("stage2", C.c_int32), ("entry", C.c_int32), ("l2_persist", C.c_uint32),
+                ("reserved", C.c_uint32 * 6)]
+
+
+class _PlanInfo(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in (
+        "filter_kind", "ring_slots", "filter_copies", "smem_bytes", "hot_nodes", "image_nodes", "hot_edges",
+        "terms_in_smem", "grid", "warps_per_cta", "hit_cap", "stage2", "entry", "kset", "pool_rounds",
+        "placement")] + [("rounds_per_cta", C.c_uint64), ("main_rounds", C.c_uint64)]
+
+
+PLACEMENTS = {"auto": 0, "global": 1, "smem": 2, "big_l1": 3}
+
+
+def build_options(**kw) -> BuildOptions:
+    o = BuildOptions()
+    _lib().pfac_build_options_init(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, int(v))
+    return o
+
+
+def plan_options(**kw) -> PlanOptions:
+    o = PlanOptions()
+    _lib().pfac_plan_options_init(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, PLACEMENTS[v] if k == "placement" and isinstance(v, str) else int(v))
+    return o
+
+
 @functools.lru_cache(None)
 def _lib():
     if not os.path.exists(lib_path):
@@ -65,6 +106,13 @@ def _lib():
     L.pfac_matches_free.restype = None
     L.pfac_workspace_bytes.argtypes = [vp, u64, C.POINTER(u64)]
     L.pfac_match_device.argtypes = [vp, C.c_int, vp, u64, u64, u64, vp, vp, u64, vp, vp, u64, vp]
+    L.pfac_match_device_ex.argtypes = [vp, C.c_int, vp, u64, u64, u64, vp, vp, u64, vp, vp, u64, vp, vp]
+    L.pfac_build_ex.argtypes = [vp, vp, u32, vp, C.POINTER(vp)]
+    L.pfac_build_options_init.argtypes = [vp]
+    L.pfac_build_options_init.restype = None
+    L.pfac_plan_options_init.argtypes = [vp]
+    L.pfac_plan_options_init.restype = None
+    L.pfac_plan_query.argtypes = [vp, C.c_int, u64, vp, vp]
     L.pfac_launches_per_call.restype = u32
     L.pfac_status_string.restype = C.c_char_p
     L.pfac_last_error.restype = C.c_char_p
@@ -92,14 +140,20 @@ def _concat(patterns):
 class Trie:
     """Handle over ``pfac_trie`` (immutable; thread-safe for concurrent matches)."""
 
-    def __init__(self, patterns=None, *, _handle=None):
+    def __init__(self, patterns=None, *, _handle=None, **build_kw):
+        """build_kw: pfac_build_options fields (filter_kind, pair_bits_per_key,
+        gram8_bits_per_key, truncate_depth); none = pfac_build_concat defaults."""
         if _handle is not None:
             self._h = _handle
             return
         data, lens = _concat(patterns if patterns is not None else [])
         h = C.c_void_p()
-        st = _lib().pfac_build_concat(data.ctypes.data if data.size else None,
-                                      lens.ctypes.data if lens.size else None, int(lens.size), C.byref(h))
+        dp, lp = (data.ctypes.data if data.size else None), (lens.ctypes.data if lens.size else None)
+        if build_kw:
+            o = build_options(**build_kw)
+            st = _lib().pfac_build_ex(dp, lp, int(lens.size), C.byref(o), C.byref(h))
+        else:
+            st = _lib().pfac_build_concat(dp, lp, int(lens.size), C.byref(h))
         _check(st, "pfac_build")
         self._h = h
 
@@ -142,6 +196,13 @@ class Trie:
         _check(_lib().pfac_image(self._h, C.byref(p), C.byref(n)), "pfac_image")
         return C.string_at(p, n.value)
 
+    def plan(self, n_starts: int, device: int = 0, **plan_kw) -> dict:
+        """pfac_plan_query: the plan a scan of n_starts starts would use."""
+        o = plan_options(**plan_kw)
+        info = _PlanInfo()
+        _check(_lib().pfac_plan_query(self._h, device, n_starts, C.byref(o), C.byref(info)), "pfac_plan_query")
+        return {f: getattr(info, f) for f, _ in _PlanInfo._fields_}
+
     def workspace_bytes(self, n_starts: int) -> int:
         v = C.c_uint64()
         _check(_lib().pfac_workspace_bytes(self._h, n_starts, C.byref(v)), "pfac_workspace_bytes")
@@ -162,8 +223,9 @@ class Trie:
 
     # ------------------------------------------------------- device match
     def match_device(self, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
-                     d_ws, ws_bytes, stream=None, device=None):
-        """Raw pfac_match_device on torch tensors / raw pointers (stream-ordered)."""
+                     d_ws, ws_bytes, stream=None, device=None, plan=None):
+        """Raw pfac_match_device(_ex) on torch tensors / raw pointers (stream-ordered).
+        `plan`: a PlanOptions (None = automatic)."""
         import torch
         ptr = (lambda x: x if isinstance(x, int) or x is None else x.data_ptr())
         if device is None:
@@ -172,33 +234,41 @@ class Trie:
             stream = torch.cuda.current_stream(device).cuda_stream
         elif hasattr(stream, "cuda_stream"):
             stream = stream.cuda_stream
-        st = _lib().pfac_match_device(self._h, device, ptr(d_text), readable_len, n_starts, pos_base,
-                                      ptr(d_pos), ptr(d_pid), capacity, ptr(d_count), ptr(d_ws), ws_bytes,
-                                      stream)
+        with torch.cuda.device(device):  # the ABI requires `device` to be current
+            st = _lib().pfac_match_device_ex(self._h, device, ptr(d_text), readable_len, n_starts, pos_base,
+                                             ptr(d_pos), ptr(d_pid), capacity, ptr(d_count), ptr(d_ws), ws_bytes,
+                                             C.byref(plan) if plan is not None else None, stream)
         _check(st, "pfac_match_device")
 
-    def match(self, text, readable_len=None, n_starts=None, pos_base=0, capacity=None):
+    def match(self, text, readable_len=None, n_starts=None, pos_base=0, capacity=None, **plan_kw):
         """Scan a CUDA uint8 tensor; returns (pos int64, pid int32) CUDA tensors sorted by (pos, pid).
-        Count-and-retry when the match count exceeds the first capacity guess."""
-        return Scanner(self, text.device).match(text, readable_len, n_starts, pos_base, capacity)
+        Count-and-retry when the match count exceeds the first capacity guess.
+        plan_kw: pfac_plan_options fields (placement=..., stage2=0, ...)."""
+        return Scanner(self, text.device, **plan_kw).match(text, readable_len, n_starts, pos_base, capacity)
 
 
 class Scanner:
     """Reusable device state for repeated scans on one device: zero-initialised
     workspace, output buffers and a device count (what bench.py times)."""
 
-    def __init__(self, trie: Trie, device, capacity: int = 1 << 16):
+    def __init__(self, trie: Trie, device, capacity: int = 1 << 16, **plan_kw):
         import torch
         self.torch = torch
         self.trie = trie
         self.device = torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.plan = plan_options(**plan_kw) if plan_kw else None
         self.ws = None
         self.ws_bytes = 0
-        self.count = torch.zeros(1, dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            self.count = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.cap = 0
         self._ensure_out(capacity)
 
     def _ensure_ws(self, n_starts):
+        # allocated and zero-filled on the device's current stream; launch()
+        # orders a foreign stream after it
         need = self.trie.workspace_bytes(max(n_starts, 1))
         if self.ws is None or need > self.ws_bytes:
             self.ws = self.torch.zeros(need, dtype=self.torch.uint8, device=self.device)
@@ -212,13 +282,23 @@ class Scanner:
             self.cap = cap
 
     def launch(self, text, readable_len=None, n_starts=None, pos_base=0, stream=None):
-        """One stream-ordered scan into the preallocated buffers (no sync)."""
-        assert text.dtype == self.torch.uint8 and text.is_cuda and text.is_contiguous()
+        """One stream-ordered scan into the preallocated buffers (no sync).
+        `stream` (default: the device's current stream) is ordered after the
+        current stream's allocation/zero-fill of the buffers, and the buffers
+        are recorded on it so the caching allocator never recycles them early."""
+        torch = self.torch
+        assert text.dtype == torch.uint8 and text.is_cuda and text.is_contiguous()
         L = text.numel() if readable_len is None else int(readable_len)
         ns = L if n_starts is None else int(n_starts)
-        self._ensure_ws(ns)
-        self.trie.match_device(text, L, ns, pos_base, self.pos, self.pid, self.cap, self.count, self.ws,
-                               self.ws_bytes, stream=stream, device=self.device.index)
+        with torch.cuda.device(self.device):
+            cur = torch.cuda.current_stream()
+            self._ensure_ws(ns)
+            if stream is not None and stream != cur:
+                stream.wait_stream(cur)
+                for b in (self.ws, self.pos, self.pid, self.count, text):
+                    b.record_stream(stream)
+            self.trie.match_device(text, L, ns, pos_base, self.pos, self.pid, self.cap, self.count, self.ws,
+                                   self.ws_bytes, stream=stream, device=self.device.index, plan=self.plan)
 
     def match(self, text, readable_len=None, n_starts=None, pos_base=0, capacity=None):
         L = text.numel() if readable_len is None else int(readable_len)

@@ -93,6 +93,41 @@ pfac_status device_image(const pfac_trie *tc, int device, const uint8_t **d_img)
 
 extern "C" {
 
+void pfac_build_options_init(pfac_build_options *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->struct_bytes = sizeof *o;
+    o->filter_kind = -1;
+}
+
+void pfac_plan_options_init(pfac_plan_options *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->struct_bytes = sizeof *o;
+    o->placement = PFAC_PLACE_AUTO;
+    o->max_filter_rep_log2 = -1;
+    o->ring_slots = -1;
+    o->ctg64 = -1;
+    o->pool64 = -1;
+    o->stage2 = -1;
+    o->entry = -1;
+}
+
+static pfac_status build_with(const uint8_t *const *patterns, const uint32_t *lengths, uint32_t n_patterns,
+                              const BuildOpts &bo, pfac_trie **out) {
+    try {
+        std::vector<uint8_t> img;
+        std::string err;
+        int st = build_image(patterns, lengths, n_patterns, bo, img, err);
+        if (st != kStatusOk) return fail(st, err);
+        return finish_handle(std::move(img), out);
+    } catch (const std::bad_alloc &) {
+        return fail(kStatusNomem, "pfac_build: out of host memory");
+    } catch (...) {
+        return fail(kStatusInvalid, "pfac_build: unexpected error");
+    }
+}
+
 pfac_status pfac_build(const uint8_t *const *patterns, const uint32_t *lengths, uint32_t n_patterns,
                        pfac_trie **out) {
     if (!out) return fail(kStatusInvalid, "pfac_build: out is NULL");
@@ -100,7 +135,7 @@ pfac_status pfac_build(const uint8_t *const *patterns, const uint32_t *lengths, 
     try {
         std::vector<uint8_t> img;
         std::string err;
-        int st = build_image(patterns, lengths, n_patterns, img, err);
+        int st = build_image(patterns, lengths, n_patterns, BuildOpts(), img, err);
         if (st != kStatusOk) return fail(st, err);
         return finish_handle(std::move(img), out);
     } catch (const std::bad_alloc &) {
@@ -124,6 +159,34 @@ pfac_status pfac_build_concat(const uint8_t *data, const uint32_t *lengths, uint
         return pfac_build(ptrs.data(), lengths, n_patterns, out);
     } catch (...) {
         return fail(kStatusNomem, "pfac_build_concat: out of host memory");
+    }
+}
+
+pfac_status pfac_build_ex(const uint8_t *data, const uint32_t *lengths, uint32_t n_patterns,
+                          const pfac_build_options *opt, pfac_trie **out) {
+    if (!out) return fail(kStatusInvalid, "pfac_build_ex: out is NULL");
+    *out = nullptr;
+    if (!lengths || n_patterns == 0) return fail(kStatusInvalid, "pfac_build_ex: no patterns");
+    BuildOpts bo;
+    if (opt) {
+        bool ok = opt->struct_bytes >= sizeof(pfac_build_options) && opt->filter_kind >= -1 && opt->filter_kind <= 4;
+        for (uint32_t r : opt->reserved) ok = ok && r == 0;
+        if (!ok) return fail(kStatusInvalid, "pfac_build_ex: bad struct_bytes, filter_kind or reserved field");
+        bo.filter_kind = opt->filter_kind;
+        if (opt->pair_bits_per_key) bo.pair_bits_per_key = opt->pair_bits_per_key;
+        if (opt->gram8_bits_per_key) bo.gram8_bits_per_key = opt->gram8_bits_per_key;
+        bo.truncate_depth = opt->truncate_depth;
+    }
+    try {
+        std::vector<const uint8_t *> ptrs(n_patterns);
+        uint64_t off = 0;
+        for (uint32_t k = 0; k < n_patterns; k++) {
+            ptrs[k] = data ? data + off : nullptr;
+            off += lengths[k];
+        }
+        return build_with(ptrs.data(), lengths, n_patterns, bo, out);
+    } catch (...) {
+        return fail(kStatusNomem, "pfac_build_ex: out of host memory");
     }
 }
 
@@ -229,20 +292,49 @@ pfac_status pfac_workspace_bytes(const pfac_trie *t, uint64_t n_starts, uint64_t
     return PFAC_OK;
 }
 
-pfac_status pfac_match_device(const pfac_trie *t, int device, const uint8_t *d_text, uint64_t readable_len,
-                              uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
-                              uint64_t capacity, uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
-                              pfac_stream stream) {
+pfac_status pfac_match_device_ex(const pfac_trie *t, int device, const uint8_t *d_text, uint64_t readable_len,
+                                 uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                                 uint64_t capacity, uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
+                                 const pfac_plan_options *opt, pfac_stream stream) {
     if (!t || !d_count || (n_starts && !d_text) || (capacity && (!d_pos || !d_pid)))
         return fail(kStatusInvalid, "pfac_match_device: NULL argument");
     if (n_starts > readable_len) return fail(kStatusInvalid, "pfac_match_device: n_starts > readable_len");
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess) return cuda_fail("pfac_match_device: no CUDA device", e);
+    if (cur != device) return fail(kStatusInvalid, "pfac_match_device: `device` is not the current CUDA device");
+    pfac_plan_options defaults;
+    pfac_plan_options_init(&defaults);
     const uint8_t *d_img = nullptr;
     pfac_status s = device_image(t, device, &d_img);
     if (s != PFAC_OK) return s;
     DevTrie dt = make_dev_trie(t->hdr, d_img);
     std::string err;
-    int st = launch_scan(dt, t->image.data(), device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
-                         d_workspace, workspace_bytes, reinterpret_cast<CUstream_st *>(stream), err);
+    int st = launch_scan(dt, t->image.data(), device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity,
+                         d_count, d_workspace, workspace_bytes, opt ? *opt : defaults,
+                         reinterpret_cast<CUstream_st *>(stream), err);
+    if (st != kStatusOk) return fail(st, err);
+    return PFAC_OK;
+}
+
+pfac_status pfac_match_device(const pfac_trie *t, int device, const uint8_t *d_text, uint64_t readable_len,
+                              uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
+                              uint64_t capacity, uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
+                              pfac_stream stream) {
+    return pfac_match_device_ex(t, device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
+                                d_workspace, workspace_bytes, nullptr, stream);
+}
+
+pfac_status pfac_plan_query(const pfac_trie *t, int device, uint64_t n_starts, const pfac_plan_options *opt,
+                            pfac_plan_info *out) {
+    if (!t || !out) return fail(kStatusInvalid, "pfac_plan_query: NULL argument");
+    pfac_plan_options defaults;
+    pfac_plan_options_init(&defaults);
+    // the plan depends on which image sections exist, not on device addresses:
+    // a placeholder base (never dereferenced) keeps present sections non-null
+    DevTrie dt = make_dev_trie(t->hdr, reinterpret_cast<const uint8_t *>(uintptr_t(1) << 40));
+    std::string err;
+    int st = plan_query(dt, t->image.data(), device, n_starts, opt ? *opt : defaults, out, err);
     if (st != kStatusOk) return fail(st, err);
     return PFAC_OK;
 }

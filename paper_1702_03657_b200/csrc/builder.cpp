@@ -36,8 +36,8 @@ inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 
 }  // namespace
 
-int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, std::vector<uint8_t> &image,
-                std::string &err) {
+int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, const BuildOpts &opt,
+                std::vector<uint8_t> &image, std::string &err) {
     if (!pats || !lens || m == 0) {
         err = "pfac_build: NULL argument or n_patterns == 0";
         return kStatusInvalid;
@@ -99,17 +99,20 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         if (terminal) {
             // union list = (ancestor's union) merged with own ids (both ascending)
             std::sort(own.begin(), own.end());
-            std::vector<uint32_t> merged;
-            if (anc != kNone) {
-                merged.assign(out_pid.begin() + out_ptr[anc], out_pid.begin() + out_ptr[anc + 1]);
-            }
-            std::vector<uint32_t> u(merged.size() + own.size());
-            std::merge(merged.begin(), merged.end(), own.begin(), own.end(), u.begin());
-            if ((uint64_t)out_pid.size() + u.size() > 0xFFFFFFFEull) {
-                err = "pfac_build: pattern-id lists exceed 2^32-2 entries";
+            // budget checked before anything is copied: nested pattern sets
+            // grow these lists quadratically
+            const uint64_t n_anc = anc != kNone ? out_ptr[anc + 1] - out_ptr[anc] : 0;
+            if ((uint64_t)out_pid.size() + n_anc + own.size() > kMaxPidEntries) {
+                err = "pfac_build: pattern-id lists exceed 2^28 entries (deeply nested pattern set)";
                 return kStatusLimit;
             }
-            out_pid.insert(out_pid.end(), u.begin(), u.end());
+            const size_t at = out_pid.size();
+            out_pid.resize(at + n_anc + own.size());
+            if (n_anc)  // the ancestor's list (ascending) merged with own ids (ascending)
+                std::merge(out_pid.begin() + out_ptr[anc], out_pid.begin() + out_ptr[anc + 1], own.begin(), own.end(),
+                           out_pid.begin() + at);
+            else
+                std::copy(own.begin(), own.end(), out_pid.begin() + at);
             term_node.push_back(v);
             out_ptr.push_back((uint32_t)out_pid.size());
             anc = (uint32_t)(term_node.size() - 1);
@@ -339,9 +342,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
             const uint8_t c = pats[k][b];
             dna = c == 'A' || c == 'C' || c == 'G' || c == 'T';
         }
-    {
-        const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
-        if (force && force[0] != '3') dna = false;
+    if (opt.filter_kind >= 0 && opt.filter_kind != 3) dna = false;  // a forced kind (tools, tests)
+    if (opt.filter_kind == 3 && !dna) {
+        err = "pfac_build: filter kind 3 needs an all-A/C/G/T pattern set with shortest >= 16";
+        return kStatusInvalid;
     }
     // 8-byte prefixes (kind 4) for big sets whose patterns are all >= 8 bytes:
     // text that shares 4-byte prefixes with many patterns (tokens, protocol
@@ -357,9 +361,22 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         std::sort(k8.begin(), k8.end());
         g8 = (uint64_t)(std::unique(k8.begin(), k8.end()) - k8.begin()) > 2048;
     }
-    {
-        const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
-        if (force && force[0] != '4') g8 = false;
+    if (opt.filter_kind == 4) {
+        if (dna || min_len < kGram8) {
+            err = "pfac_build: filter kind 4 needs shortest pattern >= 8 (and not kind 3)";
+            return kStatusInvalid;
+        }
+        g8 = true;
+    } else if (opt.filter_kind >= 0) {
+        g8 = false;
+    }
+    if ((opt.filter_kind == 1 || opt.filter_kind == 2) && (dna || g8 || min_len < 4)) {
+        err = "pfac_build: filter kinds 1 and 2 need shortest pattern >= 4";
+        return kStatusInvalid;
+    }
+    if (opt.filter_kind == 0 && min_len >= 4) {
+        err = "pfac_build: filter kind 0 is for sets whose shortest pattern is < 4 bytes";
+        return kStatusInvalid;
     }
     const uint32_t gram = dna ? kDnaGram : g8 ? kGram8 : std::min<uint32_t>(4, min_len);
     uint32_t exact = gram <= 2 ? 1u : 0u;
@@ -379,8 +396,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         }
         std::sort(k8.begin(), k8.end());
         const uint64_t distinct = std::unique(k8.begin(), k8.end()) - k8.begin();
-        uint64_t per_key = 32;  // ~32 bits per key, at most 2^20 bits (128 KiB)
-        if (const char *e = std::getenv("PFAC_G8_BITS")) per_key = std::strtoull(e, nullptr, 10);  // experiments
+        const uint64_t per_key = opt.gram8_bits_per_key;  // ~32 bits per key, at most 2^20 bits (128 KiB)
         log2_bits = 10;
         while (log2_bits < 20 && (1ull << log2_bits) < per_key * distinct) log2_bits++;
     } else if (dna) {
@@ -405,9 +421,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
         // per 4-gram (sizing below), for sets of <= 2,048 distinct 4-grams.
         // Else kind 1 (blocked two-bit, ~32 bits per key) or kind 0 (d < 4),
         // capped at 2^20 bits (kind 1, 128 KiB) or 2^19 bits (kind 0).
-        const char *force = std::getenv("PFAC_FILTER_KIND");  // experiments only (tools/)
-        const bool allow2 = !force || force[0] != '1';
-        if (kind == 1 && allow2 && distinct * 128 <= (1ull << 18)) {
+        const bool allow2 = opt.filter_kind != 1;
+        if (kind == 1 && (opt.filter_kind == 2 || (allow2 && distinct * 128 <= (1ull << 18)))) {
             kind = 2;
             log2_bits = 12;
             // 512 filter bits per distinct 4-gram (two set: fill ~0.4%), at
@@ -416,9 +431,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, st
             // copies 51.3, 512 with 1 copy 47.6, 1024 (128 KiB: 2-slot ring,
             // trie no longer whole in shared memory) 51.0: fewer survivors
             // beat fewer bank conflicts.
-            uint64_t per_key = 512;
-            if (const char *e = std::getenv("PFAC_PAIR_BITS"))  // experiments only (tools/)
-                per_key = std::strtoull(e, nullptr, 10);
+            const uint64_t per_key = opt.pair_bits_per_key;
             while ((1ull << log2_bits) < per_key * distinct && log2_bits < 19) log2_bits++;
         } else {
             log2_bits = 10;  // at most 2^20 bits (128 KiB; the kernel then keeps 2 text rounds per warp)
@@ -615,7 +628,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
     const uint64_t N = h.n_nodes, E = h.n_edges, T = h.n_terminals;
     auto in = [&](uint64_t off, uint64_t bytes) { return off >= sizeof(ImageHeader) && off + bytes <= size; };
     const uint64_t off_aux = aux_offset(h.off_node, N);  // image.h: aux follows node
-    bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E) &&
+    bool ok = N >= 2 && E == N - 1 && N <= kEdgeMask && in(h.off_node, 4 * (N + 1)) && in(h.off_label, E + 4) &&
               in(off_aux, 4 * N) && off_aux + 4 * N <= h.off_label && in(h.off_pair, 8192) &&
               (h.off_kset == 0 ? h.kset_log2 == 0
                                : (h.filter_kind == 1 && h.kset_log2 >= 6 &&
@@ -657,6 +670,52 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
         for (uint64_t i = 0; ok && h.off_entry && i < (1ull << h.entry_log2); i++)
             ok = en[4 * i + 2] == kNone || (en[4 * i + 2] > 0 && en[4 * i + 2] < N && en[4 * i + 3] >= 1 &&
                                             en[4 * i + 3] <= h.filter_gram);
+        // contents the kernel dereferences: every index it follows
+        // must stay inside its section
+        // records: 4-byte aligned bytes read a word at a time
+        for (uint64_t i = 0; ok && i < h.n_tails; i++)
+            ok = (tails[4 * i] & 3u) == 0 && (uint64_t)tails[4 * i] + ((tails[4 * i + 1] + 3ull) & ~3ull) <= h.n_tail_bytes;
+        // root table: 0 or a level-1 node
+        const uint32_t *root = reinterpret_cast<const uint32_t *>(p + h.off_root);
+        for (uint32_t c = 0; ok && c < 256; c++) ok = root[c] <= h.n_level1;
+        // level-1 bitmapped nodes: popcount = degree, prefix bytes = running popcounts
+        const uint32_t *l1 = reinterpret_cast<const uint32_t *>(p + h.off_level1);
+        for (uint64_t v = 1; ok && v <= h.n_level1; v++) {
+            const uint32_t *o = l1 + 10 * (v - 1);
+            uint32_t pre = 0;
+            for (int w = 0; ok && w < 8; w++) {
+                ok = ((o[8 + w / 4] >> (8 * (w % 4))) & 0xFFu) == pre;
+                pre += (uint32_t)__builtin_popcount(o[w]);
+            }
+            const bool rec = (node[v] & kTailBit) != 0;
+            ok = ok && (rec || pre == (node[v + 1] & kEdgeMask) - (node[v] & kEdgeMask));
+        }
+        // aux words: a record node's aux is its record index, in node order
+        const uint32_t *aux = reinterpret_cast<const uint32_t *>(p + off_aux);
+        uint64_t rank = 0;
+        for (uint64_t v = 0; ok && v < N; v++)
+            if (node[v] & kTailBit) ok = aux[v] == rank++;
+        ok = ok && rank == h.n_tails;
+        // record bitmap and its rank words (the host planner stages records by rank)
+        const uint32_t *tb = reinterpret_cast<const uint32_t *>(p + h.off_tail_bits);
+        const uint32_t *tr = reinterpret_cast<const uint32_t *>(p + h.off_tail_rank);
+        uint32_t acc = 0;
+        for (uint64_t w = 0; ok && w < (N + 31) / 32; w++) {
+            uint32_t want = 0;
+            for (uint64_t b = 0; b < 32 && 32 * w + b < N; b++) want |= ((node[32 * w + b] >> 30) & 1u) << b;
+            ok = tb[w] == want && tr[w] == acc;
+            acc += (uint32_t)__builtin_popcount(want);
+        }
+        // kept terminals: exactly the nodes with the terminal bit, ascending
+        const uint32_t *tn = reinterpret_cast<const uint32_t *>(p + h.off_term_node);
+        uint64_t k = 0;
+        for (uint64_t v = 0; ok && v < N; v++)
+            if (node[v] & kTermBit) ok = k < h.n_kept_terminals && tn[k++] == v;
+        ok = ok && k == h.n_kept_terminals;
+        // pid lists: monotone offsets, ids < n_patterns
+        for (uint64_t i = 0; ok && i < T; i++) ok = out_ptr[i] <= out_ptr[i + 1];
+        const uint32_t *pid = reinterpret_cast<const uint32_t *>(p + h.off_out_pid);
+        for (uint64_t i = 0; ok && i < h.n_out; i++) ok = pid[i] < h.n_patterns;
     }
     if (!ok) {
         err = "pfac_attach: inconsistent image sections";

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "image.h"
+#include "pfac.h"
 
 struct CUstream_st;
 #include <vector_types.h>
@@ -23,9 +24,18 @@ enum : int {
 };
 
 constexpr uint32_t kMaxPatternLen = 65535;
+constexpr uint64_t kMaxPidEntries = 1ull << 28;  // total length of the per-terminal pid lists
 
-int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, std::vector<uint8_t> &image,
-                std::string &err);
+// Build options (include/pfac.h pfac_build_options, defaults filled in).
+struct BuildOpts {
+    int filter_kind = -1;              // -1 automatic
+    uint32_t pair_bits_per_key = 512;  // kind 2 sizing
+    uint32_t gram8_bits_per_key = 32;  // kind 4 sizing
+    uint32_t truncate_depth = 0;       // 0: untruncated
+};
+
+int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, const BuildOpts &opt,
+                std::vector<uint8_t> &image, std::string &err);
 int validate_image(const uint8_t *p, uint64_t size, std::string &err);
 
 // Device-side view of an uploaded image (pointers into device memory).
@@ -64,10 +74,15 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d_image);
 // before first use).
 int workspace_bytes_for(uint64_t n_starts, int device, uint64_t *out, std::string &err);
 
-// Launches the scan; returns kStatusOk or kStatusCuda (err filled).
-int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const uint8_t *d_text, uint64_t readable_len, uint64_t n_starts,
-                uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity, uint64_t *d_count,
-                void *d_ws, uint64_t ws_bytes, CUstream_st *stream, std::string &err);
+// Launches the scan with plan options `o` (defaults: pfac_plan_options_init);
+// returns kStatusOk or an error status (err filled).
+int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const uint8_t *d_text, uint64_t readable_len,
+                uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+                uint64_t *d_count, void *d_ws, uint64_t ws_bytes, const pfac_plan_options &o, CUstream_st *stream,
+                std::string &err);
+// The plan a scan would use (no launch).
+int plan_query(const DevTrie &t, const uint8_t *host_image, int device, uint64_t n_starts,
+               const pfac_plan_options &o, pfac_plan_info *out, std::string &err);
 
 uint32_t launches_per_call();
 #ifdef PFAC_TIMING

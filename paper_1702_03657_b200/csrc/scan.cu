@@ -36,9 +36,10 @@
 //    re-scans its rounds writing rows directly.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
-#include <map>
+#include <cstring>
 #include <mutex>
 
 #include "internal.h"
@@ -70,20 +71,17 @@ constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated f
 #define PFAC_DEFER 48
 #endif
 constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to walk (kinds 1, 2; see defer_for)
-#ifndef PFAC_HOTCAP
-#define PFAC_HOTCAP 0xFFFFFFFFu
-#endif
-constexpr uint32_t kHotCap = PFAC_HOTCAP;  // cap on hot-trie smem when the trie does not fit
 constexpr uint64_t kSmallTrie = 160u << 10;  // a trie this small fits shared memory whole
 constexpr uint64_t kBigL1Trie = 1u << 20;    // "big L1" plan up to this trie size (see launch_scan)
 
-// Workspace: header (two grid-barrier counters, used alternately so that a
-// launch clears the other one for the next launch) + CTA totals + hit lists.
+// Workspace: header (a self-resetting grid barrier and the pool counter,
+// zero after every launch: no host-side state, so a captured CUDA graph may
+// replay the launch) + CTA totals + hit lists.
 struct WsHeader {
-    unsigned int barrier[2];    // grid barrier after phase 1 (alternating per launch)
-    unsigned int barrier2[2];   // grid barrier after the pool scan
-    unsigned int pool_next[2];  // next pool round
-    unsigned int pad[58];
+    unsigned int bar_count;  // CTAs arrived at the current grid barrier (0 between barriers)
+    unsigned int bar_gen;    // grid-barrier generation (any value; bumped by the last arrival)
+    unsigned int pool_next;  // next pool round (reset after the first grid barrier)
+    unsigned int pad[61];
 };
 static_assert(sizeof(WsHeader) == 256, "");
 // fixed part: header | cta_total[kMaxCtas] u64 | pool_total[kMaxCtas] u64
@@ -104,7 +102,6 @@ struct ScanArgs {
     unsigned long long *cta_total;  // [gridDim.x]
     uint2 *hits;                    // [warps][hit_cap] (start offset within the warp's range, terminal index)
     uint32_t hit_cap;
-    uint32_t parity;                // barrier counter used by this launch
     uint64_t rounds_per_cta;        // of the first n_main rounds (the CTA ranges)
     uint64_t n_main;                // rounds in CTA ranges; rounds [n_main, n_rounds) are the shared pool
     uint32_t pool_seg;              // pool rounds per CTA in the pool's scan (0: no pool)
@@ -200,14 +197,31 @@ __device__ __forceinline__ void stamp(int warp_global, int k) {
 #define STAMP(k)
 #endif
 
-// One barrier across the (co-resident, cooperative-launch) grid.
-__device__ __forceinline__ void grid_barrier(unsigned int *ctr) {
+// One barrier across the (co-resident, cooperative-launch) grid: a
+// generation (sense-reversing) barrier.  The generation is read before
+// arriving (it cannot advance before this CTA arrives); the last CTA to
+// arrive resets the count and then bumps the generation, which the others
+// wait on.  The count is back at 0 after every barrier, so the workspace
+// needs no per-launch host state.
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const unsigned int *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_barrier(WsHeader *ws) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        while (ld_acquire_u32(ctr) < gridDim.x) {
+        const uint32_t gen = ld_relaxed_u32(&ws->bar_gen);
+        __threadfence();  // this CTA's writes before its arrival
+        if (atomicAdd(&ws->bar_count, 1u) == gridDim.x - 1) {
+            ws->bar_count = 0u;
+            __threadfence();  // the reset (and every arrival seen) before the release
+            atomicAdd(&ws->bar_gen, 1u);
+        } else {
+            while (ld_acquire_u32(&ws->bar_gen) == gen) {
+            }
         }
+        __threadfence();
     }
     __syncthreads();
 }
@@ -725,11 +739,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                                                                             // then s_wtot[kWarps + 1])
     if (tid == 32) *s_next = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (blockIdx.x == 0 && tid == 0) {  // for the next launch
-        a.ws->barrier[a.parity ^ 1u] = 0u;
-        a.ws->barrier2[a.parity ^ 1u] = 0u;
-        a.ws->pool_next[a.parity ^ 1u] = 0u;
-    }
     __syncthreads();  // barriers initialised
     STAMP(11);
     Smem s;
@@ -802,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 r = kNoRound;
                 if (kPool && a.pool_seg) {
                     if (lane == 0) {
-                        const uint32_t q = atomicAdd(&a.ws->pool_next[a.parity], 1u);
+                        const uint32_t q = atomicAdd(&a.ws->pool_next, 1u);
                         if (q < (uint32_t)((a.n_starts + kRound - 1) / kRound - a.n_main)) {
                             r = (uint32_t)(a.n_main - cta_round0) + q;
                             a.round_val[cta_round0 + r] = 0ull;  // its count (ordered before the warp's
@@ -1002,7 +1011,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #endif
             // ---- stage 2 in the lane: 2-gram prefix test of each survivor;
             // `pending` becomes the kept set (sparse: appended by ballot)
-            if (Kind != 3 && (Kind != 4 || a.use_pair)) {
+            if (Kind != 3 && a.use_pair) {
                 const uint32_t rl = rid[0] < n_fast ? (uint32_t)kSlotBytes  // readable bytes from rbase
                                                     : (a.readable > rbase ? clamp32(a.readable - rbase) : 0u);
                 uint32_t km = 0;
@@ -1156,7 +1165,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     run = scan_rounds(cta_round0 + n_ctg, n_local - n_ctg, run);  // the dynamic rounds follow the blocks
     if (tid == 0) a.cta_total[blockIdx.x] = run;
     STAMP(7);
-    grid_barrier(&a.ws->barrier[a.parity]);
+    grid_barrier(a.ws);
+    if (blockIdx.x == 0 && tid == 0) a.ws->pool_next = 0u;  // phase 1 is over everywhere: ready for the next launch
     if (warp == 0) {
         unsigned long long pre = 0, all = 0;
         for (uint32_t b = lane; b < gridDim.x; b += 32) {
@@ -1189,7 +1199,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         const uint32_t n = g0 < n_rounds ? (uint32_t)min((uint64_t)a.pool_seg, n_rounds - g0) : 0u;
         const unsigned long long seg_total = scan_rounds(g0, n, 0ull);
         if (tid == 0) a.pool_total[blockIdx.x] = seg_total;
-        grid_barrier(&a.ws->barrier2[a.parity]);
+        grid_barrier(a.ws);
         unsigned long long pool_all;
         const unsigned long long v = (uint32_t)tid < gridDim.x ? __ldcg(a.pool_total + tid) : 0ull;
         const unsigned long long ex = block_excl(v, pool_all);
@@ -1359,12 +1369,13 @@ struct DeviceInfo {
 std::mutex g_dev_mu;
 DeviceInfo g_dev[64];
 
-std::mutex g_ws_mu;
-std::map<const void *, uint32_t> g_ws_parity;  // grid-barrier counter in use next, per workspace
-
 inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 int device_info(int device, DeviceInfo &out, std::string &err) {
+    if (device < 0 || device >= 64) {
+        err = "bad device ordinal";
+        return kStatusInvalid;
+    }
     std::lock_guard<std::mutex> lk(g_dev_mu);
     DeviceInfo &di = g_dev[device];
     if (!di.init) {
@@ -1414,6 +1425,199 @@ Geometry geometry(uint64_t n_starts, int sms) {
     g.off_hits = g.off_owner + ((4 * g.n_rounds + 15) & ~15ull);
     g.ws_bytes = g.off_hits + 8ull * g.warps * g.hit_cap;
     return g;
+}
+
+// The shared-memory plan and launch configuration of one scan.
+struct Plan {
+    ScanArgs a;  // layout and policy fields (the per-call pointers are set by launch_scan)
+    uint32_t slots;
+    size_t smem;
+    Geometry geo;
+    pfac_plan_info info;
+};
+
+int check_plan_options(const pfac_plan_options &o, std::string &err) {
+    bool ok = o.struct_bytes >= sizeof(pfac_plan_options) && o.placement <= PFAC_PLACE_BIG_L1 &&
+              o.max_filter_rep_log2 >= -1 && o.max_filter_rep_log2 <= 5 &&
+              (o.ring_slots == -1 || o.ring_slots == 2 || o.ring_slots == 3) && o.ctg64 >= -1 && o.ctg64 <= 64 &&
+              o.pool64 >= -1 && o.pool64 <= 32 && o.stage2 >= -1 && o.stage2 <= 1 && o.entry >= -1 &&
+              o.entry <= 1 && o.l2_persist <= 1;
+    for (uint32_t r : o.reserved) ok = ok && r == 0;
+    if (!ok) {
+        err = "pfac_plan_options: bad struct_bytes, reserved field or value";
+        return kStatusInvalid;
+    }
+    return kStatusOk;
+}
+
+// Shared-memory plan: filter at offset 0 (replicated while it fits), ring,
+// barriers, queues, root, level-1 bitmaps, warp totals, then the hot trie
+// prefix (BFS order = level order: the upper levels).
+int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di, uint64_t n_starts,
+              const pfac_plan_options &o, Plan &p, std::string &err) {
+    p.geo = geometry(n_starts, di.sms);
+    const Geometry &geo = p.geo;
+    ScanArgs &a = p.a;
+    std::memset(&a, 0, sizeof a);
+    const uint32_t filter_words = (1u << t.log2_bits) >= 32 ? (1u << t.log2_bits) / 32 : 1u;
+    const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
+    const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
+    const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
+    const uint32_t *h_tbits = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_bits);
+    const uint32_t *h_trank = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_rank);
+    const uint32_t *h_tails = reinterpret_cast<const uint32_t *>(host_image + hh.off_tails);
+    auto tails_below = [&](uint32_t H) -> uint32_t {  // rank(H)
+        return h_trank[H >> 5] + (uint32_t)__builtin_popcount(h_tbits[H >> 5] & ((1u << (H & 31)) - 1u));
+    };
+    auto tbytes_below = [&](uint32_t nt) -> uint32_t {
+        return nt < hh.n_tails ? h_tails[4 * nt] : (uint32_t)hh.n_tail_bytes;
+    };
+    auto hot_bytes = [&](uint32_t H) -> uint64_t {
+        const uint32_t nt = tails_below(H);
+        return 2ull * align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) + 16ull * nt +
+               align16(tbytes_below(nt));
+    };
+    // "Big L1" plan: a trie too big for shared memory but within a few L1s
+    // (kBigL1Trie) gets no hot levels, a 2-slot ring and one filter copy, so the
+    // L1/shared split leaves the largest L1 for the nodes the walks actually
+    // visit (measured with tools/placement.py: C3 -19%; a multi-MB trie (C5)
+    // is faster with its dense upper levels in shared memory instead)
+    const uint64_t whole = hot_bytes(t.n_nodes - 1);
+    bool big_l1 = (t.kind == 1 || t.kind == 3 || t.kind == 4) && whole > kSmallTrie && whole <= kBigL1Trie;
+    if (o.placement == PFAC_PLACE_BIG_L1) big_l1 = true;
+    if (o.placement == PFAC_PLACE_GLOBAL || o.placement == PFAC_PLACE_SMEM) big_l1 = false;
+    // walk-queue capacity: deeper for DNA (kind 3) and 8-byte-prefix (kind 4)
+    // sets, whose walks are long (measured: C5 64 -4%, C3 96 -2.5%)
+    const uint32_t defer = t.kind == 3 ? 64u : t.kind == 4 ? 96u : (uint32_t)kDefer;  // (kernel: kDefer for kinds 1, 2)
+    // the 2-gram test (and its 8 KiB table): not for DNA (every 2-gram begins
+    // a pattern, and the kernel has no stage 2 for kind 3)
+    const bool use_pair = t.kind != 3 && o.stage2 != 0;
+    uint32_t slots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
+    if (o.ring_slots > 0) slots = (uint32_t)o.ring_slots;
+    const uint32_t fixed = kWarps * slots * kSlotBytes + (kWarps * slots + 1) * 8 + 1024 +
+                           kWarps * defer * (t.kind == 1 ? 8 : 4) + (use_pair ? 8192 : 0) + align16(40 * B) +
+                           8 * (kWarps + 2) + 512;
+    if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
+        err = "pfac scan plan: filter and text ring do not fit shared memory";
+        return kStatusLimit;
+    }
+    const uint32_t rest = (uint32_t)di.max_smem_optin - fixed;
+    // priority: ring (in `fixed`) > 4 filter copies (bank conflicts of the
+    // stage-1 loads) > hot trie > more filter copies
+    const uint32_t rep_cap = o.max_filter_rep_log2 >= 0 ? (uint32_t)o.max_filter_rep_log2 : 5u;
+    uint32_t rep0 = 0;
+    while (rep0 < 2 && rep0 < rep_cap && filter_words * 4 * (2u << rep0) <= kFilterCap &&
+           filter_words * 4 * (2u << rep0) + 8192 <= rest)
+        rep0++;
+    const uint32_t trie_budget = rest - (filter_words * 4 << rep0);
+    // Whole trie in shared memory when it fits; otherwise its upper levels
+    // (the BFS prefix) in all that is left (measured: more hot levels beat a
+    // larger L1 for the deeper ones).
+    uint32_t budget = trie_budget;
+    if (big_l1 || o.placement == PFAC_PLACE_GLOBAL) budget = 64;  // root table and level-1 bitmaps only
+    if (o.hot_bytes_cap && o.hot_bytes_cap < budget) budget = o.hot_bytes_cap;
+    uint32_t lo = 1, hi = t.n_nodes - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (hot_bytes(mid) <= budget) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t H = lo;
+    const uint32_t EH = host_node[H] & kEdgeMask;
+    const uint32_t TH = tails_below(H);
+    const uint32_t TBH = tbytes_below(TH);
+    if (hot_bytes(H) > rest - (filter_words * 4 << rep0)) {
+        err = "pfac scan plan: internal shared-memory plan error";
+        return kStatusLimit;
+    }
+    const uint32_t left = rest - (uint32_t)hot_bytes(H);  // >= filter_words * 4 << rep0
+    uint32_t rep_log2 = rep0;
+    while (rep_log2 < rep_cap && filter_words * 4 * (2u << rep_log2) <= (left < kFilterCap ? left : kFilterCap))
+        rep_log2++;
+    if (big_l1) rep_log2 = 0;
+    const uint32_t filter_bytes = filter_words * 4 << rep_log2;
+
+    a.t = t;
+    a.filter_words = filter_words;
+    a.rep_log2 = rep_log2;
+    uint32_t off = align_up(filter_bytes, 128);
+    a.off_ring = off;   off += kWarps * slots * kSlotBytes;
+    a.off_bar = off;    off += (kWarps * slots + 1) * 8;
+    a.off_warp = off;   off += 8 * (kWarps + 2);  // warp totals [kWarps + 2] (the last: the CTA's round counter first)
+    off = align_up(off, 16);
+    a.off_root = off;   off += 1024;
+    a.off_defer = off;  off += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
+    a.defer = defer;
+    a.off_pair = off;   off += use_pair ? 8192 : 0;  // 2-gram prefix table [256][8] words
+    a.use_pair = use_pair;
+    a.off_bm = off;     off += align16(40 * B);
+    a.off_node = off;   off += align16(4 * (H + 1));
+    a.off_aux = off;    off += align16(4 * (H + 1));
+    a.off_label = off;  off += align16(EH);
+    {   // terminal tables in smem when small and they fit what is left
+        const uint32_t tb = align16(4 * (uint32_t)(hh.n_terminals + 1 + hh.n_kept_terminals));
+        a.off_terms = 0;
+        if (hh.n_terminals + 1 + hh.n_kept_terminals < 8192 &&
+            off + tb + 16 * TH + align16(TBH) <= (uint32_t)di.max_smem_optin) {
+            a.off_terms = off;
+            off += tb;
+        }
+    }
+    a.off_tails = off;  off += 16 * TH;
+    a.off_tbytes = off; off += align16(TBH);
+    a.hot_tails = TH;
+    a.hot_tail_bytes = TBH;
+    p.smem = off;
+    if (p.smem > (size_t)di.max_smem_optin) {
+        err = "pfac scan plan: the requested plan does not fit shared memory";
+        return kStatusLimit;
+    }
+    a.n_level1 = B;
+    a.hot_nodes = H;
+    a.hot_edges = EH;
+    // walks through a shared-memory trie are cheaper than an L2 probe of the
+    // exact key set: probe only when the trie is not wholly staged
+    a.use_kset = t.kset != nullptr && H < t.n_nodes - 1;
+    a.use_entry = t.entry != nullptr && o.entry != 0;
+    // walks through a wholly staged trie are short and even: (almost) all
+    // rounds in per-warp blocks; else the last quarter is handed out
+    // dynamically (measured: C3 -11% dynamic)
+    a.ctg64 = o.ctg64 >= 0 ? (uint32_t)o.ctg64 : (H >= t.n_nodes - 1 ? 64u : 48u);
+    // the shared pool: the text's last rounds, taken by any warp whose CTA's
+    // range is done (cross-CTA balance where walks leave the SM: content
+    // skew between ranges, e.g. C5's first ranges hold twice the matches);
+    // planned when start offsets from a CTA's first round fit 32 bits
+    {
+        const uint64_t pool64 = o.pool64 >= 0 ? (uint64_t)o.pool64 : (a.ctg64 < 64 ? 4u : 0u);
+        const uint64_t n_pool = geo.n_rounds * pool64 / 64;
+        const bool pool = t.kind != 2 && n_pool >= geo.grid && geo.n_rounds * (uint64_t)kRound <= (1ull << 32);
+        a.n_main = pool ? geo.n_rounds - n_pool : geo.n_rounds;
+        a.rounds_per_cta = pool ? (a.n_main + geo.grid - 1) / geo.grid : geo.rounds_per_cta;
+        a.pool_seg = pool ? (uint32_t)((n_pool + geo.grid - 1) / geo.grid) : 0u;
+    }
+    a.hit_cap = geo.hit_cap;
+    p.slots = slots;
+
+    pfac_plan_info &f = p.info;
+    std::memset(&f, 0, sizeof f);
+    f.filter_kind = t.kind;
+    f.ring_slots = slots;
+    f.filter_copies = 1u << rep_log2;
+    f.smem_bytes = (uint32_t)p.smem;
+    f.hot_nodes = H;
+    f.image_nodes = t.n_nodes;
+    f.hot_edges = EH;
+    f.terms_in_smem = a.off_terms != 0;
+    f.grid = (uint32_t)geo.grid;
+    f.warps_per_cta = kWarps;
+    f.hit_cap = geo.hit_cap;
+    f.stage2 = use_pair;
+    f.entry = a.use_entry;
+    f.kset = a.use_kset;
+    f.pool_rounds = (uint32_t)(geo.n_rounds - a.n_main);
+    f.placement = big_l1 ? PFAC_PLACE_BIG_L1 : (H > B ? PFAC_PLACE_SMEM : PFAC_PLACE_GLOBAL);
+    f.rounds_per_cta = a.rounds_per_cta;
+    f.main_rounds = a.n_main;
+    return kStatusOk;
 }
 
 }  // namespace
@@ -1467,39 +1671,27 @@ int debug_timing(unsigned long long *host, uint64_t n) {
 }
 #endif
 
-// Environment knobs of the tools (ablations, plan dumps), read once per
-// process: a launch costs no environment scans.
-struct Knobs {
-    bool k4_nopair, slots2, debug_plan, l2_persist, no_entry;
-    const char *bigl1_hot, *hot_bytes, *max_rep_log2, *ctg64, *pool64;
-};
-const Knobs &knobs() {
-    static const Knobs k = [] {
-        Knobs v;
-        v.k4_nopair = std::getenv("PFAC_K4_NOPAIR") != nullptr;
-        v.slots2 = std::getenv("PFAC_SLOTS2") != nullptr;
-        v.debug_plan = std::getenv("PFAC_DEBUG_PLAN") != nullptr;
-        v.l2_persist = std::getenv("PFAC_L2_PERSIST") != nullptr;
-        v.no_entry = std::getenv("PFAC_NO_ENTRY") != nullptr;
-        v.bigl1_hot = std::getenv("PFAC_BIGL1_HOT");
-        v.hot_bytes = std::getenv("PFAC_HOT_BYTES");
-        v.max_rep_log2 = std::getenv("PFAC_MAX_REP_LOG2");
-        v.ctg64 = std::getenv("PFAC_CTG64");
-        v.pool64 = std::getenv("PFAC_POOL64");
-        return v;
-    }();
-    return k;
+int plan_query(const DevTrie &t, const uint8_t *host_image, int device, uint64_t n_starts,
+               const pfac_plan_options &o, pfac_plan_info *out, std::string &err) {
+    int st = check_plan_options(o, err);
+    if (st != kStatusOk) return st;
+    DeviceInfo di;
+    st = device_info(device, di, err);
+    if (st != kStatusOk) return st;
+    Plan p;
+    st = make_plan(t, host_image, di, n_starts ? n_starts : 1, o, p, err);
+    if (st != kStatusOk) return st;
+    *out = p.info;
+    return kStatusOk;
 }
 
 int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const uint8_t *d_text,
                 uint64_t readable_len, uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
-                uint64_t capacity, uint64_t *d_count, void *d_ws, uint64_t ws_bytes, CUstream_st *stream_,
-                std::string &err) {
+                uint64_t capacity, uint64_t *d_count, void *d_ws, uint64_t ws_bytes, const pfac_plan_options &o,
+                CUstream_st *stream_, std::string &err) {
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
-    if (device < 0 || device >= 64) {
-        err = "pfac_match_device: bad device ordinal";
-        return kStatusInvalid;
-    }
+    int st = check_plan_options(o, err);
+    if (st != kStatusOk) return st;
     if (n_starts == 0) {
         cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(uint64_t), stream);
         if (e != cudaSuccess) {
@@ -1509,169 +1701,21 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
         return kStatusOk;
     }
     DeviceInfo di;
-    int st = device_info(device, di, err);
+    st = device_info(device, di, err);
     if (st != kStatusOk) return st;
-    const Geometry geo = geometry(n_starts, di.sms);
-    const uint64_t need = geo.ws_bytes;
+    Plan p;
+    st = make_plan(t, host_image, di, n_starts, o, p, err);
+    if (st != kStatusOk) return st;
+    const Geometry &geo = p.geo;
     if (geo.rounds_per_cta >= (1ull << (32 - kRoundLog2))) {  // start offsets within a CTA are 32-bit
         err = "pfac_match_device: n_starts too large for one launch (split the text)";
         return kStatusLimit;
     }
-    if (!d_ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(d_ws) & 15)) {
+    if (!d_ws || ws_bytes < geo.ws_bytes || (reinterpret_cast<uintptr_t>(d_ws) & 15)) {
         err = "pfac_match_device: workspace too small or misaligned";
         return kStatusInvalid;
     }
-    // ---- shared-memory plan: filter at offset 0 (replicated while it fits
-    // half of what the fixed parts leave), ring, barriers, queues, root,
-    // level-1 bitmaps, warp totals, then the hot trie prefix.
-    const uint32_t filter_words = (1u << t.log2_bits) >= 32 ? (1u << t.log2_bits) / 32 : 1u;
-    const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
-    const uint32_t *host_node = reinterpret_cast<const uint32_t *>(host_image + hh.off_node);
-    const uint32_t B = host_node[1] & kEdgeMask;  // root degree: level-1 nodes [1, B]
-    const uint32_t *h_tbits = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_bits);
-    const uint32_t *h_trank = reinterpret_cast<const uint32_t *>(host_image + hh.off_tail_rank);
-    const uint32_t *h_tails = reinterpret_cast<const uint32_t *>(host_image + hh.off_tails);
-    auto tails_below = [&](uint32_t H) -> uint32_t {  // rank(H)
-        return h_trank[H >> 5] + (uint32_t)__builtin_popcount(h_tbits[H >> 5] & ((1u << (H & 31)) - 1u));
-    };
-    auto tbytes_below = [&](uint32_t nt) -> uint32_t {
-        return nt < hh.n_tails ? h_tails[4 * nt] : (uint32_t)hh.n_tail_bytes;
-    };
-    auto hot_bytes = [&](uint32_t H) -> uint64_t {
-        const uint32_t nt = tails_below(H);
-        return 2ull * align16(4 * (H + 1)) + align16(host_node[H] & kEdgeMask) +
-               16ull * nt + align16(tbytes_below(nt));
-    };
-    // "Big L1" plan: a trie too big for shared memory but within a few L1s
-    // (kBigL1Trie) gets no hot levels, a 2-slot ring and one filter copy, so the
-    // L1/shared split leaves the largest L1 for the nodes the walks actually
-    // visit (measured with tools/placement.py: C3 -19%; a multi-MB trie (C5)
-    // is faster with its dense upper levels in shared memory instead)
-    const uint64_t whole = hot_bytes(t.n_nodes - 1);
-    const bool big_l1 = (t.kind == 1 || t.kind == 3 || t.kind == 4) && whole > kSmallTrie && whole <= kBigL1Trie;
-    // walk-queue capacity: deeper for DNA (kind 3) and 8-byte-prefix (kind 4)
-    // sets, whose walks are long (measured: C5 64 -4%, C3 96 -2.5%)
-    const uint32_t defer = t.kind == 3 ? 64u : t.kind == 4 ? 96u : (uint32_t)kDefer;  // (kernel: kDefer for kinds 1, 2)
-    // the 2-gram test (and its 8 KiB table): not for DNA (every 2-gram begins a
-    // pattern); optional for 8-byte prefixes (tuning knob)
-    const bool use_pair = t.kind != 3 && !(t.kind == 4 && knobs().k4_nopair);
-    uint32_t kSlots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
-    if (knobs().slots2 && (t.kind == 1 || t.kind == 3 || t.kind == 4)) kSlots = 2;  // ablation only
-    const uint32_t fixed = kWarps * kSlots * kSlotBytes + (kWarps * kSlots + 1) * 8 + 1024 +
-                           kWarps * defer * (t.kind == 1 ? 8 : 4) + (use_pair ? 8192 : 0) +
-                           align16(40 * B) + 8 * (kWarps + 2) + 512;
-    if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
-        err = "pfac_match_device: filter does not fit shared memory";
-        return kStatusLimit;
-    }
-    const uint32_t rest = (uint32_t)di.max_smem_optin - fixed;
-    // priority: ring (in `fixed`) > 4 filter copies (bank conflicts of the
-    // stage-1 loads) > hot trie > more filter copies
-    uint32_t rep0 = 0;
-    while (rep0 < 2 && filter_words * 4 * (2u << rep0) <= kFilterCap && filter_words * 4 * (2u << rep0) + 8192 <= rest)
-        rep0++;
-    const uint32_t trie_budget = rest - (filter_words * 4 << rep0);
-    // H = largest BFS prefix whose node words [0, H], labels [0, row_ptr[H]),
-    // tail bitmap/rank words and tail records + bytes (tails of nodes < H)
-    // all fit the budget
-    // Whole trie in shared memory when it fits; otherwise its upper levels
-    // (the BFS prefix) in all that is left (measured: more hot levels beat a
-    // larger L1 for the deeper ones; kHotCap is a tuning knob, default off).
-    uint32_t budget =
-        hot_bytes(t.n_nodes - 1) <= trie_budget ? trie_budget : (trie_budget < kHotCap ? trie_budget : kHotCap);
-    if (big_l1) {  // root table and level-1 bitmaps only (+ a tuning knob)
-        budget = 64;
-        if (const char *h = knobs().bigl1_hot) budget = (uint32_t)std::strtoul(h, nullptr, 10);
-    }
-    if (const char *cap = knobs().hot_bytes) {  // placement ablation (tools/placement.py) only
-        const uint32_t c = (uint32_t)std::strtoul(cap, nullptr, 10);
-        if (c < budget) budget = c;
-    }
-    uint32_t lo = 1, hi = t.n_nodes - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (hot_bytes(mid) <= budget) lo = mid; else hi = mid - 1;
-    }
-    const uint32_t H = lo;
-    const uint32_t EH = host_node[H] & kEdgeMask;
-    const uint32_t TH = tails_below(H);
-    const uint32_t TBH = tbytes_below(TH);
-    const uint32_t left = rest - (uint32_t)hot_bytes(H);  // >= filter_words * 4 << rep0
-    uint32_t rep_log2 = rep0;
-    while (rep_log2 < 5 && filter_words * 4 * (2u << rep_log2) <= (left < kFilterCap ? left : kFilterCap)) rep_log2++;
-    if (big_l1) rep_log2 = 0;
-    if (const char *r = knobs().max_rep_log2) {  // placement ablation only
-        const uint32_t m = (uint32_t)std::strtoul(r, nullptr, 10);
-        if (rep_log2 > m) rep_log2 = m;
-    }
-    const uint32_t filter_bytes = filter_words * 4 << rep_log2;
-
-    ScanArgs a;
-    a.t = t;
-    a.filter_words = filter_words;
-    a.rep_log2 = rep_log2;
-    uint32_t o = filter_bytes;
-    o = align_up(o, 128);
-    a.off_ring = o;   o += kWarps * kSlots * kSlotBytes;
-    a.off_bar = o;    o += (kWarps * kSlots + 1) * 8;
-    a.off_warp = o;   o += 8 * (kWarps + 2);  // warp totals [kWarps + 2] (the last: the CTA's round counter first)
-    o = align_up(o, 16);
-    a.off_root = o;   o += 1024;
-    a.off_defer = o;  o += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
-    a.defer = defer;
-    a.off_pair = o;   o += use_pair ? 8192 : 0;           // 2-gram prefix table [256][8] words
-    a.use_pair = use_pair;
-    a.off_bm = o;     o += align16(40 * B);
-    a.off_node = o;   o += align16(4 * (H + 1));
-    a.off_aux = o;    o += align16(4 * (H + 1));
-    a.off_label = o;  o += align16(EH);
-    {   // terminal tables in smem when small and they fit what is left
-        const uint32_t tb = align16(4 * (uint32_t)(hh.n_terminals + 1 + hh.n_kept_terminals));
-        a.off_terms = 0;
-        if (hh.n_terminals + 1 + hh.n_kept_terminals < 8192 &&
-            o + tb + 16 * TH + align16(TBH) <= (uint32_t)di.max_smem_optin) {
-            a.off_terms = o;
-            o += tb;
-        }
-    }
-    a.off_tails = o;  o += 16 * TH;
-    a.off_tbytes = o; o += align16(TBH);
-    a.hot_tails = TH;
-    a.hot_tail_bytes = TBH;
-    const size_t smem = o;
-    if (smem > (size_t)di.max_smem_optin) {
-        err = "pfac_match_device: internal shared-memory plan error";
-        return kStatusLimit;
-    }
-    a.n_level1 = B;
-    a.hot_nodes = H;
-    // walks through a shared-memory trie are cheaper than an L2 probe of the
-    // exact key set: probe only when the trie is not wholly staged
-    a.use_kset = t.kset != nullptr && H < t.n_nodes - 1;
-    a.use_entry = t.entry != nullptr && !knobs().no_entry;
-    // walks through a wholly staged trie are short and even: (almost) all
-    // rounds in per-warp blocks; else the last quarter is handed out
-    // dynamically (measured: C3 -11% dynamic)
-    {
-        const char *e = knobs().ctg64;  // tools only
-        a.ctg64 = e ? (uint32_t)std::min(64l, std::max(0l, std::atol(e))) : (H >= t.n_nodes - 1 ? 64u : 48u);
-    }
-    a.hot_edges = EH;
-    if (knobs().debug_plan) {  // tools only
-        std::fprintf(stderr,
-                         "pfac plan: kind %u smem %zu of %d; filter %u B x%u; hot nodes %u of %u (edges %u, tails %u, "
-                         "tail bytes %u); terms in smem %d; grid %llu x %d warps, %llu rounds/CTA, hit cap %u\n",
-                         t.kind, smem, di.max_smem_optin, filter_words * 4, 1u << rep_log2, H, t.n_nodes, EH, TH, TBH,
-                         a.off_terms != 0, (unsigned long long)geo.grid, kWarps,
-                         (unsigned long long)geo.rounds_per_cta, geo.hit_cap);
-    }
-    uint32_t parity;
-    {
-        std::lock_guard<std::mutex> lk(g_ws_mu);
-        uint32_t &p = g_ws_parity[d_ws];  // 0 for a new (zero-filled) workspace
-        parity = p;
-        p ^= 1u;
-    }
+    ScanArgs a = p.a;
     a.text = d_text;
     a.readable = readable_len;
     a.n_starts = n_starts;
@@ -1686,41 +1730,34 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.round_val = reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(d_ws) + kWsFixed);
     a.round_owner = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(d_ws) + geo.off_owner);
     a.hits = reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(d_ws) + geo.off_hits);
-    a.hit_cap = geo.hit_cap;
-    a.parity = parity;
-    // the shared pool: the text's last rounds, taken by any warp whose CTA's
-    // range is done (cross-CTA balance where walks leave the SM: content
-    // skew between ranges, e.g. C5's first ranges hold twice the matches);
-    // planned when start offsets from a CTA's first round stay 32-bit
-    {
-        const char *e = knobs().pool64;  // tools only: pool share in 64ths
-        const uint64_t pool64 = e ? (uint64_t)std::min(32l, std::max(0l, std::atol(e))) : (a.ctg64 < 64 ? 4u : 0u);
-        const uint64_t n_pool = geo.n_rounds * pool64 / 64;
-        const bool pool = t.kind != 2 && n_pool >= geo.grid && geo.n_rounds * (uint64_t)kRound < (1ull << 32);
-        a.n_main = pool ? geo.n_rounds - n_pool : geo.n_rounds;
-        a.rounds_per_cta = pool ? (a.n_main + geo.grid - 1) / geo.grid : geo.rounds_per_cta;
-        a.pool_seg = pool ? (uint32_t)((n_pool + geo.grid - 1) / geo.grid) : 0u;
-    }
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
-    const void *fn = kernel_for(t.kind, kSlots);
-    if (knobs().l2_persist) {  // placement ablation only: the device image as an L2 persisting window
+    const void *fn = kernel_for(t.kind, p.slots);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)geo.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+    attr[0].val.cooperative = 1;
+    cfg.numAttrs = 1;
+    if (o.l2_persist) {  // placement ablation: the device image as an L2 persisting window of this launch
+        const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
+        const size_t win = std::min<size_t>((size_t)hh.image_bytes - hh.off_node, 64u << 20);
         static std::once_flag once;
         std::call_once(once, [&] { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 64u << 20); });
-        cudaStreamAttrValue v = {};
-        v.accessPolicyWindow.base_ptr = const_cast<uint32_t *>(t.node);
-        v.accessPolicyWindow.num_bytes = (size_t)hh.image_bytes - hh.off_node;
-        v.accessPolicyWindow.hitRatio = 1.0f;
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v);
+        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[1].val.accessPolicyWindow.base_ptr = const_cast<uint32_t *>(t.node);
+        attr[1].val.accessPolicyWindow.num_bytes = win;
+        attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.numAttrs = 2;
     }
-    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)geo.grid), dim3(kThreads), args, smem, stream);
+    cfg.attrs = attr;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) {
-        {   // the kernel did not run: the barrier counter in use is unchanged
-            std::lock_guard<std::mutex> lk(g_ws_mu);
-            g_ws_parity[d_ws] = parity;
-        }
         err = std::string("scan launch: ") + cudaGetErrorString(e);
         return kStatusCuda;
     }

@@ -2,52 +2,57 @@
 """NEXT-4: Fig. 6-style placement ablation on B200.  The paper
 measured the same scan with the trie in global memory (12 Gbps) and in texture
 memory with row_ptr in shared memory (22 Gbps) on a GTX 1080 (PAPER.md:121-125,
-136).  Here, per config, the same kernel and inputs with:
-  global   - no trie level staged in shared memory (PFAC_HOT_BYTES=64: root
-             table and level-1 bitmaps only; nodes/labels/records via L1/L2)
-  smem     - the default plan (whole trie, or its upper levels, in shared memory)
-  smem+L2p - default plus the device image as an L2 persisting access window
+136).  Here, per config, the same kernel and inputs with each pfac_placement
+(include/pfac.h; chosen through pfac_match_device_ex's plan options):
+  global   - no trie level staged in shared memory (root table and level-1
+             bitmaps only; nodes/labels/records via L1/L2)
+  smem     - the whole trie, or its upper levels, in shared memory
+  smem+L2p - smem plus the device image as an L2 persisting access window
+  big_l1   - no trie level staged, 2-slot ring, one filter copy (largest L1)
+  auto     - the planner's choice
 Timing as bench.py (CUDA events, L2 flushed outside them).  One JSON line per
-(config, variant)."""
+(config, variant), with the plan the library reports."""
 import json
 import os
-import subprocess
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CHILD = r'''
-import os, sys, json, torch, numpy as np
-sys.path.insert(0, %r)
-import gen, paper_1702_03657_b200 as pf
-cid = int(sys.argv[1]); n = min(gen.config(cid)["text_len"], 1 << 30)
-text = torch.from_numpy(gen.text(cid, 0, n)).cuda()
-sc = pf.Scanner(pf.Trie(gen.patterns(cid)), "cuda:0", capacity=n // 64 + 4096)
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for _ in range(3):
-    flush.fill_(1); sc.launch(text)
-torch.cuda.synchronize()
-ts = []
-for i in range(int(sys.argv[2])):
-    flush.fill_(i)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); sc.launch(text); b.record(); torch.cuda.synchronize()
-    ts.append(a.elapsed_time(b) / 1e3)
-t = float(np.mean(ts))
-print(json.dumps({"n": n, "us": t * 1e6, "gbps": 8 * n / t / 1e9}))
-''' % ROOT
+import numpy as np
+import torch
 
-variants = {"global": {"PFAC_HOT_BYTES": "64"}, "smem": {}, "smem+L2p": {"PFAC_L2_PERSIST": "1"},
-            "global+bigL1": {"PFAC_HOT_BYTES": "64", "PFAC_SLOTS2": "1", "PFAC_MAX_REP_LOG2": "0"},
-            "global+L1mid": {"PFAC_HOT_BYTES": "64", "PFAC_SLOTS2": "1"}}
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import gen  # noqa: E402
+import paper_1702_03657_b200 as pf  # noqa: E402
+
+VARIANTS = {"global": {"placement": "global"}, "smem": {"placement": "smem"},
+            "smem+L2p": {"placement": "smem", "l2_persist": 1}, "big_l1": {"placement": "big_l1"},
+            "auto": {}}
 if os.environ.get("VARIANTS"):
-    variants = {k: v for k, v in variants.items() if k in os.environ["VARIANTS"].split(",")}
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["VARIANTS"].split(",")}
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for cid in [int(c) for c in (sys.argv[1:] or ["2", "3", "4", "5"])]:
-    reps = "100" if cid == 2 else "6"
-    for name, env in variants.items():
-        out = subprocess.run([sys.executable, "-c", CHILD, str(cid), reps], env=dict(os.environ, **env),
-                             capture_output=True, text=True)
-        if out.returncode:
-            print(json.dumps({"config": f"C{cid}", "variant": name, "error": out.stderr[-300:]}), flush=True)
-            continue
-        r = json.loads(out.stdout.strip().splitlines()[-1])
-        print(json.dumps({"config": f"C{cid}", "variant": name, **r}), flush=True)
+    n = min(gen.config(cid)["text_len"], 1 << 30)
+    text = torch.from_numpy(gen.text(cid, 0, n)).cuda()
+    trie = pf.Trie(gen.patterns(cid))
+    reps = 100 if cid == 2 else 8
+    for name, kw in VARIANTS.items():
+        sc = pf.Scanner(trie, "cuda:0", capacity=n // 64 + 4096, **kw)
+        for _ in range(3):
+            flush.fill_(1)
+            sc.launch(text)
+        torch.cuda.synchronize()
+        ts = []
+        for i in range(reps):
+            flush.fill_(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            sc.launch(text)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        t = float(np.median(ts))
+        plan = trie.plan(n, **kw)
+        print(json.dumps({"config": f"C{cid}", "variant": name, "n": n, "us": t * 1e6, "gbps": 8 * n / t / 1e9,
+                          "count": int(sc.count.item()),
+                          "plan": {k: plan[k] for k in ("placement", "hot_nodes", "image_nodes", "filter_copies",
+                                                        "ring_slots", "smem_bytes")}}), flush=True)
