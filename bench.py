@@ -4,21 +4,30 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pfac|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
 
-A step is one pass of the whole hot path (text
-streaming, per-position walk, deterministic compaction) over one batch of
-synthetic input: the C2 workload (BASELINE.json configs[1]: 1,000 printable
-ASCII patterns of length 4-32, 64 MiB of text) per GPU.  Multi-GPU is weak
-scaling: rank r scans its own 64 MiB shard of one long text plus the
-(longest-1)-byte halo of the next shard; the trie image is NCCL-broadcast once
-(outside the timed region).  Text is resident in HBM before timing; L2 is
-flushed (256 MiB write) before every step, outside the timed events.
+Workload: BASELINE.json configs[3] = C4, the configuration the metric
+"(1/2/4/8 B200)" is quoted on and the largest that fits one GPU: 100,000 byte
+patterns of length 4-128 (uniform bytes) over 4 GiB of uniform text with
+planted matches (2^32 start positions).  A step is one pass of the whole hot
+path (text streaming, per-position walk, deterministic
+compaction) over that text, plus, for N > 1, the gather of the sorted (pos,
+pid) rows to rank 0 (a8).
 
+N > 1 is STRONG scaling of the same 4 GiB: rank r owns a 4 KiB-aligned start
+range and reads a (longest-1)-byte halo; the trie image is
+NCCL-broadcast once (timed separately: `broadcast`); every step is scan +
+gather (counts all-gathered, rows sent point-to-point to rank 0), timed with
+CUDA events on each rank and maxed over ranks.  Rank 0 checks the count and
+a 64-bit digest of the gathered rows against the CPU oracle (not timed).
+
+Text is resident in HBM before timing and larger than L2 (4 GiB vs 126 MB);
+L2 is also flushed (256 MiB write) before every step, outside the events.
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the
 test-infrastructure program under oracle/) on the box's host cores instead.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -30,19 +39,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "scan throughput Gbps (1/2/4/8 B200) vs HBM roofline; trie bytes vs uncompressed"
-CONFIG_ID = 2
-WORKLOAD = "C2: 1,000 random printable-ASCII patterns (len 4-32), 64 MiB synthetic printable-ASCII text with planted matches"
+CONFIG_ID = 4
+WORKLOADS = {
+    2: "C2: 1,000 random printable-ASCII patterns (len 4-32), 64 MiB printable-ASCII text",
+    3: "C3: 10,000 Snort/ClamAV-shaped patterns (len 8-64), 1 GiB packet-like text",
+    4: "C4: 100,000 random byte patterns (len 4-128), 4 GiB uniform-byte text with planted matches",
+    5: "C5: 50,000 DNA k-mers (k=16-32), 2 GiB slice of the 16 GiB genome-like text (its 1-GPU share at G=8)",
+}
+EXTRA_BYTES = {2: 64 << 20, 3: 1 << 30, 5: 2 << 30}
 PAPER_CONTEXT = {"gbps": 22, "hw": "GTX 1080", "patterns": 1000, "text": "King James Bible", "cite": "PAPER.md:136"}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="pfac", choices=["pfac", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="skip rank 0's oracle count/digest check")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C5 side lines (N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample (wall seconds)")
     return ap.parse_args()
 
@@ -55,19 +72,28 @@ def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic():
+def load_traffic(cid):
     """dram bytes per launch of the scan kernel from the committed ncu capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
+        d = d.get(f"C{cid}", {})
         return d.get("bytes_per_launch"), d.get("source")
     except Exception:
         return None, None
+
+
+def digest(pos, pid):
+    import numpy as np
+    h = hashlib.blake2b(digest_size=8)
+    h.update(np.ascontiguousarray(pos, np.uint64).tobytes())
+    h.update(np.ascontiguousarray(pid, np.uint32).tobytes())
+    return h.hexdigest()
 
 
 # --------------------------------------------------------------- clocks
@@ -120,51 +146,74 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------ reference
+# ------------------------------------------------------------ CPU oracle
+def oracle_sample_gbps(otrie, cid, seconds, reps_cap=1000):
+    """The oracle as it stands (PFAC bitmap-trie walk, all host threads) on a
+    bounded prefix of config cid's text: (Gbps, bytes per pass, passes)."""
+    import gen
+    cores = os.cpu_count()
+    n = gen.config(cid)["text_len"]
+    probe = 16 << 20
+    text = gen.text(cid, 0, probe + 4096)
+    t0 = time.perf_counter()
+    otrie.match(text[:probe + 127], readable_len=probe + 127, lo=0, hi=probe, engine="pfac", threads=cores)
+    est = (time.perf_counter() - t0) / probe  # s per byte
+    S = int(min(n - 4096, max(probe, seconds / max(est, 1e-12))))
+    S -= S % 4096
+    if S > probe:
+        text = gen.text(cid, 0, S + 4096)
+    done, t_tot, reps = 0, 0.0, 0
+    while t_tot < seconds and reps < reps_cap:
+        t0 = time.perf_counter()
+        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine="pfac", threads=cores)
+        t_tot += time.perf_counter() - t0
+        done += S
+        reps += 1
+    return 8.0 * done / t_tot / 1e9, S, reps, t_tot
+
+
 def run_reference(args, rank):
-    """The oracle as it stands (oracle/, test infrastructure) on host cores."""
+    """`--impl reference`: the oracle as it stands (oracle/, test
+    infrastructure) on the box's host cores, same metric and config; each step
+    a bounded sample (a prefix of the C4 text) sized so the run takes about a
+    minute.  Under torchrun only rank 0 runs it."""
     if rank != 0:
         return
     import gen
     import oracle
     ps = gen.patterns(CONFIG_ID)
-    n = gen.config(CONFIG_ID)["text_len"]
-    text = gen.text(CONFIG_ID, 0, n)
-    trie = oracle.Trie(ps)
+    otrie = oracle.Trie(ps)
     cores = os.cpu_count()
-    # each step: a bounded sample of the workload (the first S bytes), sized
-    # from a probe so the whole run takes about a minute
-    t0 = time.perf_counter()
-    trie.match(text[: 4 << 20], engine="pfac", threads=cores)
-    probe = time.perf_counter() - t0
-    budget = 60.0 / max(1, args.steps + args.warmup)
-    S = int(min(n, max(1 << 20, (4 << 20) * budget / max(probe, 1e-6))))
-    S -= S % 4096
+    per_step = 45.0 / max(1, args.steps + args.warmup)
+    _, S, _, _ = oracle_sample_gbps(otrie, CONFIG_ID, per_step, reps_cap=1)
+    text = gen.text(CONFIG_ID, 0, S + 4096)
     for _ in range(args.warmup):
-        trie.match(text[:S], engine="pfac", threads=cores)
+        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine="pfac", threads=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        trie.match(text[:S], engine="pfac", threads=cores)
+        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine="pfac", threads=cores)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     gbps = 8.0 * S * len(times) / tot / 1e9
-    sample = f"first {S} bytes of the C2 text per step (PFAC bitmap-trie walk, {cores} threads)"
+    sample = f"first {S} start positions of the C4 text per step (PFAC bitmap-trie walk, {cores} threads)"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": gbps, "unit": "Gbps", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "text_bytes": S, "patterns": len(ps), "parallelism": "cpu threads"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": WORKLOADS[CONFIG_ID], "text_bytes": S, "patterns": len(ps),
+                   "parallelism": "cpu threads"},
         "cpu_baseline": {"value": gbps, "unit": "Gbps", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbps, "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
+# --------------------------------------------------------------- probes
 def read_stream_ceiling(dev, text, flush, scan_s):
     """KB0 (tools/probe/kb0.cu): a pure 16-byte read stream, timed like the scan
-    (L2 flushed outside CUDA events), on the bench's own text buffer and on a
-    1 GiB buffer: the read-only ceiling next to the copy-based MEASURED_PEAKS
-    figure.  Outside the scan's timed region; None if the probe is not built."""
+    (L2 flushed outside CUDA events), on the bench's own text buffer: the
+    read-only ceiling next to the copy-based MEASURED_PEAKS figure.  Outside
+    the scan's timed region; None if the probe is not built."""
     import ctypes as C
 
     import torch
@@ -176,49 +225,60 @@ def read_stream_ceiling(dev, text, flush, scan_s):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sink = torch.zeros(sms * 4 * 16, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    out = {}
-    for name, buf in [("bench_text", text), ("1GiB", torch.ones(1 << 30, dtype=torch.uint8, device=dev))]:
-        n = buf.numel() // 16 * 16
-        ts = []
-        for i in range(12):
-            flush.fill_(i)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            lib.kb0_launch(buf.data_ptr(), n, sink.data_ptr(), sms, stream.cuda_stream)
-            b.record(stream)
-            torch.cuda.synchronize()
-            if i >= 2:
-                ts.append(a.elapsed_time(b) / 1e3)
-        t = sum(ts) / len(ts)
-        out[name] = {"bytes": n, "us": 1e6 * t, "GBs": n / t / 1e9}
-    out["scan_vs_kb0_same_bytes"] = out["bench_text"]["us"] / (1e6 * scan_s)
-    return out
+    n = text.numel() // 16 * 16
+    ts = []
+    for i in range(8):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        lib.kb0_launch(text.data_ptr(), n, sink.data_ptr(), sms, stream.cuda_stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b) / 1e3)
+    t = sum(ts) / len(ts)
+    return {"bytes": n, "us": 1e6 * t, "GBs": n / t / 1e9, "scan_vs_kb0_same_bytes": t / scan_s}
 
 
-def cpu_baseline(seconds):
-    """Oracle timed on a bounded sample of the same workload (rank 0, N=1)."""
+def time_launches(sc, text, flush, n, reps, stream):
+    """Median/mean device time of `reps` single-launch scans (L2 flushed)."""
+    import torch
+    ts = []
+    for i in range(reps):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sc.launch(text, readable_len=n)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return statistics.median(ts), sum(ts) / len(ts)
+
+
+def extra_configs(dev, flush, peak, stream):
+    """C2, C3, C5 (1-GPU sizes) timed like the headline: side lines only."""
+    import torch
+
     import gen
-    import oracle
-    ps = gen.patterns(CONFIG_ID)
-    n = gen.config(CONFIG_ID)["text_len"]
-    text = gen.text(CONFIG_ID, 0, n)
-    trie = oracle.Trie(ps)
-    cores = os.cpu_count()
-    done, t_tot, reps = 0, 0.0, 0
-    S = n
-    t0 = time.perf_counter()
-    trie.match(text[: 1 << 20], engine="pfac", threads=cores)
-    est = (time.perf_counter() - t0) * (n >> 20)
-    if est > seconds:
-        S = max(1 << 20, int(n * seconds / est)) & ~4095
-    while t_tot < seconds and reps < 1000:
-        t0 = time.perf_counter()
-        trie.match(text[:S], engine="pfac", threads=cores)
-        t_tot += time.perf_counter() - t0
-        done += S
-        reps += 1
-    return {"value": 8.0 * done / t_tot / 1e9, "unit": "Gbps", "cores": cores, "kind": "oracle",
-            "sample": f"{reps} pass(es) over {S} bytes of the C2 text, PFAC bitmap-trie walk, {cores} threads"}
+    import paper_1702_03657_b200 as pf
+    out = {}
+    for cid, n in EXTRA_BYTES.items():
+        ps = gen.patterns(cid)
+        trie = pf.Trie(ps)
+        host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        gen.text(cid, 0, n, out=host.numpy())
+        text = host.to(dev)
+        sc = pf.Scanner(trie, dev, capacity=max(1 << 16, n // 256))
+        time_launches(sc, text, flush, n, 3, stream)
+        med, mean = time_launches(sc, text, flush, n, 30 if cid == 2 else 10, stream)
+        cnt = int(sc.count.item())
+        out[f"C{cid}"] = {"workload": WORKLOADS[cid], "text_bytes": n, "us_median": 1e6 * med,
+                          "gbps": 8.0 * n / med / 1e9, "hbm_frac": (n + 12 * cnt) / med / 1e9 / peak,
+                          "matches": cnt,
+                          "trie_image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed")}
+        del text, host, sc
+        torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------- main
@@ -228,6 +288,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -239,13 +300,23 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
 
     cfg = gen.config(CONFIG_ID)
-    shard = cfg["text_len"]                      # per-GPU bytes (weak scaling)
-    n_total = shard * world
+    n_total = cfg["text_len"]                   # 4 GiB, split across ranks (strong scaling)
     ps = gen.patterns(CONFIG_ID)
+    broadcast = None
     if world > 1:
-        trie = multigpu.broadcast_trie(pf.Trie(ps) if rank == 0 else None, src=0, device=local_rank)
+        trie0 = pf.Trie(ps) if rank == 0 else None
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        trie = multigpu.broadcast_trie(trie0, src=0, device=local_rank)
+        torch.cuda.synchronize()
+        bt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(bt, op=dist.ReduceOp.MAX)
+        broadcast = {"us": 1e6 * float(bt.item()), "image_bytes": trie.nbytes("device_image"),
+                     "what": "NCCL broadcast of the trie image + pfac_attach upload (one-time, not in value)"}
     else:
         trie = pf.Trie(ps)
     st = trie.stats()
@@ -256,108 +327,163 @@ def main():
     text = host.to(dev)
     n_starts = b - a
 
-    sc = pf.Scanner(trie, dev, capacity=max(1 << 16, n_starts // 512))
+    sc = pf.Scanner(trie, dev, capacity=max(1 << 20, n_starts // 2048))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    gpos = gpid = None
 
-    def step():
+    def scan():
         sc.launch(text, readable_len=r1 - r0, n_starts=n_starts, pos_base=a)
+
+    def gather():
+        nonlocal gpos, gpid
+        n = int(sc.count.item())
+        res = multigpu.gather_matches(sc.pos[:n], sc.pid[:n], dst=0, out=(gpos, gpid) if gpos is not None else None)
+        if res is not None:
+            gpos, gpid = res
+        return res
 
     for _ in range(max(3, args.warmup)):
         flush.fill_(1)
-        step()
+        scan()
+        if world > 1:
+            gather()
     torch.cuda.synchronize()
     count = int(sc.count.item())
-    assert count <= sc.cap
+    assert count <= sc.cap, "capacity"
 
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     sampler = ClockSampler(local_rank)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with sampler:
-        # keep the clock sampler busy for a while before the timed steps
         t_settle = time.perf_counter()
-        while time.perf_counter() - t_settle < 0.2:
+        while time.perf_counter() - t_settle < 0.2:  # let the clock sampler see load first
             flush.fill_(2)
-            step()
+            scan()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         for i in range(args.steps):
             flush.fill_(1)                 # L2 flush, outside the events
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
+            ev[i][0].record(stream)
+            scan()
+            ev[i][1].record(stream)
+            if world > 1:
+                gather()
+            ev[i][2].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    per_step = [s.elapsed_time(e) for s, e in evs]          # ms, device time of each step
-    t_rank = sum(per_step) / 1e3
+    step_ms = [s.elapsed_time(e) for s, _, e in ev]         # device time of each step
+    kern_ms = [s.elapsed_time(k) for s, k, _ in ev]         # the scan launch alone
+    t_rank = sum(step_ms) / 1e3
     t = torch.tensor([t_rank], dtype=torch.float64, device=dev)
     tot_count = torch.tensor([count], dtype=torch.int64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot_count, op=dist.ReduceOp.SUM)
     t_max = float(t.item())
-    value = 8.0 * n_total * args.steps / t_max / 1e9       # whole-job Gbps
+    value = 8.0 * n_total * args.steps / t_max / 1e9       # whole-job Gbps (all ranks' starts)
 
-    # roofline of the dominant (only) kernel: the step is exactly one launch
-    # of pfac_scan_kernel, so its average duration is the mean step time
-    kern_s = t_rank / args.steps
-    alg_bytes = (r1 - r0) + 12 * count                     # text read once + output rows
+    # roofline of the dominant (only) kernel of this rank: one scan launch
+    kern_s = sum(kern_ms) / len(kern_ms) / 1e3
+    alg_bytes = (r1 - r0) + 12 * count                     # text read once + 12 B per output row
     peak, peak_src = load_peaks()
     achieved = alg_bytes / kern_s / 1e9
-    traffic, traffic_src = load_traffic()
+    traffic, traffic_src = load_traffic(CONFIG_ID)
+    if traffic is not None and world > 1:
+        traffic = None  # the committed capture is of the 1-GPU launch
+        traffic_src = None
+
+    verify = None  # rank 0: count + digest of the rows (the last step's gather for N > 1) vs the oracle
+    otrie = None
+    if rank == 0 and not args.no_verify:
+        import oracle
+        otrie = oracle.Trie(ps)
+        if world == 1:
+            gp, gq = sc.pos[:count].cpu().numpy().astype(np.uint64), sc.pid[:count].cpu().numpy().astype(np.uint32)
+        else:
+            gp, gq = gpos.cpu().numpy().astype(np.uint64), gpid.cpu().numpy().astype(np.uint32)
+        full = host.numpy() if world == 1 else gen.text(CONFIG_ID, 0, n_total)
+        t0 = time.perf_counter()
+        wp, wq = otrie.match(full, engine="pfac", threads=os.cpu_count())
+        verify = {"rows": int(len(gp)), "digest": digest(gp, gq), "oracle_rows": int(len(wp)),
+                  "oracle_digest": digest(wp, wq),
+                  "equal": bool(len(gp) == len(wp) and np.array_equal(gp, wp) and np.array_equal(gq, wq)),
+                  "oracle_s": time.perf_counter() - t0}
+        del full
 
     e2e = None
     if not args.no_e2e:
         # end to end through the C ABI's host call (pfac_match): pinned host
-        # text -> H2D -> scan -> D2H of the sorted rows, every step
-        n_e2e = min(args.steps, 20)
-        trie.match_host(host.numpy()[: n_starts + 0])       # warm the cached device buffers
+        # text -> H2D -> scan -> D2H of the sorted rows, every step (N > 1:
+        # each rank's own shard; the rank-0 gather is not part of it)
+        n_e2e = min(args.steps, 5)
+        hv = host.numpy()
+        trie.match_host(hv)                                   # warm the cached device buffers
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ts = []
+        ts, rows = [], 0
         for _ in range(n_e2e):
             t0 = time.perf_counter()
-            pos, pid = trie.match_host(host.numpy())
+            pos, pid = trie.match_host(hv)
             ts.append(time.perf_counter() - t0)
+            rows = len(pos)
         te = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": 8.0 * (r1 - r0) * world * n_e2e / float(te.item()) / 1e9, "unit": "Gbps",
-               "h2d_bytes_per_step": int(r1 - r0), "d2h_bytes_per_step": int(8 + 12 * len(pos)),
-               "api": "pfac_match (host buffers)"}
+        e2e = {"value": 8.0 * n_total * n_e2e / float(te.item()) / 1e9, "unit": "Gbps",
+               "h2d_bytes_per_step": int(r1 - r0), "d2h_bytes_per_step": int(8 + 12 * rows),
+               "api": "pfac_match (host buffers, pinned)" + (" per rank, no gather" if world > 1 else "")}
 
     kb0 = read_stream_ceiling(dev, text, flush, kern_s) if rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.cpu_seconds)
+        import oracle
+        otrie = otrie or oracle.Trie(ps)
+        g, S, reps, tt = oracle_sample_gbps(otrie, CONFIG_ID, args.cpu_seconds)
+        cpu = {"value": g, "unit": "Gbps", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"{reps} pass(es) over the first {S} start positions of the C4 text "
+                         f"(PFAC bitmap-trie walk, {os.cpu_count()} threads, {tt:.1f} s)"}
+
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        del text
+        torch.cuda.empty_cache()
+        extras = extra_configs(dev, flush, peak, stream)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "Gbps", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "text_bytes_per_gpu": int(shard), "patterns": len(ps),
-                       "parallelism": f"text-sharded x{world} (halo {st['max_len'] - 1} B)",
-                       "l2": "flushed before every step (256 MiB write, outside the timed events)"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOADS[CONFIG_ID], "text_bytes": int(n_total), "patterns": len(ps),
+                       "parallelism": f"text-sharded x{world} (4 KiB-aligned starts, halo {st['max_len'] - 1} B)"
+                                      + (", rank-0 gather in every step" if world > 1 else ""),
+                       "l2": "text 4 GiB > L2; also flushed before every step (256 MiB write, outside the events)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "pfac_scan_kernel", "alg_bytes_per_launch": int(alg_bytes),
-                         "peak_source": peak_src, "traffic_source": traffic_src},
+                         "kernel_us": 1e6 * kern_s, "peak_source": peak_src, "traffic_source": traffic_src},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": sampler.summary(),
             "gpu_launches": args.steps * pf.launches_per_call(),
             "matches": int(tot_count.item()),
+            "verify": verify,
+            "broadcast": broadcast,
             "trie_bytes": {"device_image": trie.nbytes("device_image"), "uncompressed": trie.nbytes("uncompressed"),
                            "csr_core": trie.nbytes("csr_core"), "paper_crs": trie.nbytes("paper_crs"),
                            "dense_stt": trie.nbytes("dense_stt"),
                            "image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed")},
-            "step_ms": {"median": statistics.median(per_step), "min": min(per_step), "max": max(per_step)},
+            "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
+            "plan": trie.plan(n_starts, local_rank),
             "paper_context": PAPER_CONTEXT,
             "kb0": kb0,
+            "extra_configs": extras,
         }
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -58,9 +58,14 @@ def broadcast_trie(trie: Trie | None, src: int = 0, device: int = -1, group=None
     return Trie.attach(buf, device=device)
 
 
-def gather_matches(pos: torch.Tensor, pid: torch.Tensor, dst: int = 0, group=None):
+def gather_matches(pos: torch.Tensor, pid: torch.Tensor, dst: int = 0, group=None, out=None):
     """Concatenate per-rank (pos, pid) lists on `dst` in rank order (globally
-    sorted because start ranges are disjoint and ordered).  Others get None."""
+    sorted because start ranges are disjoint and ordered).
+    The counts are all-gathered (8 B per rank); then every other rank sends
+    exactly its rows to `dst` (point-to-point, no padding), which receives
+    them straight into the slices of its output.  `out` = optional (pos, pid)
+    buffers on `dst` with room for the total.  Returns (pos, pid) on `dst`,
+    None elsewhere."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = pos.device
@@ -68,16 +73,30 @@ def gather_matches(pos: torch.Tensor, pid: torch.Tensor, dst: int = 0, group=Non
     counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(counts, n, group=group)
     counts = [int(c.item()) for c in counts]
-    m = max(counts) if counts else 0
-    pad_pos = torch.zeros(m, dtype=torch.int64, device=dev)
-    pad_pid = torch.zeros(m, dtype=torch.int32, device=dev)
-    pad_pos[: pos.numel()] = pos
-    pad_pid[: pid.numel()] = pid
-    all_pos = [torch.empty(m, dtype=torch.int64, device=dev) for _ in range(world)]
-    all_pid = [torch.empty(m, dtype=torch.int32, device=dev) for _ in range(world)]
-    dist.all_gather(all_pos, pad_pos, group=group)
-    dist.all_gather(all_pid, pad_pid, group=group)
     if rank != dst:
+        reqs = []
+        if counts[rank]:
+            reqs.append(dist.isend(pos.contiguous(), dst, group=group))
+            reqs.append(dist.isend(pid.contiguous(), dst, group=group))
+        for r in reqs:
+            r.wait()
         return None
-    return (torch.cat([p[:c] for p, c in zip(all_pos, counts)]),
-            torch.cat([q[:c] for q, c in zip(all_pid, counts)]))
+    total = sum(counts)
+    if out is not None and out[0].numel() >= total and out[1].numel() >= total:
+        all_pos, all_pid = out[0][:total], out[1][:total]
+    else:
+        all_pos = torch.empty(total, dtype=pos.dtype, device=dev)
+        all_pid = torch.empty(total, dtype=pid.dtype, device=dev)
+    reqs, off = [], 0
+    for r, c in enumerate(counts):
+        if c:
+            if r == rank:
+                all_pos[off:off + c].copy_(pos)
+                all_pid[off:off + c].copy_(pid)
+            else:
+                reqs.append(dist.irecv(all_pos[off:off + c], r, group=group))
+                reqs.append(dist.irecv(all_pid[off:off + c], r, group=group))
+        off += c
+    for r in reqs:
+        r.wait()
+    return all_pos, all_pid
