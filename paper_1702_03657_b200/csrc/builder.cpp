@@ -462,10 +462,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
             filter[filter_pair_word(x >> 8, log2_bits)] |= 1u << (31u - (x & 31u));
             filter[filter_pair_word(x, log2_bits)] |= 1u << (31u - ((x >> 24) & 31u));
         } else if (kind == 1) {
-            const uint32_t b = filter4_block(x, log2_bits);
-            filter[2 * b] |= 1u << filter4_bit_lo(x);
-            filter[2 * b] |= 1u << filter4_bit_mid(x);
-            filter[2 * b + 1] |= 1u << filter4_bit_hi(x);
+            uint32_t &w = filter[filter4_offset(x, log2_bits) / 4];
+            w |= (1u << filter4_bit(x, 3)) | (1u << filter4_bit(x, 2)) | (1u << filter4_bit(x, 1));
         } else {
             uint32_t h = filter_index(x, log2_bits, exact);
             filter[h >> 5] |= 1u << (h & 31);

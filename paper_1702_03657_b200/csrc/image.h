@@ -58,14 +58,14 @@
 //                     is clear cannot match.  Two kinds:
 //                       kind 0 (d < 4): bit index filter_index(x) of the d-gram
 //                         x (little-endian), standard bit order;
-//                       kind 1 (d = 4): a blocked two-bit filter.  Block
-//                         (64 bits = words 2b, 2b+1) b = top (F-6) bits of
-//                         x * (kFilterMul << 8) (a hash of bytes 0..2); the
-//                         key sets bits 31-(byte3 & 31) and 31-(h2 & 31) of
-//                         word 2b, h2 = hi32(x * kFilterMul2), and bit
-//                         31-(byte2 & 31) of word 2b+1 (bit-reversed so the
-//                         kernel tests each with one rotate; scan.cu stage 1).
-//                         A start passes iff the three bits are set.
+//                       kind 1 (d = 4): a blocked three-bit filter in
+//                         32-bit words.  Word w = (hi32(x * kFilterMul) &
+//                         mask) / 4, mask = (filter bytes - 1) & ~3 (a hash
+//                         of all four bytes); the key sets bits 31-(byte3 &
+//                         31), 31-(byte2 & 31) and 31-(byte1 & 31) of word w
+//                         (bit-reversed so the kernel tests each with one
+//                         rotate by the byte; scan.cu stage 1).  A start
+//                         passes iff the three bits are set.
 //                       kind 2 (d = 4, small sets): the pair filter.  Starts k
 //                         and k+1 share bytes k+1..k+3, so one 32-bit word
 //                         b = filter_pair_word(bytes k+1..k+3) answers both:
@@ -125,7 +125,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 14;
+constexpr uint32_t kVersion = 15;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -176,11 +176,12 @@ PFAC_HD inline uint32_t gram8_block(uint32_t x0, uint32_t x1, uint32_t log2_bits
 PFAC_HD inline uint32_t filter_index(uint32_t key, uint32_t log2_bits, uint32_t exact) {
     return exact ? key : (key * kFilterMul) >> (32u - log2_bits);
 }
-// Kind 1 (d = 4): block index and the stored bit positions (word 2b, word
-// 2b+1) of the 4-gram x.
-PFAC_HD inline uint32_t filter4_block(uint32_t x, uint32_t log2_bits) {
-    return (x * (kFilterMul << 8)) >> (32u - (log2_bits - 6u));
+// Kind 1 (d = 4): byte offset of the 4-gram x's word in a filter of
+// 2^log2_bits bits (hi32(x * M) & mask), and its three bit positions.
+PFAC_HD inline uint32_t filter4_offset(uint32_t x, uint32_t log2_bits) {
+    return (uint32_t)(((uint64_t)x * kFilterMul) >> 32) & (((1u << (log2_bits - 3u)) - 1u) & ~3u);
 }
+PFAC_HD inline uint32_t filter4_bit(uint32_t x, uint32_t byte) { return 31u - ((x >> (8u * byte)) & 31u); }
 // Kind 2 (d = 4): word index of the three shared bytes x (low 24 bits used).
 PFAC_HD inline uint32_t filter_pair_word(uint32_t x, uint32_t log2_bits) {
     return (x * (kFilterMul << 8)) >> (32u - (log2_bits - 5u));
@@ -196,11 +197,6 @@ PFAC_HD inline uint32_t dna_bit_mid(uint32_t key) {
 }
 PFAC_HD inline uint32_t dna_bit_hi(uint32_t key) {
     return 31u - (uint32_t)(((uint64_t)key * kFilterMul3) >> 32 & 31u);
-}
-PFAC_HD inline uint32_t filter4_bit_lo(uint32_t x) { return 31u - ((x >> 24) & 31u); }
-PFAC_HD inline uint32_t filter4_bit_hi(uint32_t x) { return 31u - ((x >> 16) & 31u); }
-PFAC_HD inline uint32_t filter4_bit_mid(uint32_t x) {
-    return 31u - (uint32_t)(((uint64_t)x * kFilterMul2) >> 32 & 31u);
 }
 
 }  // namespace pfac

@@ -113,6 +113,7 @@ struct ScanArgs {
     uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
     uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_defer, off_pair, off_aux;
     uint32_t off_tails, off_tbytes;
+    uint32_t off_walkq;             // per-warp walk queue u32[2][kWalkQ] (two-level kinds)
     uint32_t hot_tails, hot_tail_bytes;  // records (and their bytes) of the record nodes < H
     uint32_t off_terms;             // out_ptr[T+1] + term_node[TK] in smem (0 = in global memory)
     uint32_t n_level1;              // B: the root's children are nodes [1, B]
@@ -434,11 +435,10 @@ __device__ __forceinline__ uint32_t clamp32(uint64_t x) { return x > 0xFFFFFFFFu
 
 // Stage 1 over one lane's kPerLane starts (text bytes wv[0..kWv) little-endian):
 // bit k set <=> start k may match.
-//  kind 1 (d = 4): word = hash of bytes k..k+2 (top bits of x*(M<<8)), bit =
-//    31 - (byte k+3 & 31): a rotate left by byte k+3 (the funnel shift takes
-//    its amount mod 32, so the 4-gram at k+3 serves as the amount) brings the
-//    tested bit to bit 31 and a funnel shift appends it to the mask.  Per
-//    start: IMAD (hash), SHF (word index), IMAD (address), LDS, 2x SHF.
+//  kind 1 (d = 4): word = hi32(x * M) & mask, bits 31 - (byte k+j & 31) for
+//    j = 3, 2, 1: a rotate left by byte k+j (the funnel shift takes its
+//    amount mod 32, so the 4-gram at k+j serves as the amount) brings each
+//    tested bit to bit 31 and a funnel shift appends it to the mask.
 //  kind 0 (d < 4): generic d-gram bit index.
 __device__ __forceinline__ uint32_t lds_abs(uint32_t addr) {
     uint32_t v;
@@ -450,7 +450,7 @@ __device__ __forceinline__ uint2 lds64_abs(uint32_t addr) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
     return v;
 }
-template <int Kind>
+template <int Kind, bool kImm1024 = false>
 __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t wv[kWv], const uint32_t ext[3],
                                              uint32_t sW, uint32_t sWmul, uint32_t stride, uint32_t base_lane) {
     uint32_t surv = 0;
@@ -527,25 +527,32 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
         surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
         static_assert(kPerLane <= 32, "");
     } else if (Kind == 1) {
-        constexpr uint32_t kMul = kFilterMul << 8;
+        // blocked three-bit filter in 32-bit words (image.h): one IMAD.HI
+        // (hi32(x * M) & mask = the word's byte offset), one LOP3 (& mask,
+        // ^ the lane's copy term: copy r sits at r * filter bytes with its
+        // words swizzled by r, so lanes reading different copies of a word hit
+        // different banks), one LDS (the filter's shared-window base as the
+        // immediate offset when it is 0x400), three rotates by bytes k+3, k+2,
+        // k+1 (funnel amounts are mod 32: the tested bits -> bit 31), one LOP3,
+        // one funnel shift into the mask
         uint32_t x[kPerLane + 3];
 #pragma unroll
         for (int k = 0; k < kPerLane + 1; ++k)
             x[k] = (k & 3) ? __funnelshift_r(wv[k >> 2], wv[(k >> 2) + 1], 8 * (k & 3)) : wv[k >> 2];
         x[kPerLane + 1] = x[kPerLane - 1] >> 16;  // byte kPerLane+1 in the low bits
         x[kPerLane + 2] = x[kPerLane - 1] >> 24;  // byte kPerLane+2
-        // four independent accumulation chains of 8 starts (short dependency
-        // chains); the block index uses IMAD.HI (a right shift on the FMA pipe,
-        // which the ALU-heavy bit test leaves idle): hi32(h * 2^(32-sW)) = h >> sW
+        const uint32_t mask = sWmul, t = stride;  // (kind 1: the word mask and the lane's copy term)
         uint32_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = kPerLane - 1; k >= 0; --k) {
-            const uint32_t blk = __umulhi(x[k] * kMul, sWmul);
-            const uint2 w2 = lds64_abs(blk * stride + base_lane);
-            // rotate by byte k+3 / byte k+2 (funnel amounts are mod 32): tested bits -> 31
-            // and by hi32(x * M2) (a third bit in word 2b)
-            const uint32_t r = __funnelshift_l(w2.x, w2.x, x[k + 3]) & __funnelshift_l(w2.y, w2.y, x[k + 2]) &
-                               __funnelshift_l(w2.x, w2.x, __umulhi(x[k], kFilterMul2));
+            const uint32_t off = (__umulhi(x[k], kFilterMul) & mask) ^ t;
+            uint32_t w;
+            if (kImm1024)
+                asm("ld.shared.u32 %0, [%1+1024];" : "=r"(w) : "r"(off));
+            else
+                asm("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(off + base_lane));
+            const uint32_t r = __funnelshift_l(w, w, x[k + 3]) & __funnelshift_l(w, w, x[k + 2]) &
+                               __funnelshift_l(w, w, x[k + 1]);
             acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);  // acc << 1 | bit
         }
         surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
@@ -586,13 +593,24 @@ __device__ __forceinline__ uint32_t slot_key(const uint8_t *slot, uint32_t off) 
     }
     return __funnelshift_r(w[0], w[1], sh);
 }
-// Probe the exact key set for a key.
+// Probe the exact key set for a key (open addressing, linear probing, no
+// deletions).  One 16-byte load answers the key's home slot and the rest of
+// its 4-slot group: the key anywhere in the group means present (a key is
+// never stored before its home slot, and a group never wraps the table);
+// an empty slot at or after the home slot means absent; else the next group.
 __device__ __forceinline__ bool kset_probe(const ScanArgs &a, uint32_t key) {
     const uint32_t mask = (1u << a.t.kset_log2) - 1u;
-    for (uint32_t i = kset_slot(key, a.t.kset_log2);; i = (i + 1) & mask) {
-        const uint32_t x = __ldg(a.t.kset + i);
-        if (x == key) return true;
-        if (x == a.t.kset_empty) return false;
+    const uint4 *k4 = reinterpret_cast<const uint4 *>(a.t.kset);
+    uint32_t i = kset_slot(key, a.t.kset_log2);
+    uint32_t from = i & 3u;
+    for (;;) {
+        const uint4 q = __ldg(k4 + (i >> 2));
+        if (q.x == key || q.y == key || q.z == key || q.w == key) return true;
+        const uint32_t e = a.t.kset_empty;
+        const uint32_t emp = (q.x == e ? 1u : 0u) | (q.y == e ? 2u : 0u) | (q.z == e ? 4u : 0u) | (q.w == e ? 8u : 0u);
+        if (emp >> from) return false;
+        i = ((i | 3u) + 1u) & mask;
+        from = 0;
     }
 }
 
@@ -608,89 +626,172 @@ __device__ __forceinline__ uint2 entry_find(const ScanArgs &a, uint32_t x0, uint
     }
 }
 
-// Is the start's filter key in the image's exact key set (image.h)?  Kind 3:
-// the 16-base DNA key; kinds 1, 2: the first 4 bytes.
-template <int Kind>
-__device__ __forceinline__ bool kset_has(const ScanArgs &a, const GlobalText &gt) {
-    uint32_t key;
-    if (Kind == 3) {
-        key = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            key |= __umulhi((gt.at4(4 * q) & 0x06060606u) * 0x820820u, 1u << 8) << (8 * q);
-    } else {
-        key = gt.at4(0);
-    }
-    const uint32_t mask = (1u << a.t.kset_log2) - 1u;
-    for (uint32_t i = kset_slot(key, a.t.kset_log2);; i = (i + 1) & mask) {
-        const uint32_t x = __ldg(a.t.kset + i);
-        if (x == key) return true;
-        if (x == a.t.kset_empty) return false;
-    }
-}
+// Deferred starts are decided in two ways:
+//  * direct (kinds 0 and 2, kind 1 without the key set, kinds 3/4 without
+//    the entry table): every queued start is walked from the root;
+//  * two-level (kind 1 with the exact key set, kinds 3/4 with the entry
+//    table): every queued start is first probed in its L2-resident table by
+//    a full warp; the survivors join the warp's walk queue in position order
+//    (with the entry node and depth to walk from) and are walked 32 at a time
+//    by the full warp, so a walk never runs with a lane or two of 32.
+constexpr uint32_t kEntShift = 27;  // walk-queue entry word: node | depth << 27 (0 = from the root)
+constexpr uint32_t kWalkQ = 64;     // walk-queue capacity per warp
 
 template <int Kind>
-__device__ __forceinline__ uint32_t walk_deferred(const ScanArgs *ap, const Smem s, uint64_t cta_lo, uint64_t cta_round0,
-                                                  uint32_t ctg_bytes, const uint32_t *dpos, const uint32_t *dkey,
-                                                  uint32_t n, uint2 *hits, uint32_t n_hits, unsigned long long &rows) {
-    const ScanArgs &a = *ap;
+__device__ __forceinline__ bool two_level(const ScanArgs &a) {
+    return (Kind == 1 && a.use_kset) || ((Kind == 3 || Kind == 4) && a.use_entry);
+}
+
+// Probe of one start (two-level kinds): kNone when no pattern can start
+// here, else the walk-queue entry word.
+template <int Kind>
+__device__ __forceinline__ uint32_t probe_start(const ScanArgs &a, const GlobalText &gt, uint32_t key) {
+    if (Kind == 1) return kset_probe(a, key) ? 0u : kNone;
+    if (Kind == 4) {  // enter at depth <= 8 through the entry table (a miss: no pattern starts here)
+        if (gt.end < kGram8) return kNone;
+        const uint2 en = entry_find(a, gt.at4(0), gt.at4(4));
+        return en.x ? en.x | en.y << kEntShift : kNone;
+    }
+    if (Kind == 3) {  // enter at depth <= 16 when the 16 bytes are A/C/G/T (the key
+                      // aliases other bytes, and no DNA pattern can cover those)
+        if (gt.end < kDnaGram) return kNone;
+        uint32_t k = 0;
+        bool acgt = true;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t w = gt.at4(4 * q);
+            const uint32_t c = (w >> 1) & 0x03030303u;  // the four 2-bit codes, one per byte
+            const uint32_t sel = (c & 0xFu) | ((c >> 4) & 0xF0u) | ((c >> 8) & 0xF00u) | ((c >> 12) & 0xF000u);
+            acgt &= __byte_perm(0x47544341u, 0u, sel) == w;  // code -> 'A','C','T','G'
+            k |= __umulhi((w & 0x06060606u) * 0x820820u, 1u << 8) << (8 * q);
+        }
+        if (!acgt) return kNone;
+        const uint2 en = entry_find(a, k, 0u);
+        return en.x ? en.x | en.y << kEntShift : kNone;
+    }
+    return 0u;
+}
+
+// Walk starts bpos[0, m) (m <= 32; bent = where each walk enters) with the
+// warp, text from global memory (L2: streamed moments ago); hits are appended
+// to the warp's hit list in the same (position) order and their pid counts
+// added to the lane's block rows or their round's count.  Returns the new hit
+// count.
+template <int Kind>
+__device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s, uint64_t cta_lo, uint64_t cta_round0,
+                                               uint32_t ctg_bytes, const uint32_t *bpos, const uint32_t *bent,
+                                               uint32_t m, uint2 *hits, uint32_t n_hits, unsigned long long &rows) {
     const int lane = threadIdx.x & 31;
+    uint32_t p = 0, tn = kNone;
+    if ((uint32_t)lane < m) {
+        p = bpos[lane];
+        const uint32_t ent = bent ? bent[lane] : 0u;
+        const uint64_t gp = cta_lo + p;
+        const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
+        tn = ent ? walk(a, s, gt, 0u, ent & ((1u << kEntShift) - 1u), ent >> kEntShift) : walk(a, s, gt, 0u);
+        if (tn != kNone) {
+            const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
+            if (p < ctg_bytes) rows += cnt;  // the lane's rows in its warp's block (per-warp totals)
+            else atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2), (unsigned long long)cnt);  // dynamic round
+        }
+    }
+    const bool hit = tn != kNone;
+    const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+    if (hit) {
+        const uint32_t idx = n_hits + __popc(hb & ((1u << lane) - 1u));
+        if (idx < a.hit_cap) hits[idx] = make_uint2(p, tn);
+    }
+    return n_hits + __popc(hb);
+}
+
+// The shared-memory views of the trie tables (the kernel's layout, ScanArgs).
+__device__ __forceinline__ Smem make_smem(const ScanArgs &a) {
+    extern __shared__ __align__(128) uint8_t smem_base[];
+    Smem s;
+    // terminal tables: shared-memory copies when staged (generic pointers)
+    s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem_base + a.off_terms) : a.t.out_ptr;
+    s.term_node = a.off_terms ? s.out_ptr + a.t.n_terminals + 1 : a.t.term_node;
+    s.root = reinterpret_cast<const uint32_t *>(smem_base + a.off_root);
+    s.bm = reinterpret_cast<const uint32_t *>(smem_base + a.off_bm);
+    s.node = reinterpret_cast<const uint32_t *>(smem_base + a.off_node);
+    s.aux = reinterpret_cast<const uint32_t *>(smem_base + a.off_aux);
+    s.label = smem_base + a.off_label;
+    s.tails = reinterpret_cast<const uint4 *>(smem_base + a.off_tails);
+    s.tail_bytes = smem_base + a.off_tbytes;
+    return s;
+}
+
+struct FlushOut {
+    uint32_t n_hits;  // hit records produced so far
+    uint32_t nb;      // walk-queue entries left
+    uint32_t rows;    // this lane's rows added in its warp's block
+};
+
+// Decide the queued starts dpos[0, n) (position order; dkey = kind-1 keys).
+// Two-level kinds move the probe survivors to the walk queue (bpos, bent, nb
+// entries) and walk it whenever it holds 32; `final` also walks the rest.
+// Not inlined: its registers do not weigh on the scan loop (it runs once per
+// few rounds).
+template <int Kind>
+__device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t cta_lo, uint64_t cta_round0,
+                                                uint32_t ctg_bytes, const uint32_t *dpos, const uint32_t *dkey,
+                                                uint32_t n, uint32_t *bpos, uint32_t *bent, uint32_t nb, bool final,
+                                                uint2 *hits, uint32_t n_hits) {
+    const ScanArgs &a = *ap;
+    const Smem s = make_smem(a);
+    const int lane = threadIdx.x & 31;
+    unsigned long long rows = 0;
     __syncwarp();
+    if (!two_level<Kind>(a)) {  // direct: walk every queued start
+        for (uint32_t j0 = 0; j0 < n; j0 += 32)
+            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, dpos + j0, nullptr, min(32u, n - j0), hits,
+                                      n_hits, rows);
+        __syncwarp();
+        return FlushOut{n_hits, 0u, (uint32_t)rows};
+    }
     for (uint32_t j0 = 0; j0 < n; j0 += 32) {
         const uint32_t j = j0 + lane;
-        uint32_t p = 0, tn = kNone;
+        uint32_t p = 0, ent = kNone;
         if (j < n) {
             p = dpos[j];
             const uint64_t gp = cta_lo + p;
             const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
-            // the exact key set rejects the filter's false positives before the walk
-            // (kind 1: the key was taken from the ring when queued; kind 3 reads
-            // it from the text: most of its probes hit and the walk follows)
-            if (Kind == 4 && a.use_entry) {
-                // enter at depth <= 8 through the entry table (a miss: no pattern starts here)
-                if (gt.end >= kGram8) {
-                    const uint2 en = entry_find(a, gt.at4(0), gt.at4(4));
-                    if (en.x) tn = walk(a, s, gt, 0u, en.x, en.y);
-                }
-            } else if (Kind == 3 && a.use_entry) {
-                // enter at depth <= 16 when the 16 bytes are A/C/G/T (the key
-                // aliases other bytes, and no DNA pattern can cover those)
-                if (gt.end >= kDnaGram) {
-                    uint32_t key = 0;
-                    bool acgt = true;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t w = gt.at4(4 * q);
-                        const uint32_t c = (w >> 1) & 0x03030303u;  // the four 2-bit codes, one per byte
-                        const uint32_t sel = (c & 0xFu) | ((c >> 4) & 0xF0u) | ((c >> 8) & 0xF00u) | ((c >> 12) & 0xF000u);
-                        acgt &= __byte_perm(0x47544341u, 0u, sel) == w;  // code -> 'A','C','T','G'
-                        key |= __umulhi((w & 0x06060606u) * 0x820820u, 1u << 8) << (8 * q);
-                    }
-                    if (acgt) {
-                        const uint2 en = entry_find(a, key, 0u);
-                        if (en.x) tn = walk(a, s, gt, 0u, en.x, en.y);
-                    }
-                }
-            } else if (Kind == 1 && a.use_kset ? kset_probe(a, dkey[j])
-                                               : (Kind == 3 && a.use_kset ? kset_has<Kind>(a, gt) : true)) {
-                tn = walk(a, s, gt, 0u);
-            }
-            if (tn != kNone) {
-                const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
-                if (p < ctg_bytes) rows += cnt;  // the lane's rows in its warp's block (per-warp totals)
-                else atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2), (unsigned long long)cnt);  // dynamic round
-            }
+            ent = probe_start<Kind>(a, gt, Kind == 1 ? dkey[j] : 0u);
         }
-        const bool hit = tn != kNone;
-        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-            const uint32_t idx = n_hits + __popc(hb & ((1u << lane) - 1u));
-            if (idx < a.hit_cap) hits[idx] = make_uint2(p, tn);
+        const uint32_t kb = __ballot_sync(0xffffffffu, ent != kNone);
+        if (ent != kNone) {
+            const uint32_t idx = nb + __popc(kb & ((1u << lane) - 1u));
+            bpos[idx] = p;
+            if (Kind != 1) bent[idx] = ent;
         }
-        n_hits += __popc(hb);
+        nb += __popc(kb);
+        if (nb >= 32) {  // walk the first 32, keep the rest (< 32) at the front
+            __syncwarp();
+            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, 32u,
+                                      hits, n_hits, rows);
+            uint32_t rp = 0, re = 0;
+            const bool mv = (uint32_t)lane + 32u < nb;
+            if (mv) {
+                rp = bpos[lane + 32];
+                if (Kind != 1) re = bent[lane + 32];
+            }
+            __syncwarp();
+            if (mv) {
+                bpos[lane] = rp;
+                if (Kind != 1) bent[lane] = re;
+            }
+            nb -= 32;
+            __syncwarp();
+        }
+    }
+    if (final && nb) {
+        __syncwarp();
+        n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, nb, hits,
+                                  n_hits, rows);
+        nb = 0;
     }
     __syncwarp();
-    return n_hits;
+    return FlushOut{n_hits, nb, (uint32_t)rows};
 }
 
 template <int Kind, int kSlots>
@@ -741,28 +842,23 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();  // barriers initialised
     STAMP(11);
-    Smem s;
-    // terminal tables: shared-memory copies when staged (generic pointers)
-    s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem + a.off_terms) : a.t.out_ptr;
-    s.term_node = a.off_terms ? s.out_ptr + a.t.n_terminals + 1 : a.t.term_node;
-    s.root = s_root;
-    s.bm = s_bm;
-    s.node = s_node;
-    s.aux = reinterpret_cast<const uint32_t *>(smem + a.off_aux);
-    s.label = s_label;
-    s.tails = reinterpret_cast<const uint4 *>(smem + a.off_tails);
-    s.tail_bytes = smem + a.off_tbytes;
-    // filter addressing: copies interleaved at the unit the kernel loads
-    // (kind 1: 8-byte block b of copy r at filter + 8*(b*rep + r); kinds 0
-    // and 2: word w of copy r at filter + 4*(w*rep + r)); lane l reads copy l % rep
-    // so the lanes of a phase spread over the banks
+    const Smem s = make_smem(a);
+    // filter addressing: kinds 0, 2, 3, 4: copies interleaved at the unit
+    // the kernel loads (8-byte block b of copy r at filter + 8*(b*rep + r);
+    // word w of copy r at filter + 4*(w*rep + r)); kind 1: copy r at filter +
+    // r * filter bytes, word w of it at position w ^ r.  Lane l reads copy
+    // l % rep, so the lanes of a phase spread over the banks.
     const uint32_t rep = 1u << a.rep_log2;
-    constexpr bool kBlock64 = Kind == 1 || Kind == 3 || Kind == 4;  // 64-bit two-bit blocks
+    constexpr bool kBlock64 = Kind == 3 || Kind == 4;  // 64-bit blocks
     const uint32_t unit = kBlock64 ? 8u : 4u;
     const uint32_t sW = 32u - (a.t.log2_bits - (kBlock64 ? 6u : 5u));  // block index = hash >> sW
-    const uint32_t sWmul = 1u << (32u - sW);                              // (hash * sWmul) >> 32 == hash >> sW
-    const uint32_t stride = rep * unit;
-    const uint32_t base_lane = smem_u32(smem) + ((uint32_t)lane & (rep - 1u)) * unit;
+    const uint32_t lane_copy = (uint32_t)lane & (rep - 1u);
+    const uint32_t fbytes = a.filter_words * 4u;
+    // kind 1: (word mask, copy term) in the (sWmul, stride) slots of filter32
+    const uint32_t sWmul = Kind == 1 ? (fbytes - 1u) & ~3u : 1u << (32u - sW);  // (hash * sWmul) >> 32 == hash >> sW
+    const uint32_t stride = Kind == 1 ? (lane_copy * fbytes) | (lane_copy * 4u) : rep * unit;
+    const uint32_t base_lane = smem_u32(smem) + (Kind == 1 ? 0u : lane_copy * unit);
+    const bool imm1024 = Kind == 1 && smem_u32(smem) == 1024u;  // the filter's base fits the LDS immediate
 
     const uint64_t policy = evict_first_policy();
     // starts < lim are valid: inside [0, n_starts) and their d-gram fits
@@ -879,7 +975,20 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         // (consecutive threads write consecutive units: no bank conflicts)
         // (8-16 loads in flight per thread: the image is cold in L2 here)
         const uint32_t nu = a.rep_log2 == 0 ? 0u : (kBlock64 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
-        if (kBlock64) {
+        if (Kind == 1) {  // copy r = j / words, position p = j % words holds word p ^ r
+            const uint32_t lw = (uint32_t)__ffs(a.filter_words) - 1u;
+            for (uint32_t j0 = 0; j0 < nu; j0 += 16 * kThreads) {
+                uint32_t v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const uint32_t j = j0 + tid + q * kThreads;
+                    v[q] = j < nu ? __ldg(a.t.filter + ((j & (a.filter_words - 1u)) ^ (j >> lw))) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (j0 + tid + q * kThreads < nu) s_filter[j0 + tid + q * kThreads] = v[q];
+            }
+        } else if (kBlock64) {
             const uint2 *src = reinterpret_cast<const uint2 *>(a.t.filter);
             uint2 *d = reinterpret_cast<uint2 *>(s_filter);
             for (uint32_t j0 = 0; j0 < nu; j0 += 8 * kThreads) {
@@ -949,17 +1058,20 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t n_hits = 0;  // hit records produced (warp-uniform; may exceed hit_cap)
     unsigned long long lane_rows = 0;  // rows of this lane's hits in the warp's block
     uint32_t dcount = 0;  // queued starts (warp-uniform)
+    uint32_t nb = 0;      // walk-queue entries (two-level kinds; warp-uniform)
     const uint32_t qcap = (Kind == 1 || Kind == 2) ? (uint32_t)kDefer : a.defer;  // queue capacity (per plan)
     uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * qcap;
     uint32_t *dkey = reinterpret_cast<uint32_t *>(smem + a.off_defer) + (kWarps + warp) * qcap;  // kind 1
+    // walk queue: positions (+ entry words, kinds 3/4)
+    uint32_t *bpos = reinterpret_cast<uint32_t *>(smem + a.off_walkq) + warp * (Kind == 1 ? kWalkQ : 2 * kWalkQ);
+    uint32_t *bent = bpos + kWalkQ;
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
     for (;;) {
         const bool done = rid[0] == kNoRound;
         const uint32_t rel = rid[0] * (uint32_t)kRound;  // round start relative to cta_lo
         const uint64_t rbase = cta_lo + rel;
         const uint8_t *p0 = ring + slot * kSlotBytes;
-        uint32_t pending = 0, tot = 0, r = 0;
-        bool single = false;
+        uint32_t pending = 0;
         if (!done) {
             // refill the slot of the previous round with the next round taken
             __syncwarp();  // every lane's reads of that slot precede its refill
@@ -998,7 +1110,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     ext[q] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound + 4 + 4 * q) : e;
                 }
             }
-            pending = filter32<Kind>(a, wv, ext, sW, sWmul, stride, base_lane);
+            pending = imm1024 ? filter32<Kind, true>(a, wv, ext, sW, sWmul, stride, base_lane)
+                              : filter32<Kind, false>(a, wv, ext, sW, sWmul, stride, base_lane);
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
@@ -1030,59 +1143,65 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 }
                 pending = km;
             }
-            if (__any_sync(0xffffffffu, pending != 0)) {
-                if (__any_sync(0xffffffffu, (pending & (pending - 1)) != 0)) {
-                    r = warp_excl_scan(__popc(pending), lane, &tot);
-                } else {
-                    single = true;  // at most one kept start per lane
-                    tot = 1;
-                }
-            }
-        }
-        // ---- queue the kept starts, 32 per pass; the single batch-walk site at its top
-        for (uint32_t cb = 0;; cb += 32) {
-            // kinds 1 and 3 (large sets: walks and key-set probes cost L2 round
-            // trips) flush only when this pass would not fit, for fuller
-            // batches (C4/C5 -2%); kind 2 flushes once fewer than 32 slots are
-            // left (C2: +1% the other way)
-            bool flush_now;
-            if (Kind == 1 || Kind == 3) {
-                const uint32_t kb0 = single ? __ballot_sync(0xffffffffu, pending != 0) : 0u;
-                const uint32_t need = cb >= tot ? 0u : (single ? __popc(kb0) : min(32u, tot - cb));
-                flush_now = dcount != 0 && (done || dcount + need > qcap);
+            // ---- queue the kept starts in position order (lane-major = position
+            // order; a warp's rounds increase): a warp scan of the per-lane
+            // counts (a ballot when no lane keeps two) gives each its slots
+            uint32_t ex, tot;
+            if (__any_sync(0xffffffffu, (pending & (pending - 1)) != 0)) {
+                ex = warp_excl_scan(__popc(pending), lane, &tot);
             } else {
-                flush_now = dcount != 0 && (done || dcount > qcap - 32);
-            }
-            if (flush_now) {
-#if defined(PFAC_EXP) && PFAC_EXP == 2
-                if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
-#else
-                n_hits = walk_deferred<Kind>(&a, s, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey, dcount, hits, n_hits,
-                                             lane_rows);
-#endif
-                dcount = 0;
-            }
-            if (cb >= tot) break;
-            if (single) {  // append by ballot (the queue has room for 32)
                 const uint32_t kb = __ballot_sync(0xffffffffu, pending != 0);
-                if (pending) {
-                    const uint32_t e = dcount + __popc(kb & ((1u << lane) - 1u));
-                    const uint32_t off = lane * kPerLane + (__ffs(pending) - 1);
-                    dpos[e] = rel + off;
-                    if (Kind == 1 && a.use_kset) dkey[e] = slot_key<Kind>(p0, off);
+                ex = __popc(kb & ((1u << lane) - 1u));
+                tot = __popc(kb);
+            }
+            if (tot) {
+                if (dcount + tot > qcap) {  // decide the queued starts first
+                    const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey,
+                                                             dcount, bpos, bent, nb, false, hits, n_hits);
+                    n_hits = fo.n_hits;
+                    nb = fo.nb;
+                    lane_rows += fo.rows;
+                    dcount = 0;
                 }
-                dcount += __popc(kb);
-                break;
+                if (tot <= qcap) {  // the common case: one pass
+                    uint32_t e = dcount + ex;
+                    for (uint32_t m = pending; m; m &= m - 1, ++e) {
+                        const uint32_t off = lane * kPerLane + (__ffs(m) - 1);
+                        dpos[e] = rel + off;
+                        if (Kind == 1 && a.use_kset) dkey[e] = slot_key<Kind>(p0, off);
+                    }
+                    dcount += tot;
+                    __syncwarp();
+                } else {  // more kept starts than the queue holds (dense matches): qcap at a time
+                    for (uint32_t c0 = 0; c0 < tot; c0 += qcap) {
+                        uint32_t e = ex;
+                        for (uint32_t m = pending; m; m &= m - 1, ++e) {
+                            if (e >= c0 && e < c0 + qcap) {
+                                const uint32_t off = lane * kPerLane + (__ffs(m) - 1);
+                                dpos[e - c0] = rel + off;
+                                if (Kind == 1 && a.use_kset) dkey[e - c0] = slot_key<Kind>(p0, off);
+                            }
+                        }
+                        const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey,
+                                                                 min(qcap, tot - c0), bpos, bent, nb, false, hits,
+                                                                 n_hits);
+                        n_hits = fo.n_hits;
+                        nb = fo.nb;
+                        lane_rows += fo.rows;
+                    }
+                }
             }
-            while (pending && r < cb + 32) {  // the next 32 in position order (the queue has room for 32)
-                const uint32_t off = lane * kPerLane + (__ffs(pending) - 1);
-                dpos[dcount + r - cb] = rel + off;
-                if (Kind == 1 && a.use_kset) dkey[dcount + r - cb] = slot_key<Kind>(p0, off);
-                pending &= pending - 1;
-                ++r;
-            }
-            __syncwarp();
-            dcount += min(32u, tot - cb);
+        } else if (dcount != 0 || nb != 0) {  // the warp's rounds are done: decide everything left
+#if defined(PFAC_EXP) && PFAC_EXP == 2
+            if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
+#else
+            const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey, dcount, bpos,
+                                                     bent, nb, true, hits, n_hits);
+            n_hits = fo.n_hits;
+            nb = fo.nb;
+            lane_rows += fo.rows;
+#endif
+            dcount = 0;
         }
         if (done) break;
 #pragma unroll
@@ -1308,7 +1427,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     if (lbase + 4 * q + b < a.readable) x |= (uint32_t)__ldg(a.text + lbase + 4 * q + b) << (8 * b);
                 if (q < kWv) wv[q] = x; else ext[q - kWv] = x;
             }
-            uint32_t surv = filter32<Kind>(a, wv, ext, sW, sWmul, stride, base_lane);
+            uint32_t surv = filter32<Kind, false>(a, wv, ext, sW, sWmul, stride, base_lane);
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
                 surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
@@ -1489,14 +1608,22 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     // walk-queue capacity: deeper for DNA (kind 3) and 8-byte-prefix (kind 4)
     // sets, whose walks are long (measured: C5 64 -4%, C3 96 -2.5%)
     const uint32_t defer = t.kind == 3 ? 64u : t.kind == 4 ? 96u : (uint32_t)kDefer;  // (kernel: kDefer for kinds 1, 2)
-    // the 2-gram test (and its 8 KiB table): not for DNA (every 2-gram begins
-    // a pattern, and the kernel has no stage 2 for kind 3)
-    const bool use_pair = t.kind != 3 && o.stage2 != 0;
+    // the 2-gram test (and its 8 KiB table): not for DNA (the kernel has no
+    // stage 2 for kind 3), and by default only where it is selective: at most
+    // a quarter of all 2-grams begin a pattern path (C2 1.5%, C3 5.8%; C4's
+    // random bytes 78%: the test would keep most survivors at a cost)
+    uint32_t pair_bits = 0;
+    {
+        const uint32_t *pair = reinterpret_cast<const uint32_t *>(host_image + hh.off_pair);
+        for (uint32_t j = 0; j < 2048; j++) pair_bits += (uint32_t)__builtin_popcount(pair[j]);
+    }
+    const bool use_pair = t.kind != 3 && (o.stage2 == 1 || (o.stage2 == -1 && pair_bits <= 65536u / 4));
     uint32_t slots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
     if (o.ring_slots > 0) slots = (uint32_t)o.ring_slots;
+    const uint32_t walkq = t.kind == 1 ? kWarps * kWalkQ * 4 : (t.kind == 3 || t.kind == 4) ? kWarps * 2 * kWalkQ * 4 : 0u;
     const uint32_t fixed = kWarps * slots * kSlotBytes + (kWarps * slots + 1) * 8 + 1024 +
                            kWarps * defer * (t.kind == 1 ? 8 : 4) + (use_pair ? 8192 : 0) + align16(40 * B) +
-                           8 * (kWarps + 2) + 512;
+                           8 * (kWarps + 2) + 512 + walkq;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac scan plan: filter and text ring do not fit shared memory";
         return kStatusLimit;
@@ -1546,6 +1673,7 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     off = align_up(off, 16);
     a.off_root = off;   off += 1024;
     a.off_defer = off;  off += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
+    a.off_walkq = off;  off += walkq;                                     // walk queues u32[2][kWalkQ]
     a.defer = defer;
     a.off_pair = off;   off += use_pair ? 8192 : 0;  // 2-gram prefix table [256][8] words
     a.use_pair = use_pair;

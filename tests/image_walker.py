@@ -70,10 +70,10 @@ def filter_bits(h, key):
     (all must be set for the start to survive)."""
     if h["filter_kind"] == 2:  # d = 4: pair filter, tested here as the first start of a pair
         raise ValueError("kind 2 tests depend on the start's parity; use filter_pass")
-    if h["filter_kind"] == 1:  # d = 4: blocked two-bit filter (image.h)
-        b = ((key * ((h["filter_mul"] << 8) & 0xFFFFFFFF)) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
-        h2 = ((key * 0x85EBCA6B) >> 32) & 31
-        return [2 * b * 32 + (31 - ((key >> 24) & 31)), 2 * b * 32 + (31 - h2), (2 * b + 1) * 32 + (31 - ((key >> 16) & 31))]
+    if h["filter_kind"] == 1:  # d = 4: blocked three-bit filter in 32-bit words (image.h)
+        mask = ((1 << (h["filter_log2_bits"] - 3)) - 1) & ~3
+        w = (((key * h["filter_mul"]) >> 32) & mask) // 4
+        return [w * 32 + (31 - ((key >> (8 * b)) & 31)) for b in (3, 2, 1)]
     return [filter_index(h, key)]
 
 
