@@ -491,14 +491,19 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
             if (x != kset_empty) break;
             kset_empty++;
         }
-        kset_log2 = 6;  // load <= 1/2: a miss probes ~2.5 slots, mostly in one 128-byte line
-        while ((1ull << kset_log2) < 2ull * keys.size()) kset_log2++;
+        kset_log2 = 6;  // load <= 1/4: a probe almost always reads one 16-byte bucket
+        while ((1ull << kset_log2) < 4ull * keys.size()) kset_log2++;
         kset.assign((size_t)1 << kset_log2, kset_empty);
-        const uint32_t mask = (1u << kset_log2) - 1u;
+        const uint32_t bmask = (1u << (kset_log2 - 2)) - 1u;
         for (uint32_t x : keys) {
-            uint32_t i = kset_slot(x, kset_log2);
-            while (kset[i] != kset_empty) i = (i + 1) & mask;
-            kset[i] = x;
+            for (uint32_t b = kset_bucket(x, kset_log2);; b = (b + 1) & bmask) {
+                uint32_t j = 0;
+                while (j < 4 && kset[4 * b + j] != kset_empty) j++;
+                if (j < 4) {
+                    kset[4 * b + j] = x;
+                    break;
+                }
+            }
         }
     }
 

@@ -93,12 +93,16 @@
 //                     tail/chain start (then every b1 is set).  Derived from
 //                     root + level1; the kernel tests survivors with it.
 //   kset   u32[2^kset_log2]  (filter kind 1) the exact set of the patterns'
-//                     filter keys (first 4 bytes little-endian): open
-//                     addressing, slot = (key * kFilterMul) >> (32 -
-//                     kset_log2), linear probing, empty slots hold kset_empty
-//                     (a value that is no key), load <= 1/2.  A start whose
-//                     key is absent cannot match: the walk is skipped (the
-//                     filter's false positives).
+//                     filter keys (first 4 bytes little-endian) in buckets
+//                     of 4 slots (16 bytes, one load): a key lives in the
+//                     first bucket from its home bucket (key * kFilterMul)
+//                     >> (32 - (kset_log2 - 2)) with a free slot (linear
+//                     probing over buckets); empty slots hold kset_empty (a
+//                     value that is no key); load <= 1/4.  A probe reads
+//                     buckets from home until it finds the key (present) or
+//                     an empty slot (absent).  A start whose key is absent
+//                     cannot match: the walk is skipped (the filter's false
+//                     positives).
 //   entry  u32[2^entry_log2][4]  (filter kinds 4 and 3; D = the filter gram:
 //                     8 bytes, or 16 DNA bases; every pattern has >= D bytes)
 //                     the entry table: one entry {x0, x1, node, depth} per
@@ -125,7 +129,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 15;
+constexpr uint32_t kVersion = 16;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -158,8 +162,8 @@ struct ImageHeader {
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 
-// First slot of a key in the exact key set.
-PFAC_HD inline uint32_t kset_slot(uint32_t key, uint32_t log2) { return (key * kFilterMul) >> (32u - log2); }
+// Home bucket (4 slots) of a key in the exact key set of 2^log2 slots.
+PFAC_HD inline uint32_t kset_bucket(uint32_t key, uint32_t log2) { return (key * kFilterMul) >> (34u - log2); }
 // First slot of a key (x0, x1) in the entry table.
 PFAC_HD inline uint32_t entry_slot(uint32_t x0, uint32_t x1, uint32_t log2) {
     return (x0 * kFilterMul + x1 * kFilterMul2) >> (32u - log2);

@@ -593,24 +593,17 @@ __device__ __forceinline__ uint32_t slot_key(const uint8_t *slot, uint32_t off) 
     }
     return __funnelshift_r(w[0], w[1], sh);
 }
-// Probe the exact key set for a key (open addressing, linear probing, no
-// deletions).  One 16-byte load answers the key's home slot and the rest of
-// its 4-slot group: the key anywhere in the group means present (a key is
-// never stored before its home slot, and a group never wraps the table);
-// an empty slot at or after the home slot means absent; else the next group.
+// Probe the exact key set for a key (image.h: buckets of 4 slots, one
+// 16-byte load each): present if a slot holds the key, absent if a slot is
+// empty, else the next bucket (rare at load <= 1/4).
 __device__ __forceinline__ bool kset_probe(const ScanArgs &a, uint32_t key) {
-    const uint32_t mask = (1u << a.t.kset_log2) - 1u;
+    const uint32_t bmask = (1u << (a.t.kset_log2 - 2u)) - 1u;
     const uint4 *k4 = reinterpret_cast<const uint4 *>(a.t.kset);
-    uint32_t i = kset_slot(key, a.t.kset_log2);
-    uint32_t from = i & 3u;
-    for (;;) {
-        const uint4 q = __ldg(k4 + (i >> 2));
-        if (q.x == key || q.y == key || q.z == key || q.w == key) return true;
-        const uint32_t e = a.t.kset_empty;
-        const uint32_t emp = (q.x == e ? 1u : 0u) | (q.y == e ? 2u : 0u) | (q.z == e ? 4u : 0u) | (q.w == e ? 8u : 0u);
-        if (emp >> from) return false;
-        i = ((i | 3u) + 1u) & mask;
-        from = 0;
+    const uint32_t e = a.t.kset_empty;
+    for (uint32_t b = kset_bucket(key, a.t.kset_log2);; b = (b + 1u) & bmask) {
+        const uint4 q = __ldg(k4 + b);
+        if ((q.x == key) | (q.y == key) | (q.z == key) | (q.w == key)) return true;
+        if ((q.x == e) | (q.y == e) | (q.z == e) | (q.w == e)) return false;
     }
 }
 

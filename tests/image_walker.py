@@ -174,14 +174,17 @@ def walk(h, text, i, L, v0=None, d0=1):
 
 
 def kset_has(h, key):
-    """Exact key set probe (linear probing from (key * M) >> (32 - log2))."""
+    """Exact key set probe (image.h): buckets of 4 slots from the home bucket
+    (key * M) >> (34 - log2) until the key (present) or an empty slot (absent)."""
     t, lg = h["kset"], h["kset_log2"]
-    i = ((key * 0x9E3779B1) & 0xFFFFFFFF) >> (32 - lg)
-    while int(t[i]) != h["kset_empty"]:
-        if int(t[i]) == key:
+    b = ((key * 0x9E3779B1) & 0xFFFFFFFF) >> (34 - lg)
+    while True:
+        q = [int(x) for x in t[4 * b:4 * b + 4]]
+        if key in q:
             return True
-        i = (i + 1) & ((1 << lg) - 1)
-    return False
+        if h["kset_empty"] in q:
+            return False
+        b = (b + 1) & ((1 << (lg - 2)) - 1)
 
 
 def match(h, text: bytes, readable=None, n_starts=None):
