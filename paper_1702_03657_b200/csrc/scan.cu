@@ -70,7 +70,26 @@ constexpr uint32_t kFilterCap = 65536;  // max shared bytes for the replicated f
 #ifndef PFAC_DEFER
 #define PFAC_DEFER 48
 #endif
-constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to walk (kinds 1, 2; see defer_for)
+constexpr int kDefer = PFAC_DEFER;             // per-warp queue of starts to walk (kinds 0, 1, 2)
+constexpr uint32_t kWalkQ = 64;                // walk-queue capacity per warp (two-level kinds)
+
+// Per-warp region of shared memory (one base per warp; every part at a
+// compile-time offset from it): the TMA text ring, its mbarriers, the queue
+// of kept starts (+ their keys, kind 1) and the walk queue (+ entry words,
+// kinds 3/4).
+__host__ __device__ constexpr uint32_t defer_cap(int kind) {
+    return kind == 3 ? 64u : kind == 4 ? 96u : (uint32_t)kDefer;  // deeper for DNA / 8-byte prefixes (long walks)
+}
+struct WarpLayout {
+    uint32_t ring, bars, dpos, dkey, bpos, bent, bytes;
+};
+__host__ __device__ constexpr WarpLayout warp_layout(int kind, int slots) {
+    const uint32_t ring = 0, bars = ring + slots * kSlotBytes, dpos = bars + 8u * slots,
+                   dkey = dpos + 4u * defer_cap(kind), bpos = dkey + (kind == 1 ? 4u * defer_cap(kind) : 0u),
+                   bent = bpos + ((kind == 1 || kind == 3 || kind == 4) ? 4u * kWalkQ : 0u),
+                   end = bent + ((kind == 3 || kind == 4) ? 4u * kWalkQ : 0u);
+    return WarpLayout{ring, bars, dpos, dkey, bpos, bent, (end + 15u) & ~15u};
+}
 constexpr uint64_t kSmallTrie = 160u << 10;  // a trie this small fits shared memory whole
 constexpr uint64_t kBigL1Trie = 1u << 20;    // "big L1" plan up to this trie size (see launch_scan)
 
@@ -111,9 +130,8 @@ struct ScanArgs {
     // shared-memory layout (bytes from the dynamic smem base; filter at 0)
     uint32_t filter_words;          // words of the (unreplicated) filter
     uint32_t rep_log2;              // replication factor 2^rep_log2 (<= 32)
-    uint32_t off_root, off_node, off_label, off_ring, off_bar, off_warp, off_bm, off_defer, off_pair, off_aux;
+    uint32_t off_root, off_node, off_label, off_warps, off_sbar, off_warp, off_bm, off_pair, off_aux;
     uint32_t off_tails, off_tbytes;
-    uint32_t off_walkq;             // per-warp walk queue u32[2][kWalkQ] (two-level kinds)
     uint32_t hot_tails, hot_tail_bytes;  // records (and their bytes) of the record nodes < H
     uint32_t off_terms;             // out_ptr[T+1] + term_node[TK] in smem (0 = in global memory)
     uint32_t n_level1;              // B: the root's children are nodes [1, B]
@@ -123,7 +141,6 @@ struct ScanArgs {
     uint32_t use_kset;              // probe the exact key set before walks (trie not wholly in smem)
     uint32_t ctg64;                 // share of a CTA's rounds in contiguous per-warp blocks, in 64ths
                                     // (the rest, the range's end, is handed out dynamically)
-    uint32_t defer;                 // walk-queue capacity per warp (>= 33)
     uint32_t use_pair;              // the 2-gram prefix table is staged and tested
     uint32_t use_entry;            // kind 4: walks enter through the depth-8 entry table
 };
@@ -628,7 +645,6 @@ __device__ __forceinline__ uint2 entry_find(const ScanArgs &a, uint32_t x0, uint
 //    (with the entry node and depth to walk from) and are walked 32 at a time
 //    by the full warp, so a walk never runs with a lane or two of 32.
 constexpr uint32_t kEntShift = 27;  // walk-queue entry word: node | depth << 27 (0 = from the root)
-constexpr uint32_t kWalkQ = 64;     // walk-queue capacity per warp
 
 template <int Kind>
 __device__ __forceinline__ bool two_level(const ScanArgs &a) {
@@ -799,15 +815,17 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t *s_root = reinterpret_cast<uint32_t *>(smem + a.off_root);
     uint32_t *s_node = reinterpret_cast<uint32_t *>(smem + a.off_node);
     uint8_t *s_label = smem + a.off_label;
-    uint8_t *ring = smem + a.off_ring + (uint32_t)warp * (kSlots * kSlotBytes);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.off_bar) + warp * kSlots;
+    constexpr WarpLayout WL = warp_layout(Kind, kSlots);
+    uint8_t *const wsm = smem + a.off_warps + (uint32_t)warp * WL.bytes;  // this warp's region
+    uint8_t *ring = wsm + WL.ring;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wsm + WL.bars);
     unsigned long long *s_wtot = reinterpret_cast<unsigned long long *>(smem + a.off_warp);  // [kWarps + 2]
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
 
     STAMP(0);
     // ---- barriers: per-warp text ring + one for the table staging; thread 0
     // starts the table copies (TMA bulk, evict-last) before anything else
-    uint64_t *sbar = reinterpret_cast<uint64_t *>(smem + a.off_bar) + kWarps * kSlots;
+    uint64_t *sbar = reinterpret_cast<uint64_t *>(smem + a.off_sbar);
     if (tid == 0) {
         mbar_init(sbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -886,10 +904,11 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t taken = 0;
     const uint32_t wq = n_ctg / kWarps, wrem = n_ctg % kWarps;
     const uint32_t wbeg = warp * wq + min((uint32_t)warp, wrem), wend = wbeg + wq + ((uint32_t)warp < wrem ? 1u : 0u);
+    uint32_t wnext = wbeg;  // the warp's next block round
     auto take = [&]() -> uint32_t {
         uint32_t r;
-        if (wbeg + taken < wend) {
-            r = wbeg + taken;
+        if (wnext < wend) {
+            r = wnext++;
         } else {
             r = 0;
             if (lane == 0) {
@@ -1052,12 +1071,12 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     unsigned long long lane_rows = 0;  // rows of this lane's hits in the warp's block
     uint32_t dcount = 0;  // queued starts (warp-uniform)
     uint32_t nb = 0;      // walk-queue entries (two-level kinds; warp-uniform)
-    const uint32_t qcap = (Kind == 1 || Kind == 2) ? (uint32_t)kDefer : a.defer;  // queue capacity (per plan)
-    uint32_t *dpos = reinterpret_cast<uint32_t *>(smem + a.off_defer) + warp * qcap;
-    uint32_t *dkey = reinterpret_cast<uint32_t *>(smem + a.off_defer) + (kWarps + warp) * qcap;  // kind 1
+    constexpr uint32_t qcap = defer_cap(Kind);  // queue capacity
+    uint32_t *dpos = reinterpret_cast<uint32_t *>(wsm + WL.dpos);
+    uint32_t *dkey = reinterpret_cast<uint32_t *>(wsm + WL.dkey);  // kind 1
     // walk queue: positions (+ entry words, kinds 3/4)
-    uint32_t *bpos = reinterpret_cast<uint32_t *>(smem + a.off_walkq) + warp * (Kind == 1 ? kWalkQ : 2 * kWalkQ);
-    uint32_t *bent = bpos + kWalkQ;
+    uint32_t *bpos = reinterpret_cast<uint32_t *>(wsm + WL.bpos);
+    uint32_t *bent = reinterpret_cast<uint32_t *>(wsm + WL.bent);
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
     for (;;) {
         const bool done = rid[0] == kNoRound;
@@ -1302,7 +1321,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // The pool's rows follow every range's: its counts are complete only now.
     // CTA b scans pool segment b in place, a second grid barrier, then every
     // CTA holds each segment's first row (s_pool, in the idle ring).
-    unsigned long long *s_pool = reinterpret_cast<unsigned long long *>(smem + a.off_ring);
+    unsigned long long *s_pool = reinterpret_cast<unsigned long long *>(smem + a.off_warps);
     const uint32_t pool_lo = (uint32_t)(a.n_main - cta_round0), pool_hi = (uint32_t)(n_rounds - cta_round0);
     if (kPool && a.pool_seg) {
         const unsigned long long all_main = s_wtot[kWarps + 1];
@@ -1598,9 +1617,6 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     bool big_l1 = (t.kind == 1 || t.kind == 3 || t.kind == 4) && whole > kSmallTrie && whole <= kBigL1Trie;
     if (o.placement == PFAC_PLACE_BIG_L1) big_l1 = true;
     if (o.placement == PFAC_PLACE_GLOBAL || o.placement == PFAC_PLACE_SMEM) big_l1 = false;
-    // walk-queue capacity: deeper for DNA (kind 3) and 8-byte-prefix (kind 4)
-    // sets, whose walks are long (measured: C5 64 -4%, C3 96 -2.5%)
-    const uint32_t defer = t.kind == 3 ? 64u : t.kind == 4 ? 96u : (uint32_t)kDefer;  // (kernel: kDefer for kinds 1, 2)
     // the 2-gram test (and its 8 KiB table): not for DNA (the kernel has no
     // stage 2 for kind 3), and by default only where it is selective: at most
     // a quarter of all 2-grams begin a pattern path (C2 1.5%, C3 5.8%; C4's
@@ -1613,10 +1629,12 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     const bool use_pair = t.kind != 3 && (o.stage2 == 1 || (o.stage2 == -1 && pair_bits <= 65536u / 4));
     uint32_t slots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
     if (o.ring_slots > 0) slots = (uint32_t)o.ring_slots;
-    const uint32_t walkq = t.kind == 1 ? kWarps * kWalkQ * 4 : (t.kind == 3 || t.kind == 4) ? kWarps * 2 * kWalkQ * 4 : 0u;
-    const uint32_t fixed = kWarps * slots * kSlotBytes + (kWarps * slots + 1) * 8 + 1024 +
-                           kWarps * defer * (t.kind == 1 ? 8 : 4) + (use_pair ? 8192 : 0) + align16(40 * B) +
-                           8 * (kWarps + 2) + 512 + walkq;
+    // per-warp regions (ring, barriers, queues): the kernel's warp_layout
+    // (queues deeper for DNA and 8-byte prefixes, whose walks are long:
+    // measured C5 64 -4%, C3 96 -2.5%)
+    const uint32_t warp_bytes = warp_layout((int)t.kind, (int)slots).bytes;
+    const uint32_t fixed = kWarps * warp_bytes + 16 + 1024 + (use_pair ? 8192 : 0) + align16(40 * B) +
+                           8 * (kWarps + 2) + 512;
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac scan plan: filter and text ring do not fit shared memory";
         return kStatusLimit;
@@ -1660,14 +1678,11 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     a.filter_words = filter_words;
     a.rep_log2 = rep_log2;
     uint32_t off = align_up(filter_bytes, 128);
-    a.off_ring = off;   off += kWarps * slots * kSlotBytes;
-    a.off_bar = off;    off += (kWarps * slots + 1) * 8;
+    a.off_warps = off;  off += kWarps * warp_bytes;  // per-warp regions (warp_layout)
+    a.off_sbar = off;   off += 16;                   // the table-staging mbarrier
     a.off_warp = off;   off += 8 * (kWarps + 2);  // warp totals [kWarps + 2] (the last: the CTA's round counter first)
     off = align_up(off, 16);
     a.off_root = off;   off += 1024;
-    a.off_defer = off;  off += kWarps * defer * (t.kind == 1 ? 8 : 4);  // queue u32[defer] (+ kind-1 keys)
-    a.off_walkq = off;  off += walkq;                                     // walk queues u32[2][kWalkQ]
-    a.defer = defer;
     a.off_pair = off;   off += use_pair ? 8192 : 0;  // 2-gram prefix table [256][8] words
     a.use_pair = use_pair;
     a.off_bm = off;     off += align16(40 * B);
