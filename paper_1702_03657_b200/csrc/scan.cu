@@ -1717,13 +1717,15 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     // walks through a wholly staged trie are short and even: (almost) all
     // rounds in per-warp blocks; else the last quarter is handed out
     // dynamically (measured: C3 -11% dynamic)
-    a.ctg64 = o.ctg64 >= 0 ? (uint32_t)o.ctg64 : (H >= t.n_nodes - 1 ? 64u : 48u);
+    // (kind 1, large sets of random-looking byte patterns: even work per
+    // round, so every CTA range is static and only the pool balances: C4 -2%)
+    a.ctg64 = o.ctg64 >= 0 ? (uint32_t)o.ctg64 : (H >= t.n_nodes - 1 || t.kind == 1 ? 64u : 48u);
     // the shared pool: the text's last rounds, taken by any warp whose CTA's
     // range is done (cross-CTA balance where walks leave the SM: content
     // skew between ranges, e.g. C5's first ranges hold twice the matches);
     // planned when start offsets from a CTA's first round fit 32 bits
     {
-        const uint64_t pool64 = o.pool64 >= 0 ? (uint64_t)o.pool64 : (a.ctg64 < 64 ? 4u : 0u);
+        const uint64_t pool64 = o.pool64 >= 0 ? (uint64_t)o.pool64 : (a.ctg64 < 64 || t.kind == 1 ? 4u : 0u);
         const uint64_t n_pool = geo.n_rounds * pool64 / 64;
         const bool pool = t.kind != 2 && n_pool >= geo.grid && geo.n_rounds * (uint64_t)kRound <= (1ull << 32);
         a.n_main = pool ? geo.n_rounds - n_pool : geo.n_rounds;
