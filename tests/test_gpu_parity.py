@@ -18,13 +18,13 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 
 
-def gpu_rows(trie, text_np, readable=None, n_starts=None, pos_base=0, offset=0):
+def gpu_rows(trie, text_np, readable=None, n_starts=None, pos_base=0, offset=0, **plan):
     """Scan via the C ABI; `offset` shifts the text start inside the buffer
-    to exercise unaligned device pointers."""
+    to exercise unaligned device pointers; `plan` = pfac_plan_options fields."""
     buf = torch.zeros(len(text_np) + offset + 16, dtype=torch.uint8)
-    buf[offset:offset + len(text_np)] = torch.from_numpy(np.asarray(text_np, np.uint8))
+    buf[offset:offset + len(text_np)] = torch.from_numpy(np.array(text_np, np.uint8))
     d = buf.to(DEV)[offset:offset + len(text_np)]
-    pos, pid = trie.match(d, readable_len=readable, n_starts=n_starts, pos_base=pos_base)
+    pos, pid = trie.match(d, readable_len=readable, n_starts=n_starts, pos_base=pos_base, **plan)
     return pos.cpu().numpy().astype(np.uint64), pid.cpu().numpy().astype(np.uint32)
 
 
@@ -125,20 +125,24 @@ def test_capacity_overflow_and_count():
     assert np.array_equal(sc.pid[:100].cpu().numpy().astype(np.uint32), want_q[:100])
 
 
-def test_round_pool_and_overflow():
-    """A trie too large for shared memory (C4's 100,000 patterns) plans
-    dynamic rounds and the shared round pool (the text's last 1/16); dense
-    'a' runs in a CTA range and in the pool overflow the warps' hit lists,
-    so the re-scan fallback runs over block, dynamic and pool rounds."""
+@pytest.mark.parametrize("plan", [{}, {"ctg64": 48}, {"ctg64": 32, "pool64": 8}], ids=["auto", "ctg48", "ctg32-pool8"])
+def test_round_pool_and_overflow(plan):
+    """A trie too large for shared memory (C4's 100,000 patterns) plans the
+    shared round pool (the text's last 1/16) and, with ctg64 < 64, dynamic
+    rounds; dense 'a' runs in a CTA range and in the pool overflow the warps'
+    hit lists, so the re-scan fallback runs over block, dynamic and pool
+    rounds."""
     ps = gen.patterns(4).to_list() + [b"a" * k for k in range(4, 9)]
     n = 4 << 20
     text = gen.text(4, 0, n).copy()
     text[n // 3:n // 3 + (64 << 10)] = ord("a")
     text[n - (256 << 10):n - 1000] = ord("a")
     t = pf.Trie(ps)
+    p = t.plan(n, **plan)
+    assert p["pool_rounds"] > 0
     want = oracle.Trie(ps).match(text)
-    assert_same(gpu_rows(t, text), want, "pool + overflow")
-    assert_same(gpu_rows(t, text, offset=3), want, "pool + overflow, unaligned")
+    assert_same(gpu_rows(t, text, **plan), want, "pool + overflow")
+    assert_same(gpu_rows(t, text, offset=3, **plan), want, "pool + overflow, unaligned")
 
 
 @pytest.mark.parametrize("kind", ["nested", "zero_bytes", "long", "len1", "len2", "dups"])
