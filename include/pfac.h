@@ -178,9 +178,19 @@ pfac_status pfac_attach(const void *image, uint64_t size, int device, pfac_trie 
 
 /* ------------------------------------------------------------ match, host */
 
-/* Matches `text` (HOST memory, len bytes) on the current CUDA device:
- * H2D copy, scan, D2H of the sorted (pos, pid) rows.  Synchronous.
- * len == 0 gives count 0.  Returns CUDA on any device failure. */
+/* Matches `text` (HOST memory, len bytes) on the current CUDA device and
+ * returns the sorted (pos, pid) rows in host memory.  Synchronous.
+ * The text streams through the device in chunks (the host/device
+ * transition of PAPER.md:99 and the "first memory transfer" of PAPER.md:76):
+ * chunk i (PFAC_STREAM_CHUNK starts + the (max_len - 1)-byte halo of
+ * PAPER.md:66) is copied host->device on a copy stream while chunk i-1 is
+ * scanned on a compute stream (three device text buffers), so the scan hides
+ * behind the copy.  Page-locked `text` (cudaHostAlloc / registered memory) is
+ * copied directly; pageable text goes through the handle's pinned staging
+ * buffers (a host memcpy per chunk, overlapped with the device work).  Per-
+ * chunk results concatenate in chunk order (start ranges are disjoint and
+ * ordered).  len == 0 gives count 0.  Returns CUDA on any device failure. */
+#define PFAC_STREAM_CHUNK (64ull << 20)
 pfac_status pfac_match(const pfac_trie *t, const uint8_t *text, uint64_t len, pfac_matches *out);
 
 void pfac_matches_free(pfac_matches *m);

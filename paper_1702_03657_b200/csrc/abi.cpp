@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -17,19 +18,25 @@
 
 using namespace pfac;
 
-// Device buffers pfac_match (host API) keeps between calls, per device.
+// Device state pfac_match (host API) keeps between calls, per device: the
+// streaming pipeline's streams, events, text buffers (chunk + halo each),
+// pinned staging buffers (pageable input), workspace, per-chunk outputs.
+constexpr int kStreamBufs = 3;
 struct HostCtx {
     std::mutex mu;  // one pfac_match at a time per handle and device
-    cudaStream_t st = nullptr;
-    uint8_t *d_text = nullptr;
-    uint64_t text_cap = 0;
+    cudaStream_t copy = nullptr, comp = nullptr;
+    cudaEvent_t copied[kStreamBufs] = {}, scanned[kStreamBufs] = {};
+    uint8_t *d_text[kStreamBufs] = {};
+    uint8_t *h_stage[kStreamBufs] = {};
+    uint64_t text_cap = 0, stage_cap = 0;
     void *d_ws = nullptr;
     uint64_t ws_cap = 0;
-    uint64_t *d_pos = nullptr;
+    uint64_t *d_pos = nullptr;  // chunk c's rows at [c * per_chunk, ...)
     uint32_t *d_pid = nullptr;
     uint64_t out_cap = 0;
-    uint64_t *d_count = nullptr;
-    uint64_t *h_count = nullptr;  // pinned
+    uint64_t *d_count = nullptr;  // per chunk
+    uint64_t *h_count = nullptr;  // pinned, per chunk
+    uint64_t count_cap = 0;
 };
 
 struct pfac_trie {
@@ -203,10 +210,18 @@ void pfac_free(pfac_trie *t) {
         if (!have) break;
         HostCtx &c = *kv.second;
         cudaSetDevice(kv.first);
-        if (c.st) cudaStreamSynchronize(c.st);
-        cudaFree(c.d_text); cudaFree(c.d_ws); cudaFree(c.d_pos); cudaFree(c.d_pid); cudaFree(c.d_count);
+        if (c.copy) cudaStreamSynchronize(c.copy);
+        if (c.comp) cudaStreamSynchronize(c.comp);
+        for (int b = 0; b < kStreamBufs; b++) {
+            cudaFree(c.d_text[b]);
+            cudaFreeHost(c.h_stage[b]);
+            if (c.copied[b]) cudaEventDestroy(c.copied[b]);
+            if (c.scanned[b]) cudaEventDestroy(c.scanned[b]);
+        }
+        cudaFree(c.d_ws); cudaFree(c.d_pos); cudaFree(c.d_pid); cudaFree(c.d_count);
         cudaFreeHost(c.h_count);
-        if (c.st) cudaStreamDestroy(c.st);
+        if (c.copy) cudaStreamDestroy(c.copy);
+        if (c.comp) cudaStreamDestroy(c.comp);
     }
     if (have) cudaSetDevice(prev);
     delete t;
@@ -361,23 +376,50 @@ pfac_status pfac_match(const pfac_trie *t, const uint8_t *text, uint64_t len, pf
     }
     HostCtx &c = *cp;
     std::lock_guard<std::mutex> lk(c.mu);
-    if (!c.st) {
-        if ((e = cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaMalloc(&c.d_count, 8)) != cudaSuccess || (e = cudaMallocHost(&c.h_count, 8)) != cudaSuccess)
-            return cuda_fail("pfac_match: stream/allocation", e);
+    // ---- geometry: chunks of PFAC_STREAM_CHUNK starts, each read with its halo
+    const uint64_t C = PFAC_STREAM_CHUNK, halo = t->hdr.max_len - 1;
+    const uint64_t n_chunks = (len + C - 1) / C;
+    const uint64_t buf_bytes = (std::min(len, C + halo) + 15) & ~15ull;
+    const uint64_t per_chunk = std::min(len, C) / 256 + 4096;  // row capacity per chunk (count-and-retry above)
+    const int nbuf = (int)std::min<uint64_t>(n_chunks, kStreamBufs);
+    cudaPointerAttributes attr;
+    bool pinned = cudaPointerGetAttributes(&attr, text) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // (a plain pageable pointer is not an error)
+    // ---- grow-only state
+    if (!c.copy) {
+        if ((e = cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c.comp, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail("pfac_match: streams", e);
+        for (int b = 0; b < kStreamBufs; b++)
+            if ((e = cudaEventCreateWithFlags(&c.copied[b], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&c.scanned[b], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail("pfac_match: events", e);
     }
-    // grow-only device buffers
-    if (len > c.text_cap) {
-        cudaFree(c.d_text);
-        c.d_text = nullptr;
+    if (buf_bytes > c.text_cap) {
+        for (int b = 0; b < kStreamBufs; b++) {
+            cudaFree(c.d_text[b]);
+            c.d_text[b] = nullptr;
+        }
         c.text_cap = 0;
-        if ((e = cudaMalloc(&c.d_text, len)) != cudaSuccess) return cuda_fail("pfac_match: text buffer", e);
-        c.text_cap = len;
+        for (int b = 0; b < kStreamBufs; b++)
+            if ((e = cudaMalloc(&c.d_text[b], buf_bytes)) != cudaSuccess) return cuda_fail("pfac_match: text buffers", e);
+        c.text_cap = buf_bytes;
+    }
+    if (!pinned && buf_bytes > c.stage_cap) {
+        for (int b = 0; b < kStreamBufs; b++) {
+            cudaFreeHost(c.h_stage[b]);
+            c.h_stage[b] = nullptr;
+        }
+        c.stage_cap = 0;
+        for (int b = 0; b < kStreamBufs; b++)
+            if ((e = cudaMallocHost(&c.h_stage[b], buf_bytes)) != cudaSuccess)
+                return cuda_fail("pfac_match: pinned staging", e);
+        c.stage_cap = buf_bytes;
     }
     uint64_t ws_bytes = 0;
     {
         std::string err;
-        int st = workspace_bytes_for(len, dev, &ws_bytes, err);
+        int st = workspace_bytes_for(std::min(len, C), dev, &ws_bytes, err);
         if (st != kStatusOk) return fail(st, err);
     }
     if (ws_bytes > c.ws_cap) {
@@ -385,52 +427,113 @@ pfac_status pfac_match(const pfac_trie *t, const uint8_t *text, uint64_t len, pf
         c.d_ws = nullptr;
         c.ws_cap = 0;
         if ((e = cudaMalloc(&c.d_ws, ws_bytes)) != cudaSuccess ||
-            (e = cudaMemsetAsync(c.d_ws, 0, ws_bytes, c.st)) != cudaSuccess)
+            (e = cudaMemsetAsync(c.d_ws, 0, ws_bytes, c.comp)) != cudaSuccess)
             return cuda_fail("pfac_match: workspace", e);
         c.ws_cap = ws_bytes;
     }
-    auto ensure_out = [&](uint64_t cap) -> cudaError_t {
-        if (cap <= c.out_cap) return cudaSuccess;
+    if (n_chunks * per_chunk > c.out_cap) {
         cudaFree(c.d_pos);
         cudaFree(c.d_pid);
         c.d_pos = nullptr;
         c.d_pid = nullptr;
         c.out_cap = 0;
-        cudaError_t r = cudaMalloc(&c.d_pos, cap * 8);
-        if (r == cudaSuccess) r = cudaMalloc(&c.d_pid, cap * 4);
-        if (r == cudaSuccess) c.out_cap = cap;
-        return r;
-    };
-    if ((e = ensure_out(len / 256 + 4096)) != cudaSuccess) return cuda_fail("pfac_match: output buffers", e);
-    if ((e = cudaMemcpyAsync(c.d_text, text, len, cudaMemcpyHostToDevice, c.st)) != cudaSuccess)
-        return cuda_fail("pfac_match: H2D", e);
-    uint64_t count = 0;
-    for (int attempt = 0; attempt < 2; attempt++) {
-        rs = pfac_match_device(t, dev, c.d_text, len, len, 0, c.d_pos, c.d_pid, c.out_cap, c.d_count, c.d_ws,
-                               c.ws_cap, reinterpret_cast<pfac_stream>(c.st));
-        if (rs != PFAC_OK) return rs;
-        if ((e = cudaMemcpyAsync(c.h_count, c.d_count, 8, cudaMemcpyDeviceToHost, c.st)) != cudaSuccess ||
-            (e = cudaStreamSynchronize(c.st)) != cudaSuccess)
-            return cuda_fail("pfac_match: scan", e);
-        count = *c.h_count;
-        if (count <= c.out_cap) break;
-        if (attempt == 1) return fail(kStatusCapacity, "pfac_match: capacity retry failed");
-        if ((e = ensure_out(count)) != cudaSuccess) return cuda_fail("pfac_match: output buffers", e);
+        if ((e = cudaMalloc(&c.d_pos, n_chunks * per_chunk * 8)) != cudaSuccess ||
+            (e = cudaMalloc(&c.d_pid, n_chunks * per_chunk * 4)) != cudaSuccess)
+            return cuda_fail("pfac_match: output buffers", e);
+        c.out_cap = n_chunks * per_chunk;
     }
-    if (count == 0) return PFAC_OK;
-    out->pos = static_cast<uint64_t *>(std::malloc(count * 8));
-    out->pid = static_cast<uint32_t *>(std::malloc(count * 4));
+    if (n_chunks > c.count_cap) {
+        cudaFree(c.d_count);
+        cudaFreeHost(c.h_count);
+        c.d_count = nullptr;
+        c.h_count = nullptr;
+        c.count_cap = 0;
+        if ((e = cudaMalloc(&c.d_count, 8 * n_chunks)) != cudaSuccess ||
+            (e = cudaMallocHost(&c.h_count, 8 * n_chunks)) != cudaSuccess)
+            return cuda_fail("pfac_match: counts", e);
+        c.count_cap = n_chunks;
+    }
+    // ---- the pipeline: copy chunk i on `copy` while chunk i-1 scans on `comp`
+    auto chunk = [&](uint64_t i, uint64_t &s0, uint64_t &ns, uint64_t &rd) {
+        s0 = i * C;
+        ns = std::min(C, len - s0);
+        rd = std::min(len - s0, ns + halo);
+    };
+    for (uint64_t i = 0; i < n_chunks; i++) {
+        const int b = (int)(i % (uint64_t)nbuf);
+        uint64_t s0, ns, rd;
+        chunk(i, s0, ns, rd);
+        if (i >= (uint64_t)nbuf && (e = cudaStreamWaitEvent(c.copy, c.scanned[b], 0)) != cudaSuccess)
+            return cuda_fail("pfac_match: pipeline", e);
+        const uint8_t *src = text + s0;
+        if (!pinned) {  // pageable: through pinned staging (buffer b is free once its last copy is done)
+            if (i >= (uint64_t)nbuf && (e = cudaEventSynchronize(c.copied[b])) != cudaSuccess)
+                return cuda_fail("pfac_match: pipeline", e);
+            std::memcpy(c.h_stage[b], src, rd);
+            src = c.h_stage[b];
+        }
+        if ((e = cudaMemcpyAsync(c.d_text[b], src, rd, cudaMemcpyHostToDevice, c.copy)) != cudaSuccess ||
+            (e = cudaEventRecord(c.copied[b], c.copy)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(c.comp, c.copied[b], 0)) != cudaSuccess)
+            return cuda_fail("pfac_match: H2D", e);
+        rs = pfac_match_device(t, dev, c.d_text[b], rd, ns, s0, c.d_pos + i * per_chunk, c.d_pid + i * per_chunk,
+                               per_chunk, c.d_count + i, c.d_ws, c.ws_cap, reinterpret_cast<pfac_stream>(c.comp));
+        if (rs != PFAC_OK) return rs;
+        if ((e = cudaEventRecord(c.scanned[b], c.comp)) != cudaSuccess) return cuda_fail("pfac_match: pipeline", e);
+    }
+    if ((e = cudaMemcpyAsync(c.h_count, c.d_count, 8 * n_chunks, cudaMemcpyDeviceToHost, c.comp)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(c.comp)) != cudaSuccess)
+        return cuda_fail("pfac_match: scan", e);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < n_chunks; i++) total += c.h_count[i];
+    if (total == 0) return PFAC_OK;
+    out->pos = static_cast<uint64_t *>(std::malloc(total * 8));
+    out->pid = static_cast<uint32_t *>(std::malloc(total * 4));
     if (!out->pos || !out->pid) {
         pfac_matches_free(out);
         return fail(kStatusNomem, "pfac_match: out of host memory");
     }
-    if ((e = cudaMemcpyAsync(out->pos, c.d_pos, count * 8, cudaMemcpyDeviceToHost, c.st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(out->pid, c.d_pid, count * 4, cudaMemcpyDeviceToHost, c.st)) != cudaSuccess ||
-        (e = cudaStreamSynchronize(c.st)) != cudaSuccess) {
-        pfac_matches_free(out);
-        return cuda_fail("pfac_match: D2H", e);
+    uint64_t at = 0;
+    for (uint64_t i = 0; i < n_chunks; at += c.h_count[i], i++) {
+        const uint64_t n = c.h_count[i];
+        if (n == 0) continue;
+        const uint64_t *dp = c.d_pos + i * per_chunk;
+        const uint32_t *dq = c.d_pid + i * per_chunk;
+        uint64_t *tp = nullptr;
+        uint32_t *tq = nullptr;
+        if (n > per_chunk) {  // more rows than the chunk's room: scan it again into buffers of its size
+            uint64_t s0, ns, rd;
+            chunk(i, s0, ns, rd);
+            uint64_t *tc = nullptr;
+            if ((e = cudaMalloc(&tp, n * 8)) != cudaSuccess || (e = cudaMalloc(&tq, n * 4)) != cudaSuccess ||
+                (e = cudaMalloc(&tc, 8)) != cudaSuccess ||
+                (e = cudaMemcpyAsync(c.d_text[0], text + s0, rd, cudaMemcpyHostToDevice, c.comp)) != cudaSuccess) {
+                cudaFree(tp); cudaFree(tq); cudaFree(tc);
+                pfac_matches_free(out);
+                return cuda_fail("pfac_match: retry buffers", e);
+            }
+            rs = pfac_match_device(t, dev, c.d_text[0], rd, ns, s0, tp, tq, n, tc, c.d_ws, c.ws_cap,
+                                   reinterpret_cast<pfac_stream>(c.comp));
+            cudaFree(tc);  // (stream-ordered free is not needed: the count is not read)
+            if (rs != PFAC_OK) {
+                cudaFree(tp); cudaFree(tq);
+                pfac_matches_free(out);
+                return rs;
+            }
+            dp = tp;
+            dq = tq;
+        }
+        if ((e = cudaMemcpyAsync(out->pos + at, dp, n * 8, cudaMemcpyDeviceToHost, c.comp)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(out->pid + at, dq, n * 4, cudaMemcpyDeviceToHost, c.comp)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(c.comp)) != cudaSuccess) {
+            cudaFree(tp); cudaFree(tq);
+            pfac_matches_free(out);
+            return cuda_fail("pfac_match: D2H", e);
+        }
+        cudaFree(tp);
+        cudaFree(tq);
     }
-    out->count = count;
+    out->count = total;
     return PFAC_OK;
 }
 

@@ -342,3 +342,46 @@ def test_full_c5_16gib_sharded():
         total += len(pos)
         del host
     assert total > 0
+
+
+# ------------------------------------------------ host streaming pipeline
+@pytest.mark.parametrize("pinned", [True, False], ids=["pinned", "pageable"])
+def test_pfac_match_streaming(pinned):
+    """pfac_match (host buffers) streams the text in PFAC_STREAM_CHUNK-start
+    chunks with their (max_len-1)-byte halos: 200 MiB
+    of C2 text = 4 chunks, with planted occurrences straddling every chunk
+    boundary; equal to the oracle element by element, page-locked or not."""
+    ps = gen.patterns(2)
+    n = 200 << 20
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=pinned)
+    text = host.numpy()
+    gen.text(2, 0, n, out=text)
+    C = 64 << 20
+    pats = ps.to_list()
+    longest = max(pats, key=len)
+    for k, b in enumerate(range(C, n, C)):  # a pattern across a boundary, or one ending exactly at it
+        if k % 2 == 0:
+            text[b - 5:b - 5 + len(longest)] = np.frombuffer(longest, np.uint8)
+        else:
+            text[b - len(pats[0]):b] = np.frombuffer(pats[0], np.uint8)
+    t = pf.Trie(ps)
+    got = t.match_host(text)
+    want = oracle.Trie(ps).match(text)
+    assert_same(got, want, f"streamed pfac_match ({'pinned' if pinned else 'pageable'})")
+    for k, b in enumerate(range(C, n, C)):
+        p0, k0 = (b - 5, pats.index(longest)) if k % 2 == 0 else (b - len(pats[0]), 0)
+        assert ((got[0] == p0) & (got[1] == k0)).any()
+
+
+def test_pfac_match_streaming_chunk_overflow():
+    """A chunk with more rows than its planned room (dense matches in the
+    first chunk) is scanned again into buffers of its size."""
+    ps = [b"a", b"aa", b"xyz"]
+    n = (64 << 20) + 12345
+    text = np.frombuffer(gen.text(2, 0, n).tobytes(), np.uint8).copy()
+    text[: 2 << 20] = ord("a")
+    t = pf.Trie(ps)
+    got = t.match_host(text)
+    want = oracle.Trie(ps).match(text)
+    assert len(want[0]) > (4 << 20)
+    assert_same(got, want, "chunk overflow")
