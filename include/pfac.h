@@ -53,7 +53,9 @@ typedef enum {
     PFAC_BYTES_UNCOMPRESSED = 1,  /* the paper's original trie: 36 B per node (256-bit bitmap + u32 offset) */
     PFAC_BYTES_DENSE_STT = 2,     /* Lin et al. PFAC state table: 256 x u32 per node */
     PFAC_BYTES_PAPER_CRS = 3,     /* paper CRS of the N x 9 word matrix: (2 nnz + n + 1) x 4 B */
-    PFAC_BYTES_CSR_CORE = 4       /* the path-compressed CSR trie alone: node words (4 B/node) + labels (1 B/edge) + tails (16 B + path bytes each) */
+    PFAC_BYTES_CSR_CORE = 4,      /* the path-compressed CSR trie alone: node words (4 B/node) + labels (1 B/edge) + records (16 B + path bytes each) */
+    PFAC_BYTES_TRUNCATED = 5      /* the paper's trie truncated at depth d (PAPER.md:80 step III): 36 B x nodes of depth <= d
+                                     (= PFAC_BYTES_UNCOMPRESSED when built untruncated) */
 } pfac_bytes_kind;
 
 typedef struct {
@@ -66,6 +68,8 @@ typedef struct {
     uint32_t filter_gram; /* d of the d-gram first-stage filter (<= min(4, min_len)) */
     uint32_t filter_log2_bits;
     uint32_t image_nodes; /* nodes stored in the device image after path compression of single-path tails */
+    uint32_t truncate_depth; /* 0: untruncated; d: truncated at depth d with on-device verification */
+    uint32_t verify_candidates; /* candidate records of the verify leaves (truncated tries) */
 } pfac_stats;
 
 /* Build options (pfac_build_ex).  NULL means "all defaults"; initialise a

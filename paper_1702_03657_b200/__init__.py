@@ -28,7 +28,7 @@ lib_path = os.environ.get("PFAC_LIB") or os.path.join(_HERE, "libpfac.so")  # PF
 PFAC_OK = 0
 _STATUS = {0: "PFAC_OK", 1: "PFAC_ERR_INVALID_ARG", 2: "PFAC_ERR_LIMIT", 3: "PFAC_ERR_NOMEM",
            4: "PFAC_ERR_CUDA", 5: "PFAC_ERR_CAPACITY"}
-BYTES_KINDS = {"device_image": 0, "uncompressed": 1, "dense_stt": 2, "paper_crs": 3, "csr_core": 4}
+BYTES_KINDS = {"device_image": 0, "uncompressed": 1, "dense_stt": 2, "paper_crs": 3, "csr_core": 4, "truncated": 5}
 
 
 class PfacError(RuntimeError):
@@ -40,7 +40,8 @@ class PfacError(RuntimeError):
 class _Stats(C.Structure):
     _fields_ = [("nodes", C.c_uint64), ("edges", C.c_uint64), ("terminals", C.c_uint64),
                 ("n_patterns", C.c_uint32), ("max_len", C.c_uint32), ("min_len", C.c_uint32),
-                ("filter_gram", C.c_uint32), ("filter_log2_bits", C.c_uint32), ("image_nodes", C.c_uint32)]
+                ("filter_gram", C.c_uint32), ("filter_log2_bits", C.c_uint32), ("image_nodes", C.c_uint32),
+                ("truncate_depth", C.c_uint32), ("verify_candidates", C.c_uint32)]
 
 
 class _Matches(C.Structure):

@@ -235,6 +235,7 @@ pfac_status pfac_trie_bytes(const pfac_trie *t, pfac_bytes_kind kind, uint64_t *
     case PFAC_BYTES_DENSE_STT: *out = t->hdr.bytes_dense_stt; break;
     case PFAC_BYTES_PAPER_CRS: *out = t->hdr.bytes_paper_crs; break;
     case PFAC_BYTES_CSR_CORE: *out = t->hdr.bytes_csr_core; break;
+    case PFAC_BYTES_TRUNCATED: *out = t->hdr.bytes_truncated; break;
     default: return fail(kStatusInvalid, "pfac_trie_bytes: bad kind");
     }
     return PFAC_OK;
@@ -252,6 +253,8 @@ pfac_status pfac_trie_stats(const pfac_trie *t, pfac_stats *o) {
     o->min_len = t->hdr.min_len;
     o->filter_gram = t->hdr.filter_gram;
     o->filter_log2_bits = t->hdr.filter_log2_bits;
+    o->truncate_depth = t->hdr.trunc_depth;
+    o->verify_candidates = (uint32_t)t->hdr.n_cand;
     return PFAC_OK;
 }
 

@@ -79,6 +79,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     q.push_back({0, m, 0, kNone});
     std::vector<uint32_t> own;
     std::vector<uint32_t> parent{0}, own_pid;  // per node: parent; a pattern ending here (kNone if none)
+    std::vector<uint32_t> end_at(m, kNone);    // per sorted index: the node its pattern ends at
     for (size_t head = 0; head < q.size(); head++) {
         if (q.size() > (size_t)kEdgeMask) {
             err = "pfac_build: trie exceeds 2^30-1 nodes";
@@ -89,7 +90,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
         // patterns ending exactly here sort first in the range
         uint32_t lo = r.lo;
         own.clear();
-        while (lo < r.hi && lens[ord[lo]] == r.depth) own.push_back(ord[lo++]);
+        while (lo < r.hi && lens[ord[lo]] == r.depth) {
+            end_at[lo] = v;
+            own.push_back(ord[lo++]);
+        }
         uint32_t anc = r.anc_term;
         bool terminal = !own.empty();
         own_pid.push_back(terminal ? own[0] : kNone);
@@ -137,6 +141,28 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     }
     const uint64_t N = q.size(), E = N - 1, T = term_node.size();
     node_word.push_back((uint32_t)E);  // row_ptr[N]
+    auto nchild = [&](uint64_t v) { return (node_word[v + 1] & kEdgeMask) - (node_word[v] & kEdgeMask); };
+
+    // ---- step III ("the trie is truncated at the appropriate
+    // level"; opt.truncate_depth = d > 0): nodes deeper than d leave the
+    // image; a depth-d node with children becomes a verify leaf whose record
+    // lists the distinct patterns below it (their bytes past depth d, longest
+    // first, each with the terminal index of its end node).  A walk that
+    // reaches a verify leaf compares those bytes with the text; the longest
+    // candidate that matches gives the start's pid list (it holds every
+    // pattern on its root path, PAPER.md:76 continued past depth d), else the
+    // deepest terminal already passed does: results stay exact.
+    const uint32_t d_trunc = opt.truncate_depth;
+    std::vector<uint8_t> cut(N, 0), verify(N, 0);
+    uint64_t n_trunc_nodes = N;  // nodes of the truncated (uncompressed) trie
+    if (d_trunc) {
+        n_trunc_nodes = 0;
+        for (uint64_t v = 0; v < N; v++) {
+            if (q[v].depth > d_trunc) cut[v] = 1;
+            else n_trunc_nodes++;
+            if (q[v].depth == d_trunc && nchild(v) > 0) verify[v] = 1;
+        }
+    }
 
     // ---- path compression of the non-branching deep part.  A node whose
     // strict descendants form a single path with one terminal, at its end, is
@@ -147,9 +173,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     // nodes have no branching and no other terminal).
     std::vector<uint8_t> chain_ok(N, 0);
     std::vector<uint32_t> chain_end(N, kNone);
-    auto nchild = [&](uint64_t v) { return (node_word[v + 1] & kEdgeMask) - (node_word[v] & kEdgeMask); };
     for (uint64_t v = N; v-- > 0;) {
-        if (nchild(v) != 1) continue;
+        if (nchild(v) != 1 || verify[v] || cut[v]) continue;  // (a verify leaf ends no tail)
         const uint32_t u = (node_word[v] & kEdgeMask) + 1;
         const bool term_u = (node_word[u] & kTermBit) != 0;
         if (nchild(u) == 0 && term_u) {
@@ -162,8 +187,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     }
     std::vector<uint8_t> is_tail(N, 0), removed(N, 0);
     for (uint64_t v = 1; v < N; v++)
-        if (chain_ok[v] && !chain_ok[parent[v]] && q[chain_end[v]].depth - q[v].depth >= 2) is_tail[v] = 1;
-    for (uint64_t v = 1; v < N; v++) removed[v] = removed[parent[v]] || is_tail[parent[v]];
+        if (!cut[v] && chain_ok[v] && !chain_ok[parent[v]] && q[chain_end[v]].depth - q[v].depth >= 2) is_tail[v] = 1;
+    for (uint64_t v = 1; v < N; v++) removed[v] = cut[v] || removed[parent[v]] || is_tail[parent[v]];
     // ---- internal chains: a kept node v (not the root) whose single child u
     // is non-terminal with a single child starts a chain: the nodes below v
     // down to the first node x that is terminal, branching, a leaf or a tail
@@ -173,10 +198,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     auto is_term = [&](uint64_t v) { return (node_word[v] & kTermBit) != 0; };
     std::vector<uint32_t> chain_to(N, kNone);
     for (uint64_t v = 1; v < N; v++) {
-        if (removed[v] || is_tail[v] || nchild(v) != 1) continue;
+        if (removed[v] || is_tail[v] || verify[v] || nchild(v) != 1) continue;
         uint64_t x = first_child(v);
-        if (is_term(x) || nchild(x) != 1 || is_tail[x]) continue;
-        while (!is_term(x) && nchild(x) == 1 && !is_tail[x]) {
+        if (is_term(x) || nchild(x) != 1 || is_tail[x] || verify[x]) continue;
+        while (!is_term(x) && nchild(x) == 1 && !is_tail[x] && !verify[x]) {
             removed[x] = 1;
             x = first_child(x);
         }
@@ -191,7 +216,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     order.push_back(0);
     for (size_t h = 0; h < order.size(); h++) {
         const uint64_t v = order[h];
-        if (is_tail[v]) continue;
+        if (is_tail[v] || verify[v]) continue;
         if (chain_to[v] != kNone) {
             order.push_back(chain_to[v]);
             continue;
@@ -234,7 +259,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     for (uint64_t i = 0; i < NK; i++) {
         const uint64_t v = order[i];
         const bool term = is_term(v);
-        const bool rec = is_tail[v] || chain_to[v] != kNone;
+        const bool rec = is_tail[v] || chain_to[v] != kNone || verify[v];
         cnode.push_back((uint32_t)clabel.size() | (term ? kTermBit : 0u) | (rec ? kTailBit : 0u));
         if (term) {
             nterm_old.push_back(old_ti[v]);
@@ -242,7 +267,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
         }
         if (chain_to[v] != kNone) {
             clabel.push_back(label[node_word[v] & kEdgeMask]);  // the chain's first byte (CSR shape only)
-        } else if (!is_tail[v]) {
+        } else if (!is_tail[v] && !verify[v]) {
             for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++) clabel.push_back(label[e]);
         }
     }
@@ -253,8 +278,35 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     // (chain), chain end node (chain) or 0 (tail)
     std::vector<uint32_t> tails;
     std::vector<uint8_t> tail_bytes;
+    std::vector<uint32_t> cands;  // verify candidates: records appended after the node records
+    std::vector<std::pair<uint32_t, uint32_t>> fix;  // (verify record, its first candidate) to patch
     for (uint64_t i = 0; i < NK; i++) {
         const uint64_t v = order[i];
+        if (verify[v]) {
+            // candidates: the distinct patterns below v (their end nodes), longest first
+            std::vector<uint32_t> ends;
+            for (uint32_t j = q[v].lo; j < q[v].hi; j++)
+                if (end_at[j] != kNone && end_at[j] != v && (ends.empty() || ends.back() != end_at[j]))
+                    ends.push_back(end_at[j]);
+            std::stable_sort(ends.begin(), ends.end(), [&](uint32_t x, uint32_t y) { return q[x].depth > q[y].depth; });
+            fix.push_back({(uint32_t)(tails.size() / 4), (uint32_t)(cands.size() / 4)});
+            tails.push_back(0u);  // first candidate (patched below)
+            tails.push_back((uint32_t)ends.size());
+            tails.push_back(kVerify);
+            tails.push_back(0u);
+            for (uint32_t u : ends) {
+                const uint32_t k = ord[q[u].lo];  // a pattern ending at u
+                cands.push_back((uint32_t)tail_bytes.size());
+                cands.push_back(q[u].depth - d_trunc);
+                cands.push_back((uint32_t)nterm_old.size());
+                cands.push_back(0u);
+                nterm_old.push_back(old_ti[u]);
+                tail_bytes.insert(tail_bytes.end(), pats[k] + d_trunc, pats[k] + q[u].depth);
+                while (tail_bytes.size() & 3) tail_bytes.push_back(0);
+            }
+            tail_bits[i >> 5] |= 1u << (i & 31);
+            continue;
+        }
         if (!is_tail[v] && chain_to[v] == kNone) continue;
         const uint32_t end = is_tail[v] ? chain_end[v] : chain_to[v];
         const uint32_t dv = q[v].depth, de = q[end].depth;
@@ -280,7 +332,10 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
             acc += (uint32_t)__builtin_popcount(tail_bits[w]);
         }
     }
-    const uint64_t NT = tails.size() / 4;
+    const uint64_t NT = tails.size() / 4;  // node records; the candidates follow them
+    const uint64_t NC = cands.size() / 4;
+    for (auto &f : fix) tails[4 * f.first] = (uint32_t)NT + f.second;
+    tails.insert(tails.end(), cands.begin(), cands.end());
     tail_bytes.insert(tail_bytes.end(), 4, 0);  // slack for 4-byte reads
     // pid lists in the new terminal order
     std::vector<uint32_t> cout_ptr{0}, cout_pid;
@@ -560,7 +615,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     h.off_filter = o;    o = align256(o + 4 * filter.size());
     h.off_tail_bits = o; o = align256(o + 4 * tail_bits.size());
     h.off_tail_rank = o; o = align256(o + 4 * tail_rank.size());
-    h.off_tails = o;     o = align256(o + 16 * NT);
+    h.off_tails = o;     o = align256(o + 16 * (NT + NC));
     h.off_tail_bytes = o; o = align256(o + tail_bytes.size() + 16);
     h.off_level1 = o;    o = align256(o + 40ull * B);
     h.off_pair = o;      o = align256(o + 8192);
@@ -573,12 +628,15 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     h.entry_log2 = entry_log2;
     h.n_level1 = B;
     h.n_tails = NT;
+    h.n_cand = NC;
+    h.trunc_depth = d_trunc;
+    h.bytes_truncated = 36 * n_trunc_nodes;              // PAPER.md:80 step III, 134
     h.n_tail_bytes = tail_bytes.size();
     h.image_bytes = o;
     h.bytes_uncompressed = 36 * N_full;
     h.bytes_dense_stt = 1024 * N_full;                       // 256 x u32 per state
     h.bytes_paper_crs = 4 * (2 * paper_nnz + N_full + 1);    // PAPER.md:101, N x 9 words
-    h.bytes_csr_core = 4 * (NI + 1) + EI + 16 * NT + (tail_bytes.size() - 4);  // CSR + tails
+    h.bytes_csr_core = 4 * (NI + 1) + EI + 16 * (NT + NC) + (tail_bytes.size() - 4);  // CSR + records + bytes
 
     try {
         image.assign(o, 0);
@@ -598,7 +656,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     std::memcpy(p + h.off_filter, filter.data(), 4 * filter.size());
     std::memcpy(p + h.off_tail_bits, tail_bits.data(), 4 * tail_bits.size());
     std::memcpy(p + h.off_tail_rank, tail_rank.data(), 4 * tail_rank.size());
-    if (NT) std::memcpy(p + h.off_tails, tails.data(), 16 * NT);
+    if (NT + NC) std::memcpy(p + h.off_tails, tails.data(), 16 * (NT + NC));
     if (!tail_bytes.empty()) std::memcpy(p + h.off_tail_bytes, tail_bytes.data(), tail_bytes.size());
     std::memcpy(p + h.off_level1, level1.data(), 40ull * B);
     {   // 2-gram prefix table (image.h)
@@ -640,7 +698,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
                                  : ((h.filter_kind == 4 || h.filter_kind == 3) && h.entry_log2 >= 4 &&
                                     h.entry_log2 <= 30 &&
                                     in(h.off_entry, 16ull << h.entry_log2))) &&
-              h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails >= T && h.n_nodes_full >= N &&
+              h.n_kept_terminals <= T && h.n_kept_terminals + h.n_tails + h.n_cand >= T && h.n_nodes_full >= N &&
               in(h.off_term_node, 4 * h.n_kept_terminals) && in(h.off_out_ptr, 4 * (T + 1)) && in(h.off_out_pid, 4 * h.n_out) &&
               in(h.off_root, 1024) && h.filter_log2_bits >= 5 && h.filter_log2_bits <= 24 &&
               in(h.off_filter, (1ull << h.filter_log2_bits) / 8) && h.filter_gram >= 1 &&
@@ -651,7 +709,8 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
                : h.filter_gram == kGram8 ? h.filter_kind == 4
                : h.filter_gram == 4 ? (h.filter_kind == 1 || h.filter_kind == 2) : h.filter_kind == 0) &&
               (h.filter_kind == 0 || h.filter_log2_bits >= 10) && in(h.off_tail_bits, 4 * ((N + 31) / 32)) &&
-              in(h.off_tail_rank, 4 * ((N + 31) / 32)) && in(h.off_tails, 16 * h.n_tails) &&
+              in(h.off_tail_rank, 4 * ((N + 31) / 32)) && in(h.off_tails, 16 * (h.n_tails + h.n_cand)) &&
+              (h.n_cand == 0 || h.trunc_depth > 0) && h.trunc_pad == 0 &&
               in(h.off_tail_bytes, h.n_tail_bytes) && in(h.off_level1, 40 * h.n_level1);
     if (ok) {
         const uint32_t *node = reinterpret_cast<const uint32_t *>(p + h.off_node);
@@ -660,12 +719,19 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
              h.n_level1 == (node[1] & kEdgeMask) && h.n_level1 >= 1 && h.n_level1 <= 256;
         for (uint64_t v = 0; ok && v < N; v++) ok = (node[v] & kEdgeMask) <= (node[v + 1] & kEdgeMask);
         const uint32_t *tails = reinterpret_cast<const uint32_t *>(p + h.off_tails);
-        uint64_t n_tail_ends = 0;  // tail records end at a terminal; chain records at a node
-        for (uint64_t i = 0; ok && i < h.n_tails; i++) {
-            const bool chain = tails[4 * i + 2] == kNone;
-            ok = (uint64_t)tails[4 * i] + tails[4 * i + 1] <= h.n_tail_bytes &&
-                 (chain ? (tails[4 * i + 3] > 0 && tails[4 * i + 3] < N && tails[4 * i + 1] >= 2)
-                        : (tails[4 * i + 2] >= h.n_kept_terminals && tails[4 * i + 2] < T && tails[4 * i + 3] == 0));
+        // records: tail (ends at a terminal), chain (at a node), verify leaf
+        // (a range of candidate records, each ending at a terminal)
+        uint64_t n_tail_ends = 0;
+        for (uint64_t i = 0; ok && i < h.n_tails + h.n_cand; i++) {
+            const uint32_t *r = tails + 4 * i;
+            const bool cand = i >= h.n_tails, chain = !cand && r[2] == kNone, ver = !cand && r[2] == kVerify;
+            if (ver) {
+                ok = r[0] >= h.n_tails && r[1] >= 1 && (uint64_t)r[0] + r[1] <= h.n_tails + h.n_cand && r[3] == 0;
+                continue;
+            }
+            ok = (uint64_t)r[0] + r[1] <= h.n_tail_bytes &&
+                 (chain ? (!cand && r[3] > 0 && r[3] < N && r[1] >= 2)
+                        : (r[2] >= h.n_kept_terminals && r[2] < T && r[3] == 0 && (!cand || r[1] >= 1)));
             n_tail_ends += !chain;
         }
         ok = ok && h.n_kept_terminals + n_tail_ends == T;
@@ -676,8 +742,10 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
         // contents the kernel dereferences: every index it follows
         // must stay inside its section
         // records: 4-byte aligned bytes read a word at a time
-        for (uint64_t i = 0; ok && i < h.n_tails; i++)
-            ok = (tails[4 * i] & 3u) == 0 && (uint64_t)tails[4 * i] + ((tails[4 * i + 1] + 3ull) & ~3ull) <= h.n_tail_bytes;
+        for (uint64_t i = 0; ok && i < h.n_tails + h.n_cand; i++)
+            ok = (i < h.n_tails && tails[4 * i + 2] == kVerify) ||
+                 ((tails[4 * i] & 3u) == 0 &&
+                  (uint64_t)tails[4 * i] + ((tails[4 * i + 1] + 3ull) & ~3ull) <= h.n_tail_bytes);
         // root table: 0 or a level-1 node
         const uint32_t *root = reinterpret_cast<const uint32_t *>(p + h.off_root);
         for (uint32_t c = 0; ok && c < 256; c++) ok = root[c] <= h.n_level1;

@@ -47,6 +47,17 @@
 //                       + L).  The chain start keeps one CSR edge (to x) so
 //                       the BFS numbering of the compressed tree keeps the
 //                       implicit child rule.
+//                     * verify leaf (t = kVerify; truncated tries only,
+//                       PAPER.md:80 step III at depth d): a depth-d node whose
+//                       subtree is not in the image; x = its first candidate
+//                       record, L = their count.  Candidate records follow
+//                       the n_tails node records (n_cand of them): {bytes
+//                       offset, length L, terminal index t, 0} = a distinct
+//                       pattern below the leaf (its bytes past depth d, the
+//                       terminal of its end node), longest first.  A walk at
+//                       a verify leaf returns the terminal of the first
+//                       candidate whose bytes the text matches, else its
+//                       deepest terminal passed.
 //   tail_bytes u8[..] the labels of each tail path, concatenated (each tail
 //                     starts 4-byte aligned; 4 zero bytes of slack at the end).
 //   level1 u32[B][10] the root's children (nodes 1..B) as the paper's bitmapped
@@ -129,11 +140,12 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 16;
+constexpr uint32_t kVersion = 17;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kVerify = 0xFFFFFFFEu;     // record kind: a verify leaf (truncated trie)
 constexpr uint32_t kFilterMul = 0x9E3779B1u;  // Fibonacci hashing multiplier (odd)
 constexpr uint32_t kFilterMul2 = 0x85EBCA6Bu; // second multiplier (kinds 3, 4)
 constexpr uint32_t kFilterMul3 = 0xC2B2AE35u; // third multiplier (kind 3 bit index)
@@ -158,7 +170,10 @@ struct ImageHeader {
     uint64_t off_pair;                 // 2-gram prefix table u32[256][8]
     uint64_t off_entry;                // entry table (0: none), see above
     uint32_t entry_log2, entry_pad;  // log2 of its slots; 0
-    uint8_t pad[512 - 256 - 40];
+    uint64_t n_cand;                   // verify candidate records (after the n_tails node records)
+    uint32_t trunc_depth, trunc_pad;   // PAPER.md:80 step III depth d (0: untruncated); 0
+    uint64_t bytes_truncated;          // 36 B x nodes of depth <= d (the paper's truncated trie)
+    uint8_t pad[512 - 256 - 64];
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 

@@ -330,6 +330,26 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
     const bool hot = v < a.hot_nodes;  // hot records + bytes are in shared memory
     const uint32_t idx = ax;  // aux word: the record's index (= rank among the record nodes)
     const uint4 rec = hot ? s.tails[idx] : __ldg(a.t.tails + idx);
+    if (rec.z == kVerify) {
+        // verify leaf of a truncated trie (PAPER.md:80 step III): the
+        // candidates (distinct patterns below it, longest first; records and
+        // bytes in global memory) are compared with the text; the first that
+        // matches gives the start's list (every pattern on its root path),
+        // else the deepest terminal passed does
+        for (uint32_t c = rec.x; c < rec.x + rec.y; ++c) {
+            const uint4 cr = __ldg(a.t.tails + c);
+            if ((uint64_t)j + cr.y > (uint64_t)tx.end) continue;
+            const uint32_t *pw = reinterpret_cast<const uint32_t *>(a.t.tail_bytes + cr.x);
+            bool eq = true;
+            for (uint32_t k = 0; eq && k < cr.y; k += 4) {
+                const uint32_t n = cr.y - k;
+                const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
+                eq = ((tx.at4(j + k) ^ __ldg(pw + (k >> 2))) & m) == 0;
+            }
+            if (eq) return cr.z;
+        }
+        return term_of(last);
+    }
     if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(last);
     const uint32_t *pw = reinterpret_cast<const uint32_t *>((hot ? s.tail_bytes : a.t.tail_bytes) + rec.x);
     for (uint32_t k = 0; k < rec.y; k += 4) {
@@ -1600,8 +1620,10 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     auto tails_below = [&](uint32_t H) -> uint32_t {  // rank(H)
         return h_trank[H >> 5] + (uint32_t)__builtin_popcount(h_tbits[H >> 5] & ((1u << (H & 31)) - 1u));
     };
-    auto tbytes_below = [&](uint32_t nt) -> uint32_t {
-        return nt < hh.n_tails ? h_tails[4 * nt] : (uint32_t)hh.n_tail_bytes;
+    auto tbytes_below = [&](uint32_t nt) -> uint32_t {  // bytes of the records below nt (a verify
+                                                          // record's bytes start at its first candidate's)
+        if (nt >= hh.n_tails) return (uint32_t)hh.n_tail_bytes;
+        return h_tails[4 * nt + 2] == kVerify ? h_tails[4 * h_tails[4 * nt]] : h_tails[4 * nt];
     };
     auto hot_bytes = [&](uint32_t H) -> uint64_t {
         const uint32_t nt = tails_below(H);

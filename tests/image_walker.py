@@ -10,7 +10,8 @@ TERM = 0x80000000
 TAIL = 0x40000000
 MASK = 0x3FFFFFFF
 
-_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II")
+_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II Q II Q")
+VERIFY = 0xFFFFFFFE
 
 
 def parse(image: bytes) -> dict:
@@ -21,7 +22,7 @@ def parse(image: bytes) -> dict:
             "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core",
             "n_tails", "n_tail_bytes", "off_tail_bits", "off_tail_rank", "off_tails", "off_tail_bytes",
             "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full", "off_kset", "kset_log2", "kset_empty", "off_pair",
-            "off_entry", "entry_log2", "entry_pad"]
+            "off_entry", "entry_log2", "entry_pad", "n_cand", "trunc_depth", "trunc_pad", "bytes_truncated"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
@@ -38,7 +39,7 @@ def parse(image: bytes) -> dict:
     nw = (N + 31) // 32
     h["tail_bits"] = buf[h["off_tail_bits"]:h["off_tail_bits"] + 4 * nw].view(np.uint32)
     h["tail_rank"] = buf[h["off_tail_rank"]:h["off_tail_rank"] + 4 * nw].view(np.uint32)
-    h["tails"] = buf[h["off_tails"]:h["off_tails"] + 16 * h["n_tails"]].view(np.uint32).reshape(-1, 4)
+    h["tails"] = buf[h["off_tails"]:h["off_tails"] + 16 * (h["n_tails"] + h["n_cand"])].view(np.uint32).reshape(-1, 4)
     h["tail_bytes"] = buf[h["off_tail_bytes"]:h["off_tail_bytes"] + h["n_tail_bytes"]]
     h["level1"] = buf[h["off_level1"]:h["off_level1"] + 40 * h["n_level1"]].view(np.uint32).reshape(-1, 10)
     h["pair"] = buf[h["off_pair"]:h["off_pair"] + 8192].view(np.uint32).reshape(256, 8)
@@ -146,6 +147,12 @@ def walk(h, text, i, L, v0=None, d0=1):
     while j < L:
         if node[v] & TAIL:
             off, ln, ti, x = (int(y) for y in h["tails"][tail_index(h, v)])
+            if ti == VERIFY:  # verify leaf (truncated trie): the longest candidate the text matches
+                for c in range(off, off + ln):
+                    co, cl, ct, _ = (int(y) for y in h["tails"][c])
+                    if j + cl <= L and bytes(text[j:j + cl]) == h["tail_bytes"][co:co + cl].tobytes():
+                        return ct
+                return term_of(h, last)
             if not (j + ln <= L and bytes(text[j:j + ln]) == h["tail_bytes"][off:off + ln].tobytes()):
                 return term_of(h, last)
             if ti != 0xFFFFFFFF:  # tail: ends at its terminal

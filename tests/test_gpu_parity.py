@@ -385,3 +385,45 @@ def test_pfac_match_streaming_chunk_overflow():
     want = oracle.Trie(ps).match(text)
     assert len(want[0]) > (4 << 20)
     assert_same(got, want, "chunk overflow")
+
+
+# ------------------------------------------------ truncated trie (NEXT-1)
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_truncated_trie_exact(cid):
+    """The trie cut at depth d (PAPER.md:80 step III) with on-device
+    verification of the patterns below each depth-d node gives the oracle's
+    rows exactly (4 MiB of each config, unaligned device text)."""
+    ps = gen.patterns(cid)
+    n = 1024 if cid == 1 else 4 << 20
+    text = gen.text(cid, 0, n)
+    want = oracle.Trie(ps).match(text, engine="ac" if cid == 5 else "pfac")
+    for d in [1, 2, 4, 8, 16]:
+        t = pf.Trie(ps, truncate_depth=d)
+        assert_same(gpu_rows(t, text, offset=3), want, f"C{cid} depth {d}")
+
+
+def test_truncated_random_tiny_gpu():
+    rng = np.random.default_rng(32)
+    for trial in range(120):
+        sigma = int(rng.choice([2, 4, 256]))
+        alpha = rng.choice(256, size=sigma, replace=False)
+        m = int(rng.integers(1, 40))
+        pats = [bytes(alpha[rng.integers(0, sigma, int(rng.integers(1, 14)))].astype(np.uint8)) for _ in range(m)]
+        if trial % 3 == 0:
+            pats += [pats[0], pats[0] + pats[-1]]
+        n = int(rng.choice([1, 100, 4097, 70000]))
+        text = alpha[rng.integers(0, sigma, n)].astype(np.uint8)
+        d = int(rng.integers(1, 10))
+        want = oracle.Trie(pats).match(text)
+        assert_same(gpu_rows(pf.Trie(pats, truncate_depth=d), text), want, f"trial {trial} depth {d}")
+
+
+def test_truncated_c4_full_exact():
+    """C4 at its full 4 GiB with the trie cut at the paper's eight levels."""
+    ps = gen.patterns(4)
+    n = 4 << 30
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    gen.text(4, 0, n, out=host.numpy())
+    pos, pid = pf.Trie(ps, truncate_depth=8).match(host.to(DEV))
+    want = oracle.Trie(ps).match(host.numpy())
+    assert_same((pos.cpu().numpy().astype(np.uint64), pid.cpu().numpy().astype(np.uint32)), want, "C4 depth 8")

@@ -17,7 +17,10 @@ import oracle  # noqa: E402
 import paper_1702_03657_b200 as pf  # noqa: E402
 
 cfgs = [a for a in sys.argv[1:] if ":" in a] or ["2:64", "3:1024", "4:4096", "5:2048"]
-plan = {k: (v if k == "placement" else int(v)) for k, v in (a.split("=") for a in sys.argv[1:] if "=" in a)}
+opts = {k: (v if k == "placement" else int(v)) for k, v in (a.split("=") for a in sys.argv[1:] if "=" in a)}
+BUILD = {"filter_kind", "pair_bits_per_key", "gram8_bits_per_key", "truncate_depth"}
+build = {k: v for k, v in opts.items() if k in BUILD}
+plan = {k: v for k, v in opts.items() if k not in BUILD}
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6450.0
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -28,7 +31,7 @@ for c in cfgs:
     host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     gen.text(cid, 0, n, out=host.numpy())
     text = host.to("cuda")
-    trie = pf.Trie(ps)
+    trie = pf.Trie(ps, **build)
     sc = pf.Scanner(trie, "cuda:0", capacity=max(1 << 20, n // 256), **plan)
     reps = 50 if n <= (256 << 20) else 10
     ts = []
@@ -54,6 +57,6 @@ for c in cfgs:
     print(json.dumps({"config": f"C{cid}", "mib": mib, "us": round(t * 1e6, 2), "gbps": round(8 * n / t / 1e9, 1),
                       "frac": round((n + 12 * cnt) / t / 1e9 / peak, 4), "matches": cnt, "spot_ok": ok,
                       "plan": {k: v for k, v in trie.plan(n, **plan).items() if k in ("stage2", "placement", "hot_nodes", "filter_copies", "kset", "entry")},
-                      "opts": plan}), flush=True)
+                      "opts": opts}), flush=True)
     del text, host, sc
     torch.cuda.empty_cache()
