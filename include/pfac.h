@@ -54,8 +54,15 @@ typedef enum {
     PFAC_BYTES_DENSE_STT = 2,     /* Lin et al. PFAC state table: 256 x u32 per node */
     PFAC_BYTES_PAPER_CRS = 3,     /* paper CRS of the N x 9 word matrix: (2 nnz + n + 1) x 4 B */
     PFAC_BYTES_CSR_CORE = 4,      /* the path-compressed CSR trie alone: node words (4 B/node) + labels (1 B/edge) + records (16 B + path bytes each) */
-    PFAC_BYTES_TRUNCATED = 5      /* the paper's trie truncated at depth d (PAPER.md:80 step III): 36 B x nodes of depth <= d
+    PFAC_BYTES_TRUNCATED = 5,     /* the paper's trie truncated at depth d (PAPER.md:80 step III): 36 B x nodes of depth <= d
                                      (= PFAC_BYTES_UNCOMPRESSED when built untruncated) */
+    /* built with merge_suffixes only (INVALID_ARG otherwise): */
+    PFAC_BYTES_MERGED = 6,        /* id-preserving minimal DAG (steps IV-V): 36 B x DAG nodes */
+    PFAC_BYTES_MERGED_CRS = 7,    /* its N x 9 CRS: (2 nnz + n + 1) x 4 B */
+    PFAC_BYTES_MERGED_IMAGE = 8,  /* its device sections: node words, labels, child ids, rank skips, rank table */
+    PFAC_BYTES_PIPE_TRUNC = 9,    /* the paper's pipeline: trie cut at 8 levels (or truncate_depth), 36 B/node */
+    PFAC_BYTES_PIPE_MERGED = 10,  /* ... its identical sub-tries merged by shape and terminal flag (no identity), 36 B/node */
+    PFAC_BYTES_PIPE_CRS = 11      /* ... then as the N x 9 CRS, (2 nnz + n + 1) x 4 B */
 } pfac_bytes_kind;
 
 typedef struct {
@@ -88,8 +95,20 @@ typedef struct {
                                     the trie is cut at level d; a start that reaches a depth-d
                                     node is verified on the device against the full bytes of
                                     the patterns below it (exact results either way) */
-    uint32_t reserved[7];        /* must be 0 */
+    uint32_t merge_suffixes;     /* 1: also build the minimal DAG of the trie (PAPER.md:80 steps IV-V:
+                                    similar suffixes and end nodes merged) with pattern identity kept
+                                    by path rank (image.h dag_*), scannable with the plan option
+                                    form = PFAC_FORM_MERGED_DAG, and the paper-pipeline byte counts
+                                    (PFAC_BYTES_PIPE_*) */
+    uint32_t reserved[6];        /* must be 0 */
 } pfac_build_options;
+
+/* Which structure a scan walks (pfac_plan_options.form). */
+typedef enum {
+    PFAC_FORM_CSR_TRIE = 0,   /* the path-compressed CSR trie with the first-stage filters (the product path) */
+    PFAC_FORM_MERGED_DAG = 1  /* the id-preserving merged DAG (built with merge_suffixes): a plain walk
+                                 per start with path-rank terminals (NEXT-2; exact, not tuned) */
+} pfac_form;
 
 /* Shared-memory placement of the trie for one scan (the analog of the paper's
  * Fig. 6 global vs texture + shared-memory study). */
@@ -118,7 +137,8 @@ typedef struct {
     uint32_t l2_persist;          /* 1: the device image is given as an L2 persisting access-policy
                                      window for this launch (sets the device's persisting-L2 limit
                                      to min(image, 64 MiB) on first use) */
-    uint32_t reserved[6];         /* must be 0 */
+    uint32_t form;                /* pfac_form (PFAC_FORM_MERGED_DAG needs a trie built with merge_suffixes) */
+    uint32_t reserved[5];         /* must be 0 */
 } pfac_plan_options;
 
 /* Fill *o with the defaults (struct_bytes set, every choice automatic). */

@@ -28,7 +28,9 @@ lib_path = os.environ.get("PFAC_LIB") or os.path.join(_HERE, "libpfac.so")  # PF
 PFAC_OK = 0
 _STATUS = {0: "PFAC_OK", 1: "PFAC_ERR_INVALID_ARG", 2: "PFAC_ERR_LIMIT", 3: "PFAC_ERR_NOMEM",
            4: "PFAC_ERR_CUDA", 5: "PFAC_ERR_CAPACITY"}
-BYTES_KINDS = {"device_image": 0, "uncompressed": 1, "dense_stt": 2, "paper_crs": 3, "csr_core": 4, "truncated": 5}
+BYTES_KINDS = {"device_image": 0, "uncompressed": 1, "dense_stt": 2, "paper_crs": 3, "csr_core": 4, "truncated": 5,
+               "merged": 6, "merged_crs": 7, "merged_image": 8, "pipe_trunc": 9, "pipe_merged": 10, "pipe_crs": 11}
+FORMS = {"csr_trie": 0, "merged_dag": 1}
 
 
 class PfacError(RuntimeError):
@@ -51,7 +53,8 @@ class _Matches(C.Structure):
 class BuildOptions(C.Structure):
     """pfac_build_options (include/pfac.h); fields set from keyword arguments."""
     _fields_ = [("struct_bytes", C.c_uint32), ("filter_kind", C.c_int32), ("pair_bits_per_key", C.c_uint32),
-                ("gram8_bits_per_key", C.c_uint32), ("truncate_depth", C.c_uint32), ("reserved", C.c_uint32 * 7)]
+                ("gram8_bits_per_key", C.c_uint32), ("truncate_depth", C.c_uint32), ("merge_suffixes", C.c_uint32),
+                ("reserved", C.c_uint32 * 6)]
 
 
 class PlanOptions(C.Structure):
@@ -59,7 +62,7 @@ class PlanOptions(C.Structure):
     _fields_ = [("struct_bytes", C.c_uint32), ("placement", C.c_uint32), ("hot_bytes_cap", C.c_uint32),
                 ("max_filter_rep_log2", C.c_int32), ("ring_slots", C.c_int32), ("ctg64", C.c_int32),
                 ("pool64", C.c_int32), ("stage2", C.c_int32), ("entry", C.c_int32), ("l2_persist", C.c_uint32),
-                ("reserved", C.c_uint32 * 6)]
+                ("form", C.c_uint32), ("reserved", C.c_uint32 * 5)]
 
 
 class _PlanInfo(C.Structure):
@@ -84,7 +87,9 @@ def plan_options(**kw) -> PlanOptions:
     o = PlanOptions()
     _lib().pfac_plan_options_init(C.byref(o))
     for k, v in kw.items():
-        setattr(o, k, PLACEMENTS[v] if k == "placement" and isinstance(v, str) else int(v))
+        if isinstance(v, str):
+            v = PLACEMENTS[v] if k == "placement" else FORMS[v]
+        setattr(o, k, int(v))
     return o
 
 

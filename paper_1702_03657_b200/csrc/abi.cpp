@@ -183,6 +183,8 @@ pfac_status pfac_build_ex(const uint8_t *data, const uint32_t *lengths, uint32_t
         if (opt->pair_bits_per_key) bo.pair_bits_per_key = opt->pair_bits_per_key;
         if (opt->gram8_bits_per_key) bo.gram8_bits_per_key = opt->gram8_bits_per_key;
         bo.truncate_depth = opt->truncate_depth;
+        if (opt->merge_suffixes > 1) return fail(kStatusInvalid, "pfac_build_ex: merge_suffixes must be 0 or 1");
+        bo.merge_suffixes = opt->merge_suffixes;
     }
     try {
         std::vector<const uint8_t *> ptrs(n_patterns);
@@ -236,6 +238,23 @@ pfac_status pfac_trie_bytes(const pfac_trie *t, pfac_bytes_kind kind, uint64_t *
     case PFAC_BYTES_PAPER_CRS: *out = t->hdr.bytes_paper_crs; break;
     case PFAC_BYTES_CSR_CORE: *out = t->hdr.bytes_csr_core; break;
     case PFAC_BYTES_TRUNCATED: *out = t->hdr.bytes_truncated; break;
+    case PFAC_BYTES_MERGED:
+    case PFAC_BYTES_MERGED_CRS:
+    case PFAC_BYTES_MERGED_IMAGE:
+    case PFAC_BYTES_PIPE_TRUNC:
+    case PFAC_BYTES_PIPE_MERGED:
+    case PFAC_BYTES_PIPE_CRS: {
+        const ImageHeader &h = t->hdr;
+        if (!h.n_dag_nodes) return fail(kStatusInvalid, "pfac_trie_bytes: the trie was built without merge_suffixes");
+        *out = kind == PFAC_BYTES_MERGED       ? h.bytes_merged
+               : kind == PFAC_BYTES_MERGED_CRS ? h.bytes_merged_crs
+               : kind == PFAC_BYTES_MERGED_IMAGE
+                   ? 4 * (h.n_dag_nodes + 1) + 9 * h.n_dag_edges + 4 * h.n_terminals
+               : kind == PFAC_BYTES_PIPE_TRUNC  ? h.bytes_pipe_trunc
+               : kind == PFAC_BYTES_PIPE_MERGED ? h.bytes_pipe_merged
+                                                : h.bytes_pipe_crs;
+        break;
+    }
     default: return fail(kStatusInvalid, "pfac_trie_bytes: bad kind");
     }
     return PFAC_OK;
@@ -328,8 +347,13 @@ pfac_status pfac_match_device_ex(const pfac_trie *t, int device, const uint8_t *
     if (s != PFAC_OK) return s;
     DevTrie dt = make_dev_trie(t->hdr, d_img);
     std::string err;
-    int st = launch_scan(dt, t->image.data(), device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity,
-                         d_count, d_workspace, workspace_bytes, opt ? *opt : defaults,
+    int st;
+    if (opt && opt->struct_bytes >= sizeof(pfac_plan_options) && opt->form == PFAC_FORM_MERGED_DAG)
+        st = launch_dag(t->hdr, d_img, d_text, readable_len, n_starts, pos_base, d_pos, d_pid, capacity, d_count,
+                        d_workspace, workspace_bytes, reinterpret_cast<CUstream_st *>(stream), err);
+    else
+        st = launch_scan(dt, t->image.data(), device, d_text, readable_len, n_starts, pos_base, d_pos, d_pid,
+                         capacity, d_count, d_workspace, workspace_bytes, opt ? *opt : defaults,
                          reinterpret_cast<CUstream_st *>(stream), err);
     if (st != kStatusOk) return fail(st, err);
     return PFAC_OK;

@@ -34,6 +34,79 @@ struct Range {
 
 inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 
+inline uint64_t mix64(uint64_t x) {  // splitmix64 finaliser (hashing sub-trie signatures)
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// Steps IV-V of PAPER.md:80 over the BFS trie (node_word: first edge |
+// terminal bit; the child through edge e is node e+1; depth per node):
+// classes of identical sub-tries of the trie cut at depth dlim (a node at
+// depth dlim counts as a leaf: "end nodes merged"), by terminal flag,
+// labels and child classes, bottom-up (children have larger BFS ids).
+// Returns the number of classes; cls[v] = class of node v (kNone: deeper
+// than dlim).  Hash table of (signature hash, representative node);
+// equality is checked against the representative, so no signature is stored.
+uint32_t merge_classes(const std::vector<uint32_t> &node_word, const std::vector<uint8_t> &label,
+                       const std::vector<uint32_t> &depth, uint32_t dlim, std::vector<uint32_t> &cls) {
+    const uint64_t N = depth.size();
+    cls.assign(N, kNone);
+    auto term = [&](uint64_t v) { return (node_word[v] & kTermBit) != 0; };
+    auto e0 = [&](uint64_t v) { return node_word[v] & kEdgeMask; };
+    auto e1 = [&](uint64_t v) { return depth[v] >= dlim ? e0(v) : (node_word[v + 1] & kEdgeMask); };
+    uint64_t cap = 64;
+    while (cap < 2 * N) cap <<= 1;
+    std::vector<uint64_t> slot_h(cap, 0);
+    std::vector<uint32_t> slot_rep(cap, kNone);
+    uint32_t n_cls = 0;
+    for (uint64_t v = N; v-- > 0;) {
+        if (depth[v] > dlim) continue;
+        uint64_t h = mix64(term(v) ? 0x51u : 0x17u);
+        for (uint32_t e = e0(v); e < e1(v); e++) h = mix64(h ^ ((uint64_t)label[e] << 32 | cls[e + 1]));
+        uint64_t i = h & (cap - 1);
+        for (;; i = (i + 1) & (cap - 1)) {
+            const uint32_t w = slot_rep[i];
+            if (w == kNone) {
+                slot_h[i] = h;
+                slot_rep[i] = (uint32_t)v;
+                cls[v] = n_cls++;
+                break;
+            }
+            if (slot_h[i] != h || term(w) != term(v) || e1(w) - e0(w) != e1(v) - e0(v)) continue;
+            bool same = true;
+            for (uint32_t k = 0; same && k < e1(v) - e0(v); k++)
+                same = label[e0(v) + k] == label[e0(w) + k] && cls[e0(v) + k + 1] == cls[e0(w) + k + 1];
+            if (same) {
+                cls[v] = cls[w];
+                break;
+            }
+        }
+    }
+    return n_cls;
+}
+
+// Paper CRS element count (P:101 N x 9 matrix: per node its non-zero bitmap
+// words + the offset column when it has children) of the nodes `reps` (one
+// per class) of a trie cut at dlim.
+uint64_t crs_nnz(const std::vector<uint32_t> &node_word, const std::vector<uint8_t> &label,
+                 const std::vector<uint32_t> &depth, uint32_t dlim, const std::vector<uint32_t> &reps) {
+    uint64_t nnz = 0;
+    for (uint32_t v : reps) {
+        const uint32_t a = node_word[v] & kEdgeMask, b = depth[v] >= dlim ? a : (node_word[v + 1] & kEdgeMask);
+        int last = -1;
+        if (b > a) nnz++;
+        for (uint32_t e = a; e < b; e++)
+            if ((int)(label[e] >> 5) != last) {
+                nnz++;
+                last = label[e] >> 5;
+            }
+    }
+    return nnz;
+}
+
 }  // namespace
 
 int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, const BuildOpts &opt,
@@ -344,6 +417,85 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
         cout_pid.insert(cout_pid.end(), out_pid.begin() + out_ptr[ot], out_pid.begin() + out_ptr[ot + 1]);
         cout_ptr.push_back((uint32_t)cout_pid.size());
     }
+    // ---- steps IV-V: suffix and end-node merging
+    std::vector<uint32_t> depth_of(N);
+    for (uint64_t v = 0; v < N; v++) depth_of[v] = q[v].depth;
+    std::vector<uint32_t> dag_node, dag_child, dag_skip, rank_term;
+    std::vector<uint8_t> dag_label;
+    uint64_t ND = 0, ED = 0, bytes_merged = 0, bytes_merged_crs = 0;
+    uint64_t pipe_depth = 0, bytes_pipe_trunc = 0, bytes_pipe_merged = 0, bytes_pipe_crs = 0;
+    if (opt.merge_suffixes) {
+        // (a) the paper's pipeline, byte accounting only: cut at 8 levels
+        // or the requested depth, merged without pattern identity
+        pipe_depth = d_trunc ? d_trunc : 8u;
+        std::vector<uint32_t> pcls;
+        const uint32_t npc = merge_classes(node_word, label, depth_of, (uint32_t)pipe_depth, pcls);
+        std::vector<uint32_t> preps(npc, kNone);
+        uint64_t n_pt = 0;
+        for (uint64_t v = 0; v < N; v++)
+            if (pcls[v] != kNone) {
+                n_pt++;
+                if (preps[pcls[v]] == kNone) preps[pcls[v]] = (uint32_t)v;
+            }
+        bytes_pipe_trunc = 36 * n_pt;
+        bytes_pipe_merged = 36ull * npc;
+        bytes_pipe_crs = 4 * (2 * crs_nnz(node_word, label, depth_of, (uint32_t)pipe_depth, preps) + npc + 1);
+        // (b) the id-preserving minimal DAG of the untruncated trie (scannable)
+        std::vector<uint32_t> cls;
+        const uint32_t nc = merge_classes(node_word, label, depth_of, kNone, cls);
+        std::vector<uint32_t> rep(nc, kNone);
+        for (uint64_t v = 0; v < N; v++)
+            if (rep[cls[v]] == kNone) rep[cls[v]] = (uint32_t)v;
+        // strings below each node (its own terminal + its children's), bottom-up
+        std::vector<uint32_t> cnt(N, 0);
+        for (uint64_t v = N; v-- > 0;) {
+            uint64_t c = (node_word[v] & kTermBit) ? 1 : 0;
+            for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++) c += cnt[e + 1];
+            cnt[v] = (uint32_t)c;
+        }
+        // DAG nodes numbered breadth-first from the root's class
+        std::vector<uint32_t> dnum(nc, kNone), dorder;
+        dorder.push_back(cls[0]);
+        dnum[cls[0]] = 0;
+        for (size_t hq = 0; hq < dorder.size(); hq++) {
+            const uint32_t v = rep[dorder[hq]];
+            for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++) {
+                const uint32_t cc = cls[e + 1];
+                if (dnum[cc] == kNone) {
+                    dnum[cc] = (uint32_t)dorder.size();
+                    dorder.push_back(cc);
+                }
+            }
+        }
+        for (uint32_t c : dorder) {
+            const uint32_t v = rep[c];
+            const uint32_t t = (node_word[v] & kTermBit) ? 1u : 0u;
+            dag_node.push_back((uint32_t)dag_label.size() | (t ? kTermBit : 0u));
+            uint32_t acc = t;
+            for (uint32_t e = node_word[v] & kEdgeMask; e < (node_word[v + 1] & kEdgeMask); e++) {
+                dag_label.push_back(label[e]);
+                dag_child.push_back(dnum[cls[e + 1]]);
+                dag_skip.push_back(acc);
+                acc += cnt[e + 1];
+            }
+        }
+        ND = dorder.size();
+        ED = dag_label.size();
+        dag_node.push_back((uint32_t)ED);
+        if (ND > kEdgeMask || ED > kEdgeMask) {
+            err = "pfac_build: merged DAG exceeds 2^30-1 nodes or edges";
+            return kStatusLimit;
+        }
+        // rank r = the r-th distinct pattern string (sorted order) -> its terminal index
+        std::vector<uint32_t> new_ti(T, kNone);
+        for (uint32_t i = 0; i < nterm_old.size(); i++) new_ti[nterm_old[i]] = i;
+        for (uint32_t j = 0; j < m; j++)
+            if (end_at[j] != kNone && (j == 0 || end_at[j - 1] != end_at[j])) rank_term.push_back(new_ti[old_ti[end_at[j]]]);
+        bytes_merged = 36 * ND;
+        std::vector<uint32_t> reps_all(rep.begin(), rep.end());
+        bytes_merged_crs = 4 * (2 * crs_nnz(node_word, label, depth_of, kNone, reps_all) + ND + 1);
+    }
+
     const uint64_t N_full = N;
     node_word.swap(cnode);
     label.swap(clabel);
@@ -625,6 +777,21 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     h.kset_empty = kset_empty;
     h.off_entry = entry.empty() ? 0 : o;
     o = align256(o + 4 * entry.size());
+    if (ND) {  // merged DAG sections (steps IV-V)
+        h.off_dag_node = o;  o = align256(o + 4 * (ND + 1));
+        h.off_dag_label = o; o = align256(o + ED + 16);
+        h.off_dag_child = o; o = align256(o + 4 * ED);
+        h.off_dag_skip = o;  o = align256(o + 4 * ED);
+        h.off_rank_term = o; o = align256(o + 4 * rank_term.size());
+    }
+    h.n_dag_nodes = ND;
+    h.n_dag_edges = ED;
+    h.bytes_merged = bytes_merged;
+    h.bytes_merged_crs = bytes_merged_crs;
+    h.pipe_depth = pipe_depth;
+    h.bytes_pipe_trunc = bytes_pipe_trunc;
+    h.bytes_pipe_merged = bytes_pipe_merged;
+    h.bytes_pipe_crs = bytes_pipe_crs;
     h.entry_log2 = entry_log2;
     h.n_level1 = B;
     h.n_tails = NT;
@@ -671,6 +838,15 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
     }
     if (!kset.empty()) std::memcpy(p + h.off_kset, kset.data(), 4 * kset.size());
     if (!entry.empty()) std::memcpy(p + h.off_entry, entry.data(), 4 * entry.size());
+    if (ND) {
+        std::memcpy(p + h.off_dag_node, dag_node.data(), 4 * (ND + 1));
+        if (ED) {
+            std::memcpy(p + h.off_dag_label, dag_label.data(), ED);
+            std::memcpy(p + h.off_dag_child, dag_child.data(), 4 * ED);
+            std::memcpy(p + h.off_dag_skip, dag_skip.data(), 4 * ED);
+        }
+        std::memcpy(p + h.off_rank_term, rank_term.data(), 4 * rank_term.size());
+    }
     return kStatusOk;
 }
 
@@ -783,6 +959,20 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
         for (uint64_t v = 0; ok && v < N; v++)
             if (node[v] & kTermBit) ok = k < h.n_kept_terminals && tn[k++] == v;
         ok = ok && k == h.n_kept_terminals;
+        // merged DAG (steps IV-V): CSR bounds, child ids, rank table
+        if (ok && h.n_dag_nodes) {
+            const uint64_t ND = h.n_dag_nodes, ED = h.n_dag_edges;
+            ok = ND >= 1 && ND <= kEdgeMask && ED <= kEdgeMask && in(h.off_dag_node, 4 * (ND + 1)) &&
+                 in(h.off_dag_label, ED + 16) && in(h.off_dag_child, 4 * ED) && in(h.off_dag_skip, 4 * ED) &&
+                 in(h.off_rank_term, 4 * T);
+            const uint32_t *dn = reinterpret_cast<const uint32_t *>(p + h.off_dag_node);
+            const uint32_t *dc = reinterpret_cast<const uint32_t *>(p + h.off_dag_child);
+            const uint32_t *rt = reinterpret_cast<const uint32_t *>(p + h.off_rank_term);
+            ok = ok && (dn[0] & kEdgeMask) == 0 && (dn[ND] & kEdgeMask) == ED;
+            for (uint64_t v = 0; ok && v < ND; v++) ok = (dn[v] & kEdgeMask) <= (dn[v + 1] & kEdgeMask);
+            for (uint64_t e = 0; ok && e < ED; e++) ok = dc[e] < ND;
+            for (uint64_t r = 0; ok && r < T; r++) ok = rt[r] < T;
+        }
         // pid lists: monotone offsets, ids < n_patterns
         for (uint64_t i = 0; ok && i < T; i++) ok = out_ptr[i] <= out_ptr[i + 1];
         const uint32_t *pid = reinterpret_cast<const uint32_t *>(p + h.off_out_pid);

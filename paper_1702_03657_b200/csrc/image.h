@@ -114,6 +114,26 @@
 //                     an empty slot (absent).  A start whose key is absent
 //                     cannot match: the walk is skipped (the filter's false
 //                     positives).
+//   dag_* (built with merge_suffixes; PAPER.md:80 steps IV-V "similar
+//                     suffixes are merged", "end nodes merged") the minimal
+//                     DAG of the untruncated trie: identical sub-tries
+//                     (terminal flag, labels, child classes) are one node, so
+//                     every leaf is one node (end-node merging) and equal
+//                     suffix paths are shared.  Pattern identity survives by
+//                     path rank: each node counts the distinct pattern
+//                     strings of its sub-DAG, and a walk that adds
+//                     dag_skip[e] (the node's own terminal + the counts of
+//                     its earlier children) at every edge e reaches a
+//                     terminal with the lexicographic rank r of the string it
+//                     spelled; rank_term[r] = that string's terminal index
+//                     (its pid list).  dag_node u32[ND+1] (first edge |
+//                     terminal bit), dag_label u8[ED] (ascending per node),
+//                     dag_child u32[ED], dag_skip u32[ED], rank_term u32[T].
+//   pipe_*: byte accounting only, the paper's own pipeline:
+//                     the trie truncated at pipe_depth levels, its identical
+//                     sub-tries merged by terminal flag and shape alone (no
+//                     pattern identity: the paper's terminals carry none),
+//                     then its N x 9 CRS (2 nnz + n + 1 words).
 //   entry  u32[2^entry_log2][4]  (filter kinds 4 and 3; D = the filter gram:
 //                     8 bytes, or 16 DNA bases; every pattern has >= D bytes)
 //                     the entry table: one entry {x0, x1, node, depth} per
@@ -140,7 +160,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 17;
+constexpr uint32_t kVersion = 18;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -173,7 +193,11 @@ struct ImageHeader {
     uint64_t n_cand;                   // verify candidate records (after the n_tails node records)
     uint32_t trunc_depth, trunc_pad;   // PAPER.md:80 step III depth d (0: untruncated); 0
     uint64_t bytes_truncated;          // 36 B x nodes of depth <= d (the paper's truncated trie)
-    uint8_t pad[512 - 256 - 64];
+    // steps IV-V merged DAG, id-preserving (0 sections: not built; see dag_* below)
+    uint64_t n_dag_nodes, n_dag_edges, off_dag_node, off_dag_label, off_dag_child, off_dag_skip, off_rank_term;
+    uint64_t bytes_merged, bytes_merged_crs;               // 36 B x DAG nodes; its N x 9 CRS words x 4
+    uint64_t pipe_depth, bytes_pipe_trunc, bytes_pipe_merged, bytes_pipe_crs;  // the paper's pipeline (below)
+    uint8_t pad[512 - 256 - 64 - 104];
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 

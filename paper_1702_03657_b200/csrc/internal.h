@@ -32,6 +32,7 @@ struct BuildOpts {
     uint32_t pair_bits_per_key = 512;  // kind 2 sizing
     uint32_t gram8_bits_per_key = 32;  // kind 4 sizing
     uint32_t truncate_depth = 0;       // 0: untruncated
+    uint32_t merge_suffixes = 0;       // 1: also build the id-preserving merged DAG (steps IV-V)
 };
 
 int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, const BuildOpts &opt,
@@ -85,6 +86,15 @@ int plan_query(const DevTrie &t, const uint8_t *host_image, int device, uint64_t
                const pfac_plan_options &o, pfac_plan_info *out, std::string &err);
 
 uint32_t launches_per_call();
+
+// The merged-DAG scan (dag.cu; plan form PFAC_FORM_MERGED_DAG): three
+// stream-ordered launches; its block totals live at kWsDagOffset of the
+// caller's workspace (after the main scan's header and CTA totals).
+constexpr uint64_t kWsDagOffset = 256 + 16 * 1024;
+uint64_t dag_workspace_bytes(uint64_t n_starts);
+int launch_dag(const ImageHeader &h, const uint8_t *d_img, const uint8_t *d_text, uint64_t readable_len,
+               uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid, uint64_t capacity,
+               uint64_t *d_count, void *d_ws, uint64_t ws_bytes, CUstream_st *stream, std::string &err);
 #ifdef PFAC_TIMING
 int debug_timing(unsigned long long *host, uint64_t n);
 #endif

@@ -105,6 +105,7 @@ struct WsHeader {
 static_assert(sizeof(WsHeader) == 256, "");
 // fixed part: header | cta_total[kMaxCtas] u64 | pool_total[kMaxCtas] u64
 constexpr uint64_t kWsFixed = sizeof(WsHeader) + 16ull * kMaxCtas;
+static_assert(kWsFixed == kWsDagOffset, "the merged-DAG scan's block totals follow the fixed part");
 constexpr uint32_t kNoRound = 0xFFFFFFFFu;  // take(): no round left
 
 struct ScanArgs {
@@ -1592,7 +1593,7 @@ int check_plan_options(const pfac_plan_options &o, std::string &err) {
               o.max_filter_rep_log2 >= -1 && o.max_filter_rep_log2 <= 5 &&
               (o.ring_slots == -1 || o.ring_slots == 2 || o.ring_slots == 3) && o.ctg64 >= -1 && o.ctg64 <= 64 &&
               o.pool64 >= -1 && o.pool64 <= 32 && o.stage2 >= -1 && o.stage2 <= 1 && o.entry >= -1 &&
-              o.entry <= 1 && o.l2_persist <= 1;
+              o.entry <= 1 && o.l2_persist <= 1 && o.form <= PFAC_FORM_MERGED_DAG;
     for (uint32_t r : o.reserved) ok = ok && r == 0;
     if (!ok) {
         err = "pfac_plan_options: bad struct_bytes, reserved field or value";
@@ -1819,7 +1820,7 @@ int workspace_bytes_for(uint64_t n_starts, int device, uint64_t *out, std::strin
     int st = device_info(device, di, err);
     if (st != kStatusOk) return st;
     const Geometry g = geometry(n_starts, di.sms);
-    *out = g.ws_bytes;
+    *out = std::max<uint64_t>(g.ws_bytes, dag_workspace_bytes(n_starts));  // (either form)
     return kStatusOk;
 }
 

@@ -10,7 +10,7 @@ TERM = 0x80000000
 TAIL = 0x40000000
 MASK = 0x3FFFFFFF
 
-_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II Q II Q")
+_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II Q II Q QQQQQQQ QQ QQQQ")
 VERIFY = 0xFFFFFFFE
 
 
@@ -22,7 +22,10 @@ def parse(image: bytes) -> dict:
             "off_filter", "bytes_uncompressed", "bytes_dense_stt", "bytes_paper_crs", "bytes_csr_core",
             "n_tails", "n_tail_bytes", "off_tail_bits", "off_tail_rank", "off_tails", "off_tail_bytes",
             "n_level1", "off_level1", "n_kept_terminals", "n_nodes_full", "off_kset", "kset_log2", "kset_empty", "off_pair",
-            "off_entry", "entry_log2", "entry_pad", "n_cand", "trunc_depth", "trunc_pad", "bytes_truncated"]
+            "off_entry", "entry_log2", "entry_pad", "n_cand", "trunc_depth", "trunc_pad", "bytes_truncated",
+            "n_dag_nodes", "n_dag_edges", "off_dag_node", "off_dag_label", "off_dag_child", "off_dag_skip",
+            "off_rank_term", "bytes_merged", "bytes_merged_crs", "pipe_depth", "bytes_pipe_trunc",
+            "bytes_pipe_merged", "bytes_pipe_crs"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
@@ -45,6 +48,13 @@ def parse(image: bytes) -> dict:
     h["pair"] = buf[h["off_pair"]:h["off_pair"] + 8192].view(np.uint32).reshape(256, 8)
     if h["off_kset"]:
         h["kset"] = buf[h["off_kset"]:h["off_kset"] + (4 << h["kset_log2"])].view(np.uint32)
+    if h["n_dag_nodes"]:
+        ND, ED = h["n_dag_nodes"], h["n_dag_edges"]
+        h["dag_node"] = buf[h["off_dag_node"]:h["off_dag_node"] + 4 * (ND + 1)].view(np.uint32)
+        h["dag_label"] = buf[h["off_dag_label"]:h["off_dag_label"] + ED]
+        h["dag_child"] = buf[h["off_dag_child"]:h["off_dag_child"] + 4 * ED].view(np.uint32)
+        h["dag_skip"] = buf[h["off_dag_skip"]:h["off_dag_skip"] + 4 * ED].view(np.uint32)
+        h["rank_term"] = buf[h["off_rank_term"]:h["off_rank_term"] + 4 * T].view(np.uint32)
     if h["off_entry"]:
         h["entry"] = buf[h["off_entry"]:h["off_entry"] + (16 << h["entry_log2"])].view(np.uint32).reshape(-1, 4)
     return h
@@ -221,3 +231,32 @@ def match(h, text: bytes, readable=None, n_starts=None):
             for r in range(int(h["out_ptr"][ti]), int(h["out_ptr"][ti + 1])):
                 rows.append((i, int(h["out_pid"][r])))
     return rows
+
+
+def dag_walk(h, text, i, L):
+    """Merged DAG (image.h dag_*): walk from the root adding each edge's rank
+    skip; the rank at the deepest terminal reached -> its terminal index."""
+    node, lab, child, skip = h["dag_node"], h["dag_label"], h["dag_child"], h["dag_skip"]
+    v, rank, last, j = 0, 0, None, i
+    while j < L:
+        a, b = int(node[v]) & MASK, int(node[v + 1]) & MASK
+        k = int(np.searchsorted(lab[a:b], text[j]))
+        if k >= b - a or lab[a + k] != text[j]:
+            break
+        rank += int(skip[a + k])
+        v = int(child[a + k])
+        j += 1
+        if int(node[v]) & TERM:
+            last = rank
+    return None if last is None else int(h["rank_term"][last])
+
+
+def dag_match(h, text, readable=None, n_starts=None):
+    L = len(text) if readable is None else readable
+    ns = L if n_starts is None else n_starts
+    out = []
+    for i in range(ns):
+        t = dag_walk(h, text, i, L)
+        if t is not None:
+            out += [(i, int(p)) for p in h["out_pid"][h["out_ptr"][t]:h["out_ptr"][t + 1]]]
+    return out

@@ -427,3 +427,36 @@ def test_truncated_c4_full_exact():
     pos, pid = pf.Trie(ps, truncate_depth=8).match(host.to(DEV))
     want = oracle.Trie(ps).match(host.numpy())
     assert_same((pos.cpu().numpy().astype(np.uint64), pid.cpu().numpy().astype(np.uint32)), want, "C4 depth 8")
+
+
+# ------------------------------------------- merged DAG (NEXT-2) on the GPU
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_merged_dag_scan_exact(cid):
+    """The id-preserving merged DAG (PAPER.md:80 steps IV-V) scanned on the
+    device (plan form PFAC_FORM_MERGED_DAG: path-rank walks) gives the
+    oracle's rows exactly; the main form of the same handle too."""
+    ps = gen.patterns(cid)
+    n = 1024 if cid == 1 else 2 << 20
+    text = gen.text(cid, 0, n)
+    want = oracle.Trie(ps).match(text, engine="ac" if cid == 5 else "pfac")
+    t = pf.Trie(ps, merge_suffixes=1)
+    assert_same(gpu_rows(t, text, offset=1, form="merged_dag"), want, f"C{cid} merged DAG")
+    assert_same(gpu_rows(t, text), want, f"C{cid} CSR form of a merged build")
+
+
+def test_merged_dag_random_tiny_gpu():
+    rng = np.random.default_rng(33)
+    for trial in range(120):
+        sigma = int(rng.choice([2, 4, 256]))
+        alpha = rng.choice(256, size=sigma, replace=False)
+        m = int(rng.integers(1, 40))
+        pats = [bytes(alpha[rng.integers(0, sigma, int(rng.integers(1, 14)))].astype(np.uint8)) for _ in range(m)]
+        if trial % 3 == 0:
+            pats += [pats[0], pats[0] + pats[-1]]
+        n = int(rng.choice([1, 100, 20000, 70000]))
+        text = alpha[rng.integers(0, sigma, n)].astype(np.uint8)
+        L = int(rng.integers(0, n + 1))
+        ns = int(rng.integers(0, L + 1))
+        wp, wq = oracle.Trie(pats).match(text, readable_len=L, lo=0, hi=ns)
+        got = gpu_rows(pf.Trie(pats, merge_suffixes=1), text, readable=L, n_starts=ns, pos_base=7, form="merged_dag")
+        assert_same(got, (wp + np.uint64(7), wq), f"trial {trial}")
