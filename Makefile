@@ -35,6 +35,11 @@ $(PKG)/libpfac_exp1.so: $(CSRC) $(CHDR)
 $(PKG)/libpfac_exp2.so: $(CSRC) $(CHDR)
 	$(NVCC) $(NVFLAGS) -DPFAC_TIMING -DPFAC_EXP=2 -shared -o $@ $(CSRC) -lcudart
 
+# bounds-checked build (device-side index asserts; tools/checked_tests.sh)
+$(PKG)/libpfac_checked.so: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -DPFAC_CHECKED -shared -o $@ $(CSRC) -lcudart
+checked: $(PKG)/libpfac_checked.so
+
 # experiment / instrumented builds (tools/timing.py; never used by tests or bench)
 EXPLIBS := $(PKG)/libpfac_timing.so $(PKG)/libpfac_stream.so $(PKG)/libpfac_exp1.so $(PKG)/libpfac_exp2.so
 exp: $(EXPLIBS)

@@ -36,7 +36,7 @@ struct DagArgs {
     const uint32_t *child;  // [ED]
     const uint32_t *skip;   // [ED]
     const uint32_t *rank_term;
-    uint32_t n_ranks;
+    uint32_t n_ranks, n_nodes, n_edges;
     const uint32_t *out_ptr, *out_pid;
     const uint8_t *text;
     uint64_t readable, n_starts, pos_base;
@@ -70,6 +70,7 @@ __device__ __forceinline__ uint32_t dag_walk(const DagArgs &a, uint64_t i) {
             if (__ldg(a.label + lo) == c) e = lo;
         }
         if (e == kNone) break;  // mismatch: the thread terminates
+        PFAC_CHECK(e < a.n_edges && __ldg(a.child + e) < a.n_nodes);
         rank += __ldg(a.skip + e);
         v = __ldg(a.child + e);
         if (__ldg(a.node + v) & kTermBit) last = rank;
@@ -191,6 +192,8 @@ int launch_dag(const ImageHeader &h, const uint8_t *d_img, const uint8_t *d_text
     a.skip = reinterpret_cast<const uint32_t *>(d_img + h.off_dag_skip);
     a.rank_term = reinterpret_cast<const uint32_t *>(d_img + h.off_rank_term);
     a.n_ranks = (uint32_t)h.n_terminals;
+    a.n_nodes = (uint32_t)h.n_dag_nodes;
+    a.n_edges = (uint32_t)h.n_dag_edges;
     a.out_ptr = reinterpret_cast<const uint32_t *>(d_img + h.off_out_ptr);
     a.out_pid = reinterpret_cast<const uint32_t *>(d_img + h.off_out_pid);
     a.text = d_text;

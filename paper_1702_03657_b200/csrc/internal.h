@@ -13,6 +13,23 @@ struct CUstream_st;
 
 namespace pfac {
 
+#ifdef PFAC_CHECKED
+// Bounds-checked build (libpfac_checked.so; tools/checked_tests.sh): every
+// index the kernel follows into an image section, a shared-memory table, a
+// queue or a workspace array is asserted, and a failed check traps (the
+// launch fails).  It stands in for compute-sanitizer, which this GPU pool
+// does not allow.
+#define PFAC_CHECK(c)          \
+    do {                       \
+        if (!(c)) __trap();    \
+    } while (0)
+#else
+#define PFAC_CHECK(c) \
+    do {              \
+    } while (0)
+#endif
+
+
 // mirrors pfac_status in include/pfac.h
 enum : int {
     kStatusOk = 0,
@@ -67,6 +84,8 @@ struct DevTrie {
     uint32_t exact;
     uint32_t kind;       // filter kind (image.h)
     uint32_t n_nodes;
+    // section sizes (bounds of the checked build, PFAC_CHECKED)
+    uint32_t n_edges, n_records, n_tail_bytes, n_out, n_level1;
 };
 
 DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d_image);

@@ -270,12 +270,15 @@ struct Smem {
 };
 
 __device__ __forceinline__ uint32_t node_word(const ScanArgs &a, const Smem &s, uint32_t v) {
+    PFAC_CHECK(v <= a.t.n_nodes);
     return v <= a.hot_nodes ? s.node[v] : __ldg(a.t.node + v);
 }
 __device__ __forceinline__ uint32_t aux_word(const ScanArgs &a, const Smem &s, uint32_t v) {
+    PFAC_CHECK(v < a.t.n_nodes);
     return v <= a.hot_nodes ? s.aux[v] : __ldg(a.t.aux + v);
 }
 __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, uint32_t e) {
+    PFAC_CHECK(e < a.t.n_edges);
     return e < a.hot_edges ? (uint32_t)s.label[e] : (uint32_t)__ldg(a.t.label + e);
 }
 
@@ -330,7 +333,10 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
     nv = kNone;
     const bool hot = v < a.hot_nodes;  // hot records + bytes are in shared memory
     const uint32_t idx = ax;  // aux word: the record's index (= rank among the record nodes)
+    PFAC_CHECK(idx < a.t.n_records && (!hot || idx < a.hot_tails));
     const uint4 rec = hot ? s.tails[idx] : __ldg(a.t.tails + idx);
+    PFAC_CHECK(rec.z == kVerify ? (uint64_t)rec.x + rec.y <= a.t.n_records
+                                : (uint64_t)rec.x + rec.y <= a.t.n_tail_bytes && (!hot || rec.x + rec.y <= a.hot_tail_bytes + 3));
     if (rec.z == kVerify) {
         // verify leaf of a truncated trie (PAPER.md:80 step III): the
         // candidates (distinct patterns below it, longest first; records and
@@ -339,6 +345,7 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
         // else the deepest terminal passed does
         for (uint32_t c = rec.x; c < rec.x + rec.y; ++c) {
             const uint4 cr = __ldg(a.t.tails + c);
+            PFAC_CHECK((uint64_t)cr.x + cr.y <= a.t.n_tail_bytes && cr.z < a.t.n_terminals);
             if ((uint64_t)j + cr.y > (uint64_t)tx.end) continue;
             const uint32_t *pw = reinterpret_cast<const uint32_t *>(a.t.tail_bytes + cr.x);
             bool eq = true;
@@ -371,6 +378,7 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
                                      bool l1, uint32_t wn, uint32_t ax) {
     uint32_t nv = kNone;
     if (l1) {  // level 1 -> 2 through the bitmap
+        PFAC_CHECK(v >= 1 && v <= a.t.n_level1);
         const uint32_t *bm = s.bm + (v - 1) * 10;
         const uint32_t word = bm[c >> 5];
         if (!((word >> (c & 31)) & 1u)) return kNone;
@@ -584,6 +592,7 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
 #pragma unroll
         for (int k = kPerLane - 1; k >= 0; --k) {
             const uint32_t off = (__umulhi(x[k], kFilterMul) & mask) ^ t;
+            PFAC_CHECK(off < (a.filter_words * 4u << a.rep_log2));
             uint32_t w;
             if (kImm1024)
                 asm("ld.shared.u32 %0, [%1+1024];" : "=r"(w) : "r"(off));
@@ -639,6 +648,7 @@ __device__ __forceinline__ bool kset_probe(const ScanArgs &a, uint32_t key) {
     const uint4 *k4 = reinterpret_cast<const uint4 *>(a.t.kset);
     const uint32_t e = a.t.kset_empty;
     for (uint32_t b = kset_bucket(key, a.t.kset_log2);; b = (b + 1u) & bmask) {
+        PFAC_CHECK(b <= bmask);
         const uint4 q = __ldg(k4 + b);
         if ((q.x == key) | (q.y == key) | (q.z == key) | (q.w == key)) return true;
         if ((q.x == e) | (q.y == e) | (q.z == e) | (q.w == e)) return false;
@@ -651,6 +661,7 @@ __device__ __forceinline__ bool kset_probe(const ScanArgs &a, uint32_t key) {
 __device__ __forceinline__ uint2 entry_find(const ScanArgs &a, uint32_t x0, uint32_t x1) {
     const uint32_t mask = (1u << a.t.entry_log2) - 1u;
     for (uint32_t i = entry_slot(x0, x1, a.t.entry_log2);; i = (i + 1) & mask) {
+        PFAC_CHECK(i <= mask);
         const uint4 e = __ldg(a.t.entry + i);
         if (e.z == kNone) return make_uint2(0u, 0u);
         if (e.x == x0 && e.y == x1) return make_uint2(e.z, e.w);
@@ -720,7 +731,10 @@ __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s,
         const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
         tn = ent ? walk(a, s, gt, 0u, ent & ((1u << kEntShift) - 1u), ent >> kEntShift) : walk(a, s, gt, 0u);
         if (tn != kNone) {
+            PFAC_CHECK(tn < a.t.n_terminals);
             const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
+            PFAC_CHECK(s.out_ptr[tn + 1] <= a.t.n_out);
+            PFAC_CHECK(p < ctg_bytes || cta_round0 + (p >> kRoundLog2) < (a.n_starts + kRound - 1) / kRound);
             if (p < ctg_bytes) rows += cnt;  // the lane's rows in its warp's block (per-warp totals)
             else atomicAdd(a.round_val + cta_round0 + (p >> kRoundLog2), (unsigned long long)cnt);  // dynamic round
         }
@@ -791,6 +805,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
         const uint32_t kb = __ballot_sync(0xffffffffu, ent != kNone);
         if (ent != kNone) {
             const uint32_t idx = nb + __popc(kb & ((1u << lane) - 1u));
+            PFAC_CHECK(idx < kWalkQ);
             bpos[idx] = p;
             if (Kind != 1) bent[idx] = ent;
         }
@@ -1200,6 +1215,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     uint32_t e = dcount + ex;
                     for (uint32_t m = pending; m; m &= m - 1, ++e) {
                         const uint32_t off = lane * kPerLane + (__ffs(m) - 1);
+                        PFAC_CHECK(e < qcap);
                         dpos[e] = rel + off;
                         if (Kind == 1 && a.use_kset) dkey[e] = slot_key<Kind>(p0, off);
                     }
@@ -1812,6 +1828,11 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.exact = h.filter_exact;
     t.kind = h.filter_kind;
     t.n_nodes = (uint32_t)h.n_nodes;
+    t.n_edges = (uint32_t)h.n_edges;
+    t.n_records = (uint32_t)(h.n_tails + h.n_cand);
+    t.n_tail_bytes = (uint32_t)h.n_tail_bytes;
+    t.n_out = (uint32_t)h.n_out;
+    t.n_level1 = (uint32_t)h.n_level1;
     return t;
 }
 

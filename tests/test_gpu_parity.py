@@ -460,3 +460,27 @@ def test_merged_dag_random_tiny_gpu():
         wp, wq = oracle.Trie(pats).match(text, readable_len=L, lo=0, hi=ns)
         got = gpu_rows(pf.Trie(pats, merge_suffixes=1), text, readable=L, n_starts=ns, pos_base=7, form="merged_dag")
         assert_same(got, (wp + np.uint64(7), wq), f"trial {trial}")
+
+
+# ---------------------------------------------- placements (NEXT-4 parity)
+@pytest.mark.parametrize("placement", [{"placement": "global"}, {"placement": "smem"}, {"placement": "big_l1"},
+                                       {"placement": "smem", "l2_persist": 1}, {"placement": "smem", "hot_bytes_cap": 4096},
+                                       {"max_filter_rep_log2": 0, "ring_slots": 2}, {"stage2": 0}, {"stage2": 1}],
+                         ids=["global", "smem", "big_l1", "smem-l2persist", "smem-4KiB", "rep1-slots2", "stage2-off",
+                              "stage2-on"])
+@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+def test_placement_variants_exact(cid, placement):
+    """Every trie placement and plan knob of the Fig. 6-style ablation
+    (tools/placement.py) gives the oracle's rows:
+    placement changes speed only."""
+    ps = gen.patterns(cid)
+    text = gen.text(cid, 0, 2 << 20)
+    want = oracle.Trie(ps).match(text, engine="ac" if cid == 5 else "pfac")
+    t = pf.Trie(ps)
+    if cid == 5 and placement.get("stage2") == 1:
+        placement = {"stage2": 0}  # (no 2-gram stage for the DNA filter)
+    p = t.plan(len(text), **placement)
+    if "placement" in placement:
+        want_pl = pf.PLACEMENTS[placement["placement"]]
+        assert p["placement"] == want_pl or (want_pl == 2 and p["hot_nodes"] <= 8), p
+    assert_same(gpu_rows(t, text, offset=2, **placement), want, f"C{cid} {placement}")
