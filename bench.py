@@ -255,6 +255,22 @@ def time_launches(sc, text, flush, n, reps, stream):
     return statistics.median(ts), sum(ts) / len(ts)
 
 
+STAGE_KINDS = ["uncompressed", "pipe_trunc", "pipe_merged", "pipe_crs", "paper_crs", "merged", "merged_image",
+               "csr_core", "device_image"]
+
+
+def byte_stages(ps):
+    """Fig. 5-style per-stage trie bytes (PAPER.md:80 steps I-V)
+    from a build with merge_suffixes: the paper's pipeline (36 B/node trie ->
+    cut at 8 levels -> merged -> N x 9 CRS) next to this library's exact forms."""
+    import paper_1702_03657_b200 as pf
+    t = pf.Trie(ps, merge_suffixes=1)
+    b = {k: t.nbytes(k) for k in STAGE_KINDS}
+    b["pipe_crs_vs_uncompressed"] = b["pipe_crs"] / b["uncompressed"]
+    b["device_image_vs_uncompressed"] = b["device_image"] / b["uncompressed"]
+    return b
+
+
 def extra_configs(dev, flush, peak, stream):
     """C2, C3, C5 (1-GPU sizes) timed like the headline: side lines only."""
     import torch
@@ -275,7 +291,8 @@ def extra_configs(dev, flush, peak, stream):
         out[f"C{cid}"] = {"workload": WORKLOADS[cid], "text_bytes": n, "us_median": 1e6 * med,
                           "gbps": 8.0 * n / med / 1e9, "hbm_frac": (n + 12 * cnt) / med / 1e9 / peak,
                           "matches": cnt,
-                          "trie_image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed")}
+                          "trie_image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed"),
+                          "trie_bytes_stages": byte_stages(ps)}
         del text, host, sc
         torch.cuda.empty_cache()
     return out
@@ -449,6 +466,19 @@ def main():
                "sample": f"{reps} pass(es) over the first {S} start positions of the C4 text "
                          f"(PFAC bitmap-trie walk, {os.cpu_count()} threads, {tt:.1f} s)"}
 
+    variants = None  # the C4 launch with the trie cut at 8 levels (NEXT-1) and as the merged DAG (NEXT-2)
+    if rank == 0 and world == 1 and not args.no_extras:
+        variants = {}
+        for name, bkw, pkw in [("truncated_depth8", {"truncate_depth": 8}, {}),
+                               ("merged_dag", {"merge_suffixes": 1}, {"form": "merged_dag"})]:
+            tv = pf.Trie(ps, **bkw)
+            sv = pf.Scanner(tv, dev, capacity=max(1 << 20, n_starts // 2048), **pkw)
+            med, _ = time_launches(sv, text, flush, r1 - r0, 5, stream)
+            variants[name] = {"us_median": 1e6 * med, "gbps": 8.0 * n_starts / med / 1e9,
+                              "matches": int(sv.count.item()), "equal_count": int(sv.count.item()) == count,
+                              "trie_bytes": {k: tv.nbytes(k) for k in ("truncated", "device_image")
+                                             if k != "truncated" or bkw.get("truncate_depth")}}
+            del sv, tv
     extras = None
     if rank == 0 and world == 1 and not args.no_extras:
         del text
@@ -478,7 +508,9 @@ def main():
             "trie_bytes": {"device_image": trie.nbytes("device_image"), "uncompressed": trie.nbytes("uncompressed"),
                            "csr_core": trie.nbytes("csr_core"), "paper_crs": trie.nbytes("paper_crs"),
                            "dense_stt": trie.nbytes("dense_stt"),
-                           "image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed")},
+                           "image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed"),
+                           "stages": byte_stages(ps) if rank == 0 else None},
+            "variants": variants,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
             "plan": trie.plan(n_starts, local_rank),
             "paper_context": PAPER_CONTEXT,

@@ -60,23 +60,26 @@ def _worker(rank, world, port, n_text, q):
                 np.array_equal(out[1].numpy().astype(np.uint32), full[1])
             q.put(("r0", img_ok, same, len(full[0])))
         else:
-            q.put(("r1", img_ok, out is None, 0))
+            q.put((f"r{rank}", img_ok, out is None, 0))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_text", [3 * 4096 + 17, 2 << 20])
-def test_gloo_world2_broadcast_shard_gather(n_text):
+@pytest.mark.parametrize("world,n_text", [(2, 3 * 4096 + 17), (2, 2 << 20), (3, (2 << 20) + 999)])
+def test_gloo_broadcast_shard_gather(world, n_text):
+    """World 2 and 3 (uneven shards and counts): broadcast, shard + halo,
+    point-to-point gather to rank 0 == the unsharded oracle result."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_text, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_text, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict((x[0], x[1:]) for x in [q.get(timeout=300) for _ in procs])
+    res = [q.get(timeout=300) for _ in procs]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res["r0"][0] and res["r1"][0], "broadcast image differs"
-    assert res["r0"][1], "gathered shards != unsharded oracle result"
-    assert res["r1"][1]
+    assert all(r[1] for r in res), "broadcast image differs"
+    r0 = [r for r in res if r[0] == "r0"][0]
+    assert r0[2], "gathered shards != unsharded oracle result"
+    assert all(r[2] for r in res if r[0] != "r0")
