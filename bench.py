@@ -265,7 +265,8 @@ def byte_stages(ps):
     cut at 8 levels -> merged -> N x 9 CRS) next to this library's exact forms."""
     import paper_1702_03657_b200 as pf
     t = pf.Trie(ps, merge_suffixes=1)
-    b = {k: t.nbytes(k) for k in STAGE_KINDS}
+    b = {k: t.nbytes(k) for k in STAGE_KINDS if k != "device_image"}
+    b["device_image"] = pf.Trie(ps).nbytes("device_image")  # the product build (no DAG sections)
     b["pipe_crs_vs_uncompressed"] = b["pipe_crs"] / b["uncompressed"]
     b["device_image_vs_uncompressed"] = b["device_image"] / b["uncompressed"]
     return b

@@ -1791,7 +1791,7 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     f.entry = a.use_entry;
     f.kset = a.use_kset;
     f.pool_rounds = (uint32_t)(geo.n_rounds - a.n_main);
-    f.placement = big_l1 ? PFAC_PLACE_BIG_L1 : (H > 1 ? PFAC_PLACE_SMEM : PFAC_PLACE_GLOBAL);
+    f.placement = big_l1 ? PFAC_PLACE_BIG_L1 : o.placement == PFAC_PLACE_GLOBAL ? PFAC_PLACE_GLOBAL : PFAC_PLACE_SMEM;
     f.rounds_per_cta = a.rounds_per_cta;
     f.main_rounds = a.n_main;
     return kStatusOk;
