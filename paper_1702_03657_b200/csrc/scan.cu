@@ -161,6 +161,31 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// (the same on 32-bit shared-window addresses: no generic->shared conversion per use)
+__device__ __forceinline__ void mbar_arrive_expect_tx_s(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s_s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
+                                           uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     while (!done) {
@@ -668,6 +693,23 @@ __device__ __forceinline__ uint2 entry_find(const ScanArgs &a, uint32_t x0, uint
     }
 }
 
+// The shared-memory views of the trie tables (the kernel's layout, ScanArgs).
+__device__ __forceinline__ Smem make_smem(const ScanArgs &a) {
+    extern __shared__ __align__(128) uint8_t smem_base[];
+    Smem s;
+    // terminal tables: shared-memory copies when staged (generic pointers)
+    s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem_base + a.off_terms) : a.t.out_ptr;
+    s.term_node = a.off_terms ? s.out_ptr + a.t.n_terminals + 1 : a.t.term_node;
+    s.root = reinterpret_cast<const uint32_t *>(smem_base + a.off_root);
+    s.bm = reinterpret_cast<const uint32_t *>(smem_base + a.off_bm);
+    s.node = reinterpret_cast<const uint32_t *>(smem_base + a.off_node);
+    s.aux = reinterpret_cast<const uint32_t *>(smem_base + a.off_aux);
+    s.label = smem_base + a.off_label;
+    s.tails = reinterpret_cast<const uint4 *>(smem_base + a.off_tails);
+    s.tail_bytes = smem_base + a.off_tbytes;
+    return s;
+}
+
 // Deferred starts are decided in two ways:
 //  * direct (kinds 0 and 2, kind 1 without the key set, kinds 3/4 without
 //    the entry table): every queued start is walked from the root;
@@ -719,10 +761,11 @@ __device__ __forceinline__ uint32_t probe_start(const ScanArgs &a, const GlobalT
 // added to the lane's block rows or their round's count.  Returns the new hit
 // count.
 template <int Kind>
-__device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s, uint64_t cta_lo, uint64_t cta_round0,
+__device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, uint64_t cta_lo, uint64_t cta_round0,
                                                uint32_t ctg_bytes, const uint32_t *bpos, const uint32_t *bent,
                                                uint32_t m, uint2 *hits, uint32_t n_hits, unsigned long long &rows) {
     const int lane = threadIdx.x & 31;
+    const Smem s = make_smem(a);  // (built here: walks are rare in the two-level kinds)
     uint32_t p = 0, tn = kNone;
     if ((uint32_t)lane < m) {
         p = bpos[lane];
@@ -748,23 +791,6 @@ __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s,
     return n_hits + __popc(hb);
 }
 
-// The shared-memory views of the trie tables (the kernel's layout, ScanArgs).
-__device__ __forceinline__ Smem make_smem(const ScanArgs &a) {
-    extern __shared__ __align__(128) uint8_t smem_base[];
-    Smem s;
-    // terminal tables: shared-memory copies when staged (generic pointers)
-    s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem_base + a.off_terms) : a.t.out_ptr;
-    s.term_node = a.off_terms ? s.out_ptr + a.t.n_terminals + 1 : a.t.term_node;
-    s.root = reinterpret_cast<const uint32_t *>(smem_base + a.off_root);
-    s.bm = reinterpret_cast<const uint32_t *>(smem_base + a.off_bm);
-    s.node = reinterpret_cast<const uint32_t *>(smem_base + a.off_node);
-    s.aux = reinterpret_cast<const uint32_t *>(smem_base + a.off_aux);
-    s.label = smem_base + a.off_label;
-    s.tails = reinterpret_cast<const uint4 *>(smem_base + a.off_tails);
-    s.tail_bytes = smem_base + a.off_tbytes;
-    return s;
-}
-
 struct FlushOut {
     uint32_t n_hits;  // hit records produced so far
     uint32_t nb;      // walk-queue entries left
@@ -782,13 +808,12 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
                                                 uint32_t n, uint32_t *bpos, uint32_t *bent, uint32_t nb, bool final,
                                                 uint2 *hits, uint32_t n_hits) {
     const ScanArgs &a = *ap;
-    const Smem s = make_smem(a);
     const int lane = threadIdx.x & 31;
     unsigned long long rows = 0;
     __syncwarp();
     if (!two_level<Kind>(a)) {  // direct: walk every queued start
         for (uint32_t j0 = 0; j0 < n; j0 += 32)
-            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, dpos + j0, nullptr, min(32u, n - j0), hits,
+            n_hits = walk_batch<Kind>(a, cta_lo, cta_round0, ctg_bytes, dpos + j0, nullptr, min(32u, n - j0), hits,
                                       n_hits, rows);
         __syncwarp();
         return FlushOut{n_hits, 0u, (uint32_t)rows};
@@ -812,7 +837,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
         nb += __popc(kb);
         if (nb >= 32) {  // walk the first 32, keep the rest (< 32) at the front
             __syncwarp();
-            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, 32u,
+            n_hits = walk_batch<Kind>(a, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, 32u,
                                       hits, n_hits, rows);
             uint32_t rp = 0, re = 0;
             const bool mv = (uint32_t)lane + 32u < nb;
@@ -831,7 +856,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
     }
     if (final && nb) {
         __syncwarp();
-        n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, nb, hits,
+        n_hits = walk_batch<Kind>(a, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, nb, hits,
                                   n_hits, rows);
         nb = 0;
     }
@@ -979,9 +1004,11 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         uint8_t *dst = ring + slot * kSlotBytes;
         if (r < n_fast) {  // the whole slot is readable and aligned: one bulk copy
             if (lane == 0) {
+                const uint32_t ws = smem_u32(wsm), bar = ws + WL.bars + 8u * slot;
                 fence_proxy_async_smem();  // prior generic accesses of the slot precede the async write
-                mbar_arrive_expect_tx(&bars[slot], kSlotBytes);
-                bulk_g2s(dst, a.text + cta_lo + (uint64_t)r * kRound, kSlotBytes, &bars[slot], policy);
+                mbar_arrive_expect_tx_s(bar, kSlotBytes);
+                bulk_g2s_s(ws + WL.ring + slot * kSlotBytes, a.text + cta_lo + (uint64_t)r * kRound, kSlotBytes, bar,
+                           policy);
             }
             return;
         }
@@ -1125,7 +1152,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             __syncwarp();  // every lane's reads of that slot precede its refill
             rid[kSlots - 1] = take();
             if (rid[kSlots - 1] != kNoRound) issue(rid[kSlots - 1], slot == 0 ? kSlots - 1 : slot - 1);
-            mbar_wait(&bars[slot], phase);
+            mbar_wait_s(smem_u32(wsm) + WL.bars + 8u * slot, phase);
 #ifdef PFAC_TIMING
             if (taken == kSlots) STAMP(6);  // the first round's text is in
 #endif
