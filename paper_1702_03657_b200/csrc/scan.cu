@@ -1241,10 +1241,15 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 if (tot <= qcap) {  // the common case: one pass
                     uint32_t e = dcount + ex;
                     for (uint32_t m = pending; m; m &= m - 1, ++e) {
-                        const uint32_t off = lane * kPerLane + (__ffs(m) - 1);
                         PFAC_CHECK(e < qcap);
-                        dpos[e] = rel + off;
-                        if (Kind == 1 && a.use_kset) dkey[e] = slot_key<Kind>(p0, off);
+                        dpos[e] = rel + lane * kPerLane + (__ffs(m) - 1);
+                    }
+                    if (Kind == 1 && a.use_kset) {
+                        // the keys of the new entries, one per lane (the per-lane loop
+                        // above only scatters offsets: it runs max-over-lanes times)
+                        __syncwarp();
+                        for (uint32_t j = dcount + (uint32_t)lane; j < dcount + tot; j += 32)
+                            dkey[j] = slot_key<Kind>(p0, dpos[j] - rel);
                     }
                     dcount += tot;
                     __syncwarp();
