@@ -784,6 +784,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
         h.off_dag_skip = o;  o = align256(o + 4 * ED);
         h.off_rank_term = o; o = align256(o + 4 * rank_term.size());
     }
+    h.off_rec = o;  o = align256(o + 16 * NI);  // node records (image.h)
     h.n_dag_nodes = ND;
     h.n_dag_edges = ED;
     h.bytes_merged = bytes_merged;
@@ -837,6 +838,15 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
         }
     }
     if (!kset.empty()) std::memcpy(p + h.off_kset, kset.data(), 4 * kset.size());
+    {   // node records {node[v], node[v+1], aux[v], 0}
+        uint32_t *rec = reinterpret_cast<uint32_t *>(p + h.off_rec);
+        for (uint64_t v = 0; v < NI; v++) {
+            rec[4 * v] = node_word[v];
+            rec[4 * v + 1] = node_word[v + 1];
+            rec[4 * v + 2] = aux[v];
+            rec[4 * v + 3] = 0;
+        }
+    }
     if (!entry.empty()) std::memcpy(p + h.off_entry, entry.data(), 4 * entry.size());
     if (ND) {
         std::memcpy(p + h.off_dag_node, dag_node.data(), 4 * (ND + 1));
@@ -959,6 +969,11 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
         for (uint64_t v = 0; ok && v < N; v++)
             if (node[v] & kTermBit) ok = k < h.n_kept_terminals && tn[k++] == v;
         ok = ok && k == h.n_kept_terminals;
+        // node records: copies of the node and aux words
+        ok = ok && in(h.off_rec, 16 * N);
+        const uint32_t *rc = reinterpret_cast<const uint32_t *>(p + h.off_rec);
+        for (uint64_t v = 0; ok && v < N; v++)
+            ok = rc[4 * v] == node[v] && rc[4 * v + 1] == node[v + 1] && rc[4 * v + 2] == aux[v] && rc[4 * v + 3] == 0;
         // merged DAG (steps IV-V): CSR bounds, child ids, rank table
         if (ok && h.n_dag_nodes) {
             const uint64_t ND = h.n_dag_nodes, ED = h.n_dag_edges;

@@ -19,6 +19,9 @@
 //                     else 0.  Read next to the node word, it saves the walk a
 //                     dependent label (or rank) load per level.
 //   label  u8[E]      edge labels (CRS val, one byte per edge).
+//   rec    uint4[N]   per node {node[v], node[v+1], aux[v], 0}: the three
+//                     words a walk level needs, in one 16-byte load (for the
+//                     nodes not staged in shared memory; v19).
 //   term_node u32[TK] ascending ids of the terminal nodes kept in the image
 //                     (terminal indices 0..TK-1); terminal indices TK..T-1 are
 //                     the ends of the compressed tails, in tail order.
@@ -160,7 +163,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 18;
+constexpr uint32_t kVersion = 19;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -197,7 +200,8 @@ struct ImageHeader {
     uint64_t n_dag_nodes, n_dag_edges, off_dag_node, off_dag_label, off_dag_child, off_dag_skip, off_rank_term;
     uint64_t bytes_merged, bytes_merged_crs;               // 36 B x DAG nodes; its N x 9 CRS words x 4
     uint64_t pipe_depth, bytes_pipe_trunc, bytes_pipe_merged, bytes_pipe_crs;  // the paper's pipeline (below)
-    uint8_t pad[512 - 256 - 64 - 104];
+    uint64_t off_rec;                  // node records uint4[N] (below)
+    uint8_t pad[512 - 256 - 64 - 112];
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 

@@ -60,6 +60,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err);
 struct DevTrie {
     const uint32_t *node;
     const uint32_t *aux;  // per node: record index or packed labels (image.h)
+    const uint4 *rec;     // per node: {node[v], node[v+1], aux[v], 0} (image.h)
     const uint8_t *label;
     const uint32_t *term_node;
     const uint32_t *out_ptr;

@@ -294,14 +294,6 @@ struct Smem {
     const uint32_t *term_node;  // kept terminal node ids (smem or global)
 };
 
-__device__ __forceinline__ uint32_t node_word(const ScanArgs &a, const Smem &s, uint32_t v) {
-    PFAC_CHECK(v <= a.t.n_nodes);
-    return v <= a.hot_nodes ? s.node[v] : __ldg(a.t.node + v);
-}
-__device__ __forceinline__ uint32_t aux_word(const ScanArgs &a, const Smem &s, uint32_t v) {
-    PFAC_CHECK(v < a.t.n_nodes);
-    return v <= a.hot_nodes ? s.aux[v] : __ldg(a.t.aux + v);
-}
 __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, uint32_t e) {
     PFAC_CHECK(e < a.t.n_edges);
     return e < a.hot_edges ? (uint32_t)s.label[e] : (uint32_t)__ldg(a.t.label + e);
@@ -465,6 +457,23 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
 // Fig. 3: 256-bit child bitmap + offset, child = offset + rank of c among the
 // set bits); deeper nodes use the CSR label list of the image; tail and chain
 // starts compare their path's bytes at once.
+__device__ __forceinline__ void node_load(const ScanArgs &a, const Smem &s, uint32_t v, uint32_t &w, uint32_t &wn,
+                                          uint32_t &ax) {
+    // the node's word, the next node's word (its edge end) and its aux word:
+    // from shared memory for the staged nodes, else one 16-byte record load
+    if (v < a.hot_nodes) {
+        w = s.node[v];
+        wn = s.node[v + 1];
+        ax = s.aux[v];
+    } else {
+        PFAC_CHECK(v < a.t.n_nodes);
+        const uint4 r = __ldg(a.t.rec + v);
+        w = r.x;
+        wn = r.y;
+        ax = r.z;
+    }
+}
+
 template <class Text>
 __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0, uint32_t v0 = 0,
                          uint32_t d0 = 1) {
@@ -472,9 +481,8 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
     // first d0 bytes spell (the depth-8 entry table); else from the root
     uint32_t v = v0 ? v0 : s.root[tx.at(r0)];
     if (v == 0) return kNone;
-    // the node's word, the next node's word (its edge end) and its aux word
-    // are loaded together: no load waits on the branch on the first
-    uint32_t w = node_word(a, s, v), wn = node_word(a, s, v + 1), ax = aux_word(a, s, v);
+    uint32_t w, wn, ax;
+    node_load(a, s, v, w, wn, ax);
     uint32_t last = (w & kTermBit) ? v : kNone;
     uint32_t j = r0 + d0;
     bool l1 = d0 == 1;  // v is a level-1 node: the next step uses its bitmap
@@ -493,9 +501,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
         }
         l1 = false;
         v = nv;
-        w = node_word(a, s, v);
-        wn = node_word(a, s, v + 1);
-        ax = aux_word(a, s, v);
+        node_load(a, s, v, w, wn, ax);
         if (w & kTermBit) last = v;
     }
     return term_of(last);
@@ -761,11 +767,14 @@ __device__ __forceinline__ uint32_t probe_start(const ScanArgs &a, const GlobalT
 // added to the lane's block rows or their round's count.  Returns the new hit
 // count.
 template <int Kind>
-__device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, uint64_t cta_lo, uint64_t cta_round0,
-                                               uint32_t ctg_bytes, const uint32_t *bpos, const uint32_t *bent,
-                                               uint32_t m, uint2 *hits, uint32_t n_hits, unsigned long long &rows) {
+__device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s_in, uint64_t cta_lo,
+                                               uint64_t cta_round0, uint32_t ctg_bytes, const uint32_t *bpos,
+                                               const uint32_t *bent, uint32_t m, uint2 *hits, uint32_t n_hits,
+                                               unsigned long long &rows) {
     const int lane = threadIdx.x & 31;
-    const Smem s = make_smem(a);  // (built here: walks are rare in the two-level kinds)
+    // kind 1 builds its shared-memory views here (its walks are rare: C4
+    // -4.5%); the walk-heavy kinds take them from the flush (C3 -17%)
+    const Smem s = Kind == 1 ? make_smem(a) : s_in;
     uint32_t p = 0, tn = kNone;
     if ((uint32_t)lane < m) {
         p = bpos[lane];
@@ -808,12 +817,13 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
                                                 uint32_t n, uint32_t *bpos, uint32_t *bent, uint32_t nb, bool final,
                                                 uint2 *hits, uint32_t n_hits) {
     const ScanArgs &a = *ap;
+    const Smem s = Kind == 1 ? Smem{} : make_smem(a);  // (see walk_batch)
     const int lane = threadIdx.x & 31;
     unsigned long long rows = 0;
     __syncwarp();
     if (!two_level<Kind>(a)) {  // direct: walk every queued start
         for (uint32_t j0 = 0; j0 < n; j0 += 32)
-            n_hits = walk_batch<Kind>(a, cta_lo, cta_round0, ctg_bytes, dpos + j0, nullptr, min(32u, n - j0), hits,
+            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, dpos + j0, nullptr, min(32u, n - j0), hits,
                                       n_hits, rows);
         __syncwarp();
         return FlushOut{n_hits, 0u, (uint32_t)rows};
@@ -837,7 +847,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
         nb += __popc(kb);
         if (nb >= 32) {  // walk the first 32, keep the rest (< 32) at the front
             __syncwarp();
-            n_hits = walk_batch<Kind>(a, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, 32u,
+            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, 32u,
                                       hits, n_hits, rows);
             uint32_t rp = 0, re = 0;
             const bool mv = (uint32_t)lane + 32u < nb;
@@ -856,7 +866,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
     }
     if (final && nb) {
         __syncwarp();
-        n_hits = walk_batch<Kind>(a, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, nb, hits,
+        n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, nb, hits,
                                   n_hits, rows);
         nb = 0;
     }
@@ -1835,6 +1845,7 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     DevTrie t;
     t.node = reinterpret_cast<const uint32_t *>(d + h.off_node);
     t.aux = reinterpret_cast<const uint32_t *>(d + aux_offset(h.off_node, h.n_nodes));
+    t.rec = reinterpret_cast<const uint4 *>(d + h.off_rec);
     t.label = d + h.off_label;
     t.term_node = reinterpret_cast<const uint32_t *>(d + h.off_term_node);
     t.out_ptr = reinterpret_cast<const uint32_t *>(d + h.off_out_ptr);

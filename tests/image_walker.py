@@ -10,7 +10,7 @@ TERM = 0x80000000
 TAIL = 0x40000000
 MASK = 0x3FFFFFFF
 
-_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II Q II Q QQQQQQQ QQ QQQQ")
+_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II Q II Q QQQQQQQ QQ QQQQ Q")
 VERIFY = 0xFFFFFFFE
 
 
@@ -25,7 +25,7 @@ def parse(image: bytes) -> dict:
             "off_entry", "entry_log2", "entry_pad", "n_cand", "trunc_depth", "trunc_pad", "bytes_truncated",
             "n_dag_nodes", "n_dag_edges", "off_dag_node", "off_dag_label", "off_dag_child", "off_dag_skip",
             "off_rank_term", "bytes_merged", "bytes_merged_crs", "pipe_depth", "bytes_pipe_trunc",
-            "bytes_pipe_merged", "bytes_pipe_crs"]
+            "bytes_pipe_merged", "bytes_pipe_crs", "off_rec"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
