@@ -318,6 +318,34 @@ struct GlobalText {
             if (r + b < end) x |= (uint32_t)__ldg(g + r + b) << (8 * b);
         return x;
     }
+    // Do the L text bytes from r equal the words pw (L <= end - r checked by
+    // the caller)?  The fast path slides over the aligned text words, one load
+    // per 4 bytes; the pattern words come from shared (kHot) or global memory.
+    template <bool kHot>
+    __device__ __forceinline__ bool equal(uint32_t r, const uint32_t *pw, uint32_t L) const {
+        const uintptr_t ad = reinterpret_cast<uintptr_t>(g + r);
+        if (aligned && r + L + 8 <= end) {
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(ad & ~(uintptr_t)3);
+            const uint32_t sh = 8 * (uint32_t)(ad & 3);
+            uint32_t a0 = __ldg(w);
+            for (uint32_t k = 0; k < L; k += 4) {
+                const uint32_t a1 = __ldg(w + (k >> 2) + 1);
+                const uint32_t n = L - k;
+                const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
+                const uint32_t pk = kHot ? pw[k >> 2] : __ldg(pw + (k >> 2));
+                if ((__funnelshift_r(a0, a1, sh) ^ pk) & m) return false;
+                a0 = a1;
+            }
+            return true;
+        }
+        for (uint32_t k = 0; k < L; k += 4) {
+            const uint32_t n = L - k;
+            const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
+            const uint32_t pk = kHot ? pw[k >> 2] : __ldg(pw + (k >> 2));
+            if ((at4(r + k) ^ pk) & m) return false;
+        }
+        return true;
+    }
 };
 
 // Walk from the start at offset r0 to the first mismatch; returns the terminal
@@ -364,25 +392,16 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
             const uint4 cr = __ldg(a.t.tails + c);
             PFAC_CHECK((uint64_t)cr.x + cr.y <= a.t.n_tail_bytes && cr.z < a.t.n_terminals);
             if ((uint64_t)j + cr.y > (uint64_t)tx.end) continue;
-            const uint32_t *pw = reinterpret_cast<const uint32_t *>(a.t.tail_bytes + cr.x);
-            bool eq = true;
-            for (uint32_t k = 0; eq && k < cr.y; k += 4) {
-                const uint32_t n = cr.y - k;
-                const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
-                eq = ((tx.at4(j + k) ^ __ldg(pw + (k >> 2))) & m) == 0;
-            }
-            if (eq) return cr.z;
+            if (tx.template equal<false>(j, reinterpret_cast<const uint32_t *>(a.t.tail_bytes + cr.x), cr.y))
+                return cr.z;
         }
         return term_of(last);
     }
     if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(last);
-    const uint32_t *pw = reinterpret_cast<const uint32_t *>((hot ? s.tail_bytes : a.t.tail_bytes) + rec.x);
-    for (uint32_t k = 0; k < rec.y; k += 4) {
-        const uint32_t n = rec.y - k;
-        const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
-        const uint32_t pwk = hot ? pw[k >> 2] : __ldg(pw + (k >> 2));
-        if ((tx.at4(j + k) ^ pwk) & m) return term_of(last);
-    }
+    // (separate loops: no shared/global select per word)
+    const bool eq = hot ? tx.template equal<true>(j, reinterpret_cast<const uint32_t *>(s.tail_bytes + rec.x), rec.y)
+                        : tx.template equal<false>(j, reinterpret_cast<const uint32_t *>(a.t.tail_bytes + rec.x), rec.y);
+    if (!eq) return term_of(last);
     if (rec.z != kNone) return rec.z;  // tail
     nv = rec.w;                         // chain
     len = rec.y;
