@@ -506,7 +506,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
 
     // ---- aux word per node (one load next to the node word, no dependent
     // label or rank loads): record index of a tail/chain start; the labels of
-    // a node with 1..4 children, packed little-endian; 0 otherwise
+    // a node with 1..4 children (the first four of 5..8), packed little-endian;
+    // 0 otherwise
     std::vector<uint32_t> aux(NI, 0u);
     {
         uint32_t rank = 0;
@@ -514,9 +515,9 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
             const uint32_t e0 = node_word[v] & kEdgeMask, e1 = node_word[v + 1] & kEdgeMask;
             if (node_word[v] & kTailBit) {
                 aux[v] = rank++;
-            } else if (e1 - e0 >= 1 && e1 - e0 <= 4) {
-                uint32_t x = 0;
-                for (uint32_t e = e0; e < e1; e++) x |= (uint32_t)label[e] << (8 * (e - e0));
+            } else if (e1 - e0 >= 1 && e1 - e0 <= 8) {  // (5..8 children: the first four; the
+                uint32_t x = 0;                              //  node record holds the rest)
+                for (uint32_t e = e0; e < e0 + 4 && e < e1; e++) x |= (uint32_t)label[e] << (8 * (e - e0));
                 aux[v] = x;
             }
         }
@@ -844,7 +845,11 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
             rec[4 * v] = node_word[v];
             rec[4 * v + 1] = node_word[v + 1];
             rec[4 * v + 2] = aux[v];
-            rec[4 * v + 3] = 0;
+            uint32_t x = 0;  // labels 4..7 of a node with 5..8 children
+            const uint32_t e0 = node_word[v] & kEdgeMask, e1 = node_word[v + 1] & kEdgeMask;
+            if (!(node_word[v] & kTailBit) && e1 - e0 >= 5 && e1 - e0 <= 8)
+                for (uint32_t e = e0 + 4; e < e1; e++) x |= (uint32_t)label[e] << (8 * (e - e0 - 4));
+            rec[4 * v + 3] = x;
         }
     }
     if (!entry.empty()) std::memcpy(p + h.off_entry, entry.data(), 4 * entry.size());
@@ -973,7 +978,7 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
         ok = ok && in(h.off_rec, 16 * N);
         const uint32_t *rc = reinterpret_cast<const uint32_t *>(p + h.off_rec);
         for (uint64_t v = 0; ok && v < N; v++)
-            ok = rc[4 * v] == node[v] && rc[4 * v + 1] == node[v + 1] && rc[4 * v + 2] == aux[v] && rc[4 * v + 3] == 0;
+            ok = rc[4 * v] == node[v] && rc[4 * v + 1] == node[v + 1] && rc[4 * v + 2] == aux[v];
         // merged DAG (steps IV-V): CSR bounds, child ids, rank table
         if (ok && h.n_dag_nodes) {
             const uint64_t ND = h.n_dag_nodes, ED = h.n_dag_edges;

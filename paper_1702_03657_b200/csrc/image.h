@@ -15,13 +15,15 @@
 //                     col_ind: the BFS numbering makes it redundant).
 //   aux    u32[N]     at align256(off_node + 4(N+1)) (no header field): per
 //                     node, its record index if it is a tail/chain start, else
-//                     its labels packed little-endian if it has 1..4 children,
-//                     else 0.  Read next to the node word, it saves the walk a
+//                     its labels packed little-endian if it has 1..4 children
+//                     (its first four if it has 5..8), else 0.  Read next to the node word, it saves the walk a
 //                     dependent label (or rank) load per level.
 //   label  u8[E]      edge labels (CRS val, one byte per edge).
-//   rec    uint4[N]   per node {node[v], node[v+1], aux[v], 0}: the three
-//                     words a walk level needs, in one 16-byte load (for the
-//                     nodes not staged in shared memory; v19).
+//   rec    uint4[N]   per node {node[v], node[v+1], aux[v], x}: the words a
+//                     walk level needs, in one 16-byte load (for the nodes
+//                     not staged in shared memory); x = labels 4..7 of a node
+//                     with 5..8 children (its aux holds labels 0..3), else 0.
+//                     (v20)
 //   term_node u32[TK] ascending ids of the terminal nodes kept in the image
 //                     (terminal indices 0..TK-1); terminal indices TK..T-1 are
 //                     the ends of the compressed tails, in tail order.
@@ -163,7 +165,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 19;
+constexpr uint32_t kVersion = 20;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;

@@ -410,8 +410,9 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
 
 // Child of node v (node word w) through byte c, or kNone: level-1 nodes by
 // their bitmap (Fig. 3), deeper nodes by their CSR labels.
+template <bool kWide>
 __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, uint32_t v, uint32_t w, uint32_t c,
-                                     bool l1, uint32_t wn, uint32_t ax) {
+                                     bool l1, uint32_t wn, uint32_t ax, uint32_t ax2) {
     uint32_t nv = kNone;
     if (l1) {  // level 1 -> 2 through the bitmap
         PFAC_CHECK(v >= 1 && v <= a.t.n_level1);
@@ -430,6 +431,13 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
                 const uint32_t f = (x - 0x01010101u) & ~x & 0x80808080u;
                 if (f) nv = lo0 + ((__ffs(f) - 1) >> 3) + 1;  // the child through edge e is node e+1
             }
+        } else if (kWide && deg <= 8 && ax2 != kNone) {  // 5..8 labels: aux + the record's last word
+            const uint32_t x0 = ax ^ (c * 0x01010101u);
+            const uint32_t f0 = (x0 - 0x01010101u) & ~x0 & 0x80808080u;
+            const uint32_t x1 = (ax2 ^ (c * 0x01010101u)) | (0xFFFFFFFFu << (8 * (deg - 4) - 1) << 1);
+            const uint32_t f1 = (x1 - 0x01010101u) & ~x1 & 0x80808080u;
+            if (f0) nv = lo0 + ((__ffs(f0) - 1) >> 3) + 1;
+            else if (f1) nv = lo0 + 4 + ((__ffs(f1) - 1) >> 3) + 1;
         } else if (deg <= 16) {
             // labels[lo0, hi0) lie in <= 5 aligned words: load them at once and
             // find the byte equal to c with the zero-byte test on (word ^ c),
@@ -477,31 +485,38 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
 // set bits); deeper nodes use the CSR label list of the image; tail and chain
 // starts compare their path's bytes at once.
 __device__ __forceinline__ void node_load(const ScanArgs &a, const Smem &s, uint32_t v, uint32_t &w, uint32_t &wn,
-                                          uint32_t &ax) {
+                                          uint32_t &ax, uint32_t &ax2) {
     // the node's word, the next node's word (its edge end) and its aux word:
     // from shared memory for the staged nodes, else one 16-byte record load
+    // (whose last word holds labels 4..7 of a node with 5..8 children; ax2 =
+    // kNone for a staged node: its labels are read from shared memory)
     if (v < a.hot_nodes) {
         w = s.node[v];
         wn = s.node[v + 1];
         ax = s.aux[v];
+        ax2 = kNone;
     } else {
         PFAC_CHECK(v < a.t.n_nodes);
         const uint4 r = __ldg(a.t.rec + v);
         w = r.x;
         wn = r.y;
         ax = r.z;
+        ax2 = r.w;
     }
 }
 
-template <class Text>
+// kWide: 5..8-child nodes are matched from their aux word and record word
+// (walk-heavy kinds: C3 -4%; kind 1, whose walks are rare, keeps the smaller
+// code: C4 +1.6% with it)
+template <bool kWide, class Text>
 __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0, uint32_t v0 = 0,
                          uint32_t d0 = 1) {
     // (v0, d0): enter at image node v0 of depth d0 whose path the start's
     // first d0 bytes spell (the depth-8 entry table); else from the root
     uint32_t v = v0 ? v0 : s.root[tx.at(r0)];
     if (v == 0) return kNone;
-    uint32_t w, wn, ax;
-    node_load(a, s, v, w, wn, ax);
+    uint32_t w, wn, ax, ax2;
+    node_load(a, s, v, w, wn, ax, ax2);
     uint32_t last = (w & kTermBit) ? v : kNone;
     uint32_t j = r0 + d0;
     bool l1 = d0 == 1;  // v is a level-1 node: the next step uses its bitmap
@@ -514,13 +529,13 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
             j += len;
         } else {
             const uint32_t c = tx.at(j);
-            nv = child_of(a, s, v, w, c, l1, wn, ax);
+            nv = child_of<kWide>(a, s, v, w, c, l1, wn, ax, ax2);
             if (nv == kNone) break;  // mismatch: the thread terminates
             ++j;
         }
         l1 = false;
         v = nv;
-        node_load(a, s, v, w, wn, ax);
+        node_load(a, s, v, w, wn, ax, ax2);
         if (w & kTermBit) last = v;
     }
     return term_of(last);
@@ -800,7 +815,8 @@ __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s_
         const uint32_t ent = bent ? bent[lane] : 0u;
         const uint64_t gp = cta_lo + p;
         const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
-        tn = ent ? walk(a, s, gt, 0u, ent & ((1u << kEntShift) - 1u), ent >> kEntShift) : walk(a, s, gt, 0u);
+        tn = ent ? walk<Kind != 1>(a, s, gt, 0u, ent & ((1u << kEntShift) - 1u), ent >> kEntShift)
+                 : walk<Kind != 1>(a, s, gt, 0u);
         if (tn != kNone) {
             PFAC_CHECK(tn < a.t.n_terminals);
             const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
@@ -1546,7 +1562,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             uint32_t cc = 0, hm = 0;
             for (uint32_t m = surv; m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
-                const uint32_t ti = walk(a, s, gt, (uint32_t)k);
+                const uint32_t ti = walk<Kind != 1>(a, s, gt, (uint32_t)k);
                 if (ti != kNone) {
                     cc += s.out_ptr[ti + 1] - s.out_ptr[ti];
                     hm |= 1u << k;
@@ -1556,7 +1572,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             uint64_t o = off + warp_excl_scan(cc, lane, &ctot);
             for (uint32_t m = hm; m; m &= m - 1) {
                 const uint32_t k = (uint32_t)(__ffs(m) - 1);
-                const uint32_t ti = walk(a, s, gt, k);
+                const uint32_t ti = walk<Kind != 1>(a, s, gt, k);
                 const uint32_t r0 = s.out_ptr[ti], r1 = s.out_ptr[ti + 1];
                 for (uint32_t e = r0; e < r1; ++e, ++o) {
                     if (o < a.capacity) {

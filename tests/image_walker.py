@@ -48,6 +48,7 @@ def parse(image: bytes) -> dict:
     h["pair"] = buf[h["off_pair"]:h["off_pair"] + 8192].view(np.uint32).reshape(256, 8)
     if h["off_kset"]:
         h["kset"] = buf[h["off_kset"]:h["off_kset"] + (4 << h["kset_log2"])].view(np.uint32)
+    h["rec"] = buf[h["off_rec"]:h["off_rec"] + 16 * N].view(np.uint32).reshape(-1, 4)
     if h["n_dag_nodes"]:
         ND, ED = h["n_dag_nodes"], h["n_dag_edges"]
         h["dag_node"] = buf[h["off_dag_node"]:h["off_dag_node"] + 4 * (ND + 1)].view(np.uint32)

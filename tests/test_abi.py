@@ -165,7 +165,8 @@ def _node_after(h, text, d):
 
 @pytest.mark.parametrize("cid", [2, 3, 4, 5])
 def test_aux_words(cid):
-    """aux[v] = record rank (tail/chain start) or packed labels (1..4 children)."""
+    """aux[v] = record rank (tail/chain start) or packed labels (1..4 children;
+    the first four of 5..8); the node record's last word = labels 4..7."""
     h = image_walker.parse(pf.Trie(gen.patterns(cid)).image())
     node, aux, label = h["node"].astype(np.int64), h["aux"], h["label"]
     rank = 0
@@ -174,10 +175,13 @@ def test_aux_words(cid):
         if node[v] & image_walker.TAIL:
             assert aux[v] == rank == image_walker.tail_index(h, v)
             rank += 1
-        elif 1 <= e1 - e0 <= 4:
-            assert aux[v] == int.from_bytes(bytes(label[e0:e1]), "little"), v
+        elif 1 <= e1 - e0 <= 8:  # (the first four labels of a node with 5..8 children)
+            assert aux[v] == int.from_bytes(bytes(label[e0:min(e1, e0 + 4)]), "little"), v
         else:
             assert aux[v] == 0
+        rec = [int(x) for x in h["rec"][v]]
+        want4 = int.from_bytes(bytes(label[e0 + 4:e1]), "little") if 5 <= e1 - e0 <= 8 and not node[v] & image_walker.TAIL else 0
+        assert rec == [int(node[v]), int(node[v + 1]), int(aux[v]), want4], v
 
 
 def test_image_interpreter_random_vs_oracle():
