@@ -661,9 +661,8 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
             filter[2 * b + 1] |= 1u << (31u - (x1 & 31u));
         } else if (kind == 3) {
             const uint32_t key = dna_key(pats[k]);
-            const uint32_t b = dna_block(key, log2_bits);
-            filter[2 * b] |= (1u << dna_bit_lo(key)) | (1u << dna_bit_mid(key));
-            filter[2 * b + 1] |= 1u << dna_bit_hi(key);
+            filter[filter4_offset(key, log2_bits) / 4] |=
+                (1u << dna_bit(key, 0)) | (1u << dna_bit(key, 16)) | (1u << dna_bit(key, 26));
         } else if (kind == 2) {
             // as the first start of a pair: shared bytes are P[1..3], own byte P[0];
             // as the second start: shared bytes are P[0..2], own byte P[3]

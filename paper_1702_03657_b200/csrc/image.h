@@ -93,16 +93,14 @@
 //                         start of kind 1 at the same fill for 2 bits per key.
 //                       kind 3 (d = 16, DNA: every pattern byte in {A,C,G,T}
 //                         and the shortest pattern >= 16): a blocked three-bit
-//                         filter over the 2-bit codes of the first 16 bytes,
-//                         key = sum code(byte i) << 2i with code(b) = (b>>1)&3
-//                         (A 0, C 1, T 2, G 3; any other byte aliases, which
-//                         can only add false positives).  Block (words 2b,
-//                         2b+1) b = top (F-6) bits of key * kFilterMul; the key
-//                         sets bits 31-(key & 31) and 31-(h2 & 31) of word 2b
-//                         and bit 31-(h3 & 31) of word 2b+1, h2 =
-//                         hi32(key * kFilterMul2), h3 = hi32(key * kFilterMul3)
-//                         (~0.3% false positives at 2^20 bits for 50,000 keys,
-//                         ~1.1% with two bits).
+//                         filter in 32-bit words over the 2-bit codes of the
+//                         first 16 bytes, key = sum code(byte i) << 2i with
+//                         code(b) = (b>>1)&3 (A 0, C 1, T 2, G 3; any other
+//                         byte aliases, which can only add false positives).
+//                         Word = (hi32(key * kFilterMul) & mask) / 4 as kind 1;
+//                         bits 31-((key >> s) & 31) for s = 0, 16, 26 (bases
+//                         0-2, 8-10, 13-15: the kernel rotates by the keys of
+//                         starts k, k+8, k+13, whose low bits these are; v21).
 //   pair   u32[256][8]  the 2-gram prefix table: word (b0, q) bit j set iff
 //                     the walk from a start with bytes (b0, 32q + j) gets past
 //                     level 1, or b0's level-1 node already is a terminal or a
@@ -165,7 +163,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 20;
+constexpr uint32_t kVersion = 21;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -237,15 +235,6 @@ PFAC_HD inline uint32_t filter_pair_word(uint32_t x, uint32_t log2_bits) {
 }
 // Kind 3 (DNA): 2-bit code of a byte, key of 16 bytes, block and bit positions.
 PFAC_HD inline uint32_t dna_code(uint32_t b) { return (b >> 1) & 3u; }
-PFAC_HD inline uint32_t dna_block(uint32_t key, uint32_t log2_bits) {
-    return (key * kFilterMul) >> (32u - (log2_bits - 6u));
-}
-PFAC_HD inline uint32_t dna_bit_lo(uint32_t key) { return 31u - (key & 31u); }
-PFAC_HD inline uint32_t dna_bit_mid(uint32_t key) {
-    return 31u - (uint32_t)(((uint64_t)key * kFilterMul2) >> 32 & 31u);
-}
-PFAC_HD inline uint32_t dna_bit_hi(uint32_t key) {
-    return 31u - (uint32_t)(((uint64_t)key * kFilterMul3) >> 32 & 31u);
-}
+PFAC_HD inline uint32_t dna_bit(uint32_t key, uint32_t shift) { return 31u - ((key >> shift) & 31u); }
 
 }  // namespace pfac

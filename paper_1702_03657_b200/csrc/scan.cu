@@ -570,7 +570,8 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
         // + 15) packed into c[0..2] (byte i's code at bits 2i of the stream);
         // per word: ((w & 0x06060606) * 0x820820) >> 24 gathers the four codes
         // (b >> 1) & 3 into one byte (no carries reach bits 24..31)
-        uint32_t c[3];
+        uint32_t c[4];
+        c[3] = 0;  // (keys 32..44 need only their low bits, bytes < 48)
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             uint32_t pk[4];
@@ -582,16 +583,26 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
             }
             c[q] = pk[0] + pk[1] * 0x100u + pk[2] * 0x10000u + pk[3] * 0x1000000u;
         }
+        // keys of starts 0..kPerLane+12 (the low bits of key k+8 / k+13 are
+        // bases 8-10 / 13-15 of start k: its second and third bit positions)
+        uint32_t key[kPerLane + 14];
+#pragma unroll
+        for (int k = 0; k < kPerLane + 14; ++k)
+            key[k] = (k & 15) ? __funnelshift_r(c[k >> 4], c[(k >> 4) + 1], 2 * (k & 15)) : c[k >> 4];
+        const uint32_t mask = sWmul, t = stride;  // (the word mask and the lane's copy term, as kind 1)
         uint32_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = kPerLane - 1; k >= 0; --k) {
-            const uint32_t key = (k & 15) ? __funnelshift_r(c[k >> 4], c[(k >> 4) + 1], 2 * (k & 15)) : c[k >> 4];
-            const uint32_t blk = __umulhi(key * kFilterMul, sWmul);
-            const uint2 w2 = lds64_abs(blk * stride + base_lane);
-            const uint32_t h2 = __umulhi(key, kFilterMul2), h3 = __umulhi(key, kFilterMul3);
-            // rotate by key / h2 / h3 (funnel amounts are mod 32): tested bits -> 31
-            const uint32_t r = __funnelshift_l(w2.x, w2.x, key) & __funnelshift_l(w2.x, w2.x, h2) &
-                               __funnelshift_l(w2.y, w2.y, h3);
+            const uint32_t off = (__umulhi(key[k], kFilterMul) & mask) ^ t;
+            PFAC_CHECK(off < (a.filter_words * 4u << a.rep_log2));
+            uint32_t w;
+            if (kImm1024)
+                asm("ld.shared.u32 %0, [%1+1024];" : "=r"(w) : "r"(off));
+            else
+                asm("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(off + base_lane));
+            // rotate by the keys of starts k, k+8, k+13 (funnel amounts are mod 32): tested bits -> 31
+            const uint32_t r = __funnelshift_l(w, w, key[k]) & __funnelshift_l(w, w, key[k + 8]) &
+                               __funnelshift_l(w, w, key[k + 13]);
             acc[k >> 3] = __funnelshift_l(r, acc[k >> 3], 1);  // acc << 1 | bit
         }
         surv = acc[0] | (acc[1] << 8) | (acc[2] << 16) | (acc[3] << 24);
@@ -960,22 +971,23 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     __syncthreads();  // barriers initialised
     STAMP(11);
     const Smem s = make_smem(a);
-    // filter addressing: kinds 0, 2, 3, 4: copies interleaved at the unit
-    // the kernel loads (8-byte block b of copy r at filter + 8*(b*rep + r);
-    // word w of copy r at filter + 4*(w*rep + r)); kind 1: copy r at filter +
+    // filter addressing: kinds 0, 2, 4: copies interleaved at the unit the
+    // kernel loads (8-byte block b of copy r at filter + 8*(b*rep + r); word
+    // w of copy r at filter + 4*(w*rep + r)); kinds 1, 3: copy r at filter +
     // r * filter bytes, word w of it at position w ^ r.  Lane l reads copy
     // l % rep, so the lanes of a phase spread over the banks.
     const uint32_t rep = 1u << a.rep_log2;
-    constexpr bool kBlock64 = Kind == 3 || Kind == 4;  // 64-bit blocks
+    constexpr bool kBlock64 = Kind == 4;                // 64-bit blocks
+    constexpr bool kWordSwz = Kind == 1 || Kind == 3;   // 32-bit words, swizzled copies
     const uint32_t unit = kBlock64 ? 8u : 4u;
     const uint32_t sW = 32u - (a.t.log2_bits - (kBlock64 ? 6u : 5u));  // block index = hash >> sW
     const uint32_t lane_copy = (uint32_t)lane & (rep - 1u);
     const uint32_t fbytes = a.filter_words * 4u;
     // kind 1: (word mask, copy term) in the (sWmul, stride) slots of filter32
-    const uint32_t sWmul = Kind == 1 ? (fbytes - 1u) & ~3u : 1u << (32u - sW);  // (hash * sWmul) >> 32 == hash >> sW
-    const uint32_t stride = Kind == 1 ? (lane_copy * fbytes) | (lane_copy * 4u) : rep * unit;
-    const uint32_t base_lane = smem_u32(smem) + (Kind == 1 ? 0u : lane_copy * unit);
-    const bool imm1024 = Kind == 1 && smem_u32(smem) == 1024u;  // the filter's base fits the LDS immediate
+    const uint32_t sWmul = kWordSwz ? (fbytes - 1u) & ~3u : 1u << (32u - sW);  // (hash * sWmul) >> 32 == hash >> sW
+    const uint32_t stride = kWordSwz ? (lane_copy * fbytes) | (lane_copy * 4u) : rep * unit;
+    const uint32_t base_lane = smem_u32(smem) + (kWordSwz ? 0u : lane_copy * unit);
+    const bool imm1024 = kWordSwz && smem_u32(smem) == 1024u;  // the filter's base fits the LDS immediate
 
     const uint64_t policy = evict_first_policy();
     // starts < lim are valid: inside [0, n_starts) and their d-gram fits
@@ -1095,7 +1107,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         // (consecutive threads write consecutive units: no bank conflicts)
         // (8-16 loads in flight per thread: the image is cold in L2 here)
         const uint32_t nu = a.rep_log2 == 0 ? 0u : (kBlock64 ? a.filter_words / 2 : a.filter_words) << a.rep_log2;
-        if (Kind == 1) {  // copy r = j / words, position p = j % words holds word p ^ r
+        if (kWordSwz) {  // copy r = j / words, position p = j % words holds word p ^ r
             const uint32_t lw = (uint32_t)__ffs(a.filter_words) - 1u;
             for (uint32_t j0 = 0; j0 < nu; j0 += 16 * kThreads) {
                 uint32_t v[16];

@@ -112,13 +112,10 @@ def filter_pass(h, key, start=0):
         hh = (x0 * 0x9E3779B1 + x1 * 0x85EBCA6B) & 0xFFFFFFFF
         b = hh >> (32 - (h["filter_log2_bits"] - 6))
         return bool((int(f[2 * b]) >> (31 - (x0 & 31))) & 1) and bool((int(f[2 * b + 1]) >> (31 - (x1 & 31))) & 1)
-    if h["filter_kind"] == 3:
-        f = h["filter"]
-        b = ((key * 0x9E3779B1) & 0xFFFFFFFF) >> (32 - (h["filter_log2_bits"] - 6))
-        lo = 31 - (key & 31)
-        mid = 31 - (((key * 0x85EBCA6B) >> 32) & 31)
-        hi = 31 - (((key * 0xC2B2AE35) >> 32) & 31)
-        return bool((int(f[2 * b]) >> lo) & (int(f[2 * b]) >> mid) & (int(f[2 * b + 1]) >> hi) & 1)
+    if h["filter_kind"] == 3:  # 32-bit words as kind 1; bits from bases 0-2, 8-10, 13-15 (image.h)
+        mask = ((1 << (h["filter_log2_bits"] - 3)) - 1) & ~3
+        w = int(h["filter"][(((key * 0x9E3779B1) >> 32) & mask) // 4])
+        return all((w >> (31 - ((key >> s) & 31))) & 1 for s in (0, 16, 26))
     if h["filter_kind"] == 2:
         f = h["filter"]
         if start % 2 == 0:  # first of the pair: shared bytes 1..3, own byte 0
