@@ -310,6 +310,23 @@ def test_full_size_exact(cid, n_bytes, engine):
     assert _full_size_exact(cid, n_bytes, engine) > 0
 
 
+def test_launch_past_4gib():
+    """One launch over more than 2^32 start positions (C4 patterns on 4.25
+    GiB: the cross-CTA pool is planned only up to 2^32 starts, so this runs
+    the pool-less plan with 64-bit positions past 4 GiB), full-array exact."""
+    ps = gen.patterns(4)
+    n = (4 << 30) + (256 << 20)
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    gen.text(4, 0, n, out=host.numpy())
+    t = pf.Trie(ps)
+    assert t.plan(n)["pool_rounds"] == 0
+    pos, pid = t.match(host.to(DEV))
+    got = (pos.cpu().numpy().astype(np.uint64), pid.cpu().numpy().astype(np.uint32))
+    want = oracle.Trie(ps).match(host.numpy())
+    assert int(want[0][-1]) >= (4 << 30)  # rows past 2^32 are checked
+    assert_same(got, want, "C4 text, 4.25 GiB, one launch")
+
+
 def test_full_c5_16gib_sharded():
     """C5's whole 16 GiB text as the 8 halo'd shards of the 8-GPU layout
     (multigpu.shard_bounds / read_range; PAPER.md:66 overlap rule), each
