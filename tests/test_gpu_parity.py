@@ -505,3 +505,63 @@ def test_placement_variants_exact(cid, placement):
     if "placement" in placement and "hot_bytes_cap" not in placement:
         assert p["placement"] == pf.PLACEMENTS[placement["placement"]], p
     assert_same(gpu_rows(t, text, offset=2, **placement), want, f"C{cid} {placement}")
+
+
+# ------------------------------------- launch hygiene (ADVICE r1 fixes)
+def test_cuda_graph_replay():
+    """The scan captured once in a CUDA graph and replayed many times gives
+    the same exact rows every time: the grid barrier resets itself in device
+    memory (no host-side per-launch state baked into the graph)."""
+    ps = gen.patterns(4)
+    text = gen.text(4, 0, 8 << 20)
+    want = oracle.Trie(ps).match(text)
+    t = pf.Trie(ps)
+    d = torch.from_numpy(text.copy()).to(DEV)
+    s = torch.cuda.Stream()
+    sc = pf.Scanner(t, DEV, capacity=1 << 16)
+    with torch.cuda.stream(s):
+        sc.launch(d)  # warm-up (allocations happen outside the capture)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sc.launch(d)
+    for rep in range(6):
+        sc.count.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        n = int(sc.count.item())
+        got = (sc.pos[:n].cpu().numpy().astype(np.uint64), sc.pid[:n].cpu().numpy().astype(np.uint32))
+        assert_same(got, want, f"graph replay {rep}")
+
+
+def test_launch_on_foreign_stream():
+    """Scanner.launch(stream=s) on a stream other than the current one: the
+    workspace's allocation and zero-fill are ordered before the scan."""
+    ps = gen.patterns(2)
+    text = gen.text(2, 0, 4 << 20)
+    want = oracle.Trie(ps).match(text)
+    d = torch.from_numpy(text.copy()).to(DEV)
+    for _ in range(3):
+        sc = pf.Scanner(pf.Trie(ps), DEV, capacity=1 << 16)
+        s = torch.cuda.Stream()
+        sc.launch(d, stream=s)
+        s.synchronize()
+        n = int(sc.count.item())
+        got = (sc.pos[:n].cpu().numpy().astype(np.uint64), sc.pid[:n].cpu().numpy().astype(np.uint32))
+        assert_same(got, want, "foreign stream")
+
+
+def test_device_must_be_current():
+    """pfac_match_device refuses a `device` that is not the current device
+    (INVALID_ARG) instead of mixing contexts."""
+    import ctypes as C
+    t = pf.Trie([b"abc"])
+    d = torch.zeros(64, dtype=torch.uint8, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    pos = torch.zeros(16, dtype=torch.int64, device=DEV)
+    pid = torch.zeros(16, dtype=torch.int32, device=DEV)
+    ws = torch.zeros(t.workspace_bytes(64), dtype=torch.uint8, device=DEV)
+    st = pf._lib().pfac_match_device(t._h, 5, d.data_ptr(), 64, 64, 0, pos.data_ptr(), pid.data_ptr(), 16,
+                                     cnt.data_ptr(), ws.data_ptr(), ws.numel(), None)
+    assert st == 1
+    assert b"current" in pf._lib().pfac_last_error()
