@@ -158,9 +158,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 // (the same on 32-bit shared-window addresses: no generic->shared conversion per use)
 __device__ __forceinline__ void mbar_arrive_expect_tx_s(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
@@ -185,6 +182,38 @@ __device__ __forceinline__ void bulk_g2s_s(uint32_t dst, const void *src, uint32
             dst),
         "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// The dynamic shared memory's shared-window address: the 1 KiB the system
+// reserves per block comes first, and the scan kernel has no static shared
+// memory and no cluster (the CTA-rank bits of the window are 0).  The kernel
+// checks it at entry; its per-warp queues and ring are then addressed with
+// 32-bit constants-plus-offsets (no generic->shared conversion per access).
+constexpr uint32_t kSmemBase = 1024u;
+// Queue / ring accesses on 32-bit shared addresses.  Ordered among
+// themselves and against the warp's __syncwarp() (volatile, memory clobber).
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32q(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds8q(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 lds128q(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
@@ -701,11 +730,15 @@ __device__ __forceinline__ uint32_t filter32(const ScanArgs &a, const uint32_t w
 // The filter key of the start at slot offset off (the slot holds 16 bytes
 // past the round, so the 16 DNA bytes are always in it): kind 3 the 16-base
 // DNA key, else the first 4 bytes.
+// (slot: the slot's 32-bit shared address)
 template <int Kind>
-__device__ __forceinline__ uint32_t slot_key(const uint8_t *slot, uint32_t off) {
-    const uint32_t *w = reinterpret_cast<const uint32_t *>(slot + (off & ~3u));
+__device__ __forceinline__ uint32_t slot_key(uint32_t slot, uint32_t off) {
+    const uint32_t wa = slot + (off & ~3u);
     const uint32_t sh = 8 * (off & 3);
     if (Kind == 3) {
+        uint32_t w[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) w[q] = lds32q(wa + 4 * q);
         uint32_t key = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -714,7 +747,7 @@ __device__ __forceinline__ uint32_t slot_key(const uint8_t *slot, uint32_t off) 
         }
         return key;
     }
-    return __funnelshift_r(w[0], w[1], sh);
+    return __funnelshift_r(lds32q(wa), lds32q(wa + 4), sh);
 }
 // Probe the exact key set for a key (image.h: buckets of 4 slots, one
 // 16-byte load each): present if a slot holds the key, absent if a slot is
@@ -806,15 +839,15 @@ __device__ __forceinline__ uint32_t probe_start(const ScanArgs &a, const GlobalT
     return 0u;
 }
 
-// Walk starts bpos[0, m) (m <= 32; bent = where each walk enters) with the
-// warp, text from global memory (L2: streamed moments ago); hits are appended
+// Walk starts bpos[0, m) (m <= 32; bent = where each walk enters, 0: from
+// the root; both 32-bit shared addresses of u32 arrays) with the warp, text from global memory (L2: streamed moments ago); hits are appended
 // to the warp's hit list in the same (position) order and their pid counts
 // added to the lane's block rows or their round's count.  Returns the new hit
 // count.
 template <int Kind>
 __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s_in, uint64_t cta_lo,
-                                               uint64_t cta_round0, uint32_t ctg_bytes, const uint32_t *bpos,
-                                               const uint32_t *bent, uint32_t m, uint2 *hits, uint32_t n_hits,
+                                               uint64_t cta_round0, uint32_t ctg_bytes, uint32_t bpos,
+                                               uint32_t bent, uint32_t m, uint2 *hits, uint32_t n_hits,
                                                unsigned long long &rows) {
     const int lane = threadIdx.x & 31;
     // kind 1 builds its shared-memory views here (its walks are rare: C4
@@ -822,8 +855,8 @@ __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s_
     const Smem s = Kind == 1 ? make_smem(a) : s_in;
     uint32_t p = 0, tn = kNone;
     if ((uint32_t)lane < m) {
-        p = bpos[lane];
-        const uint32_t ent = bent ? bent[lane] : 0u;
+        p = lds32q(bpos + 4u * lane);
+        const uint32_t ent = bent ? lds32q(bent + 4u * lane) : 0u;
         const uint64_t gp = cta_lo + p;
         const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
         tn = ent ? walk<Kind != 1>(a, s, gt, 0u, ent & ((1u << kEntShift) - 1u), ent >> kEntShift)
@@ -855,12 +888,13 @@ struct FlushOut {
 // Decide the queued starts dpos[0, n) (position order; dkey = kind-1 keys).
 // Two-level kinds move the probe survivors to the walk queue (bpos, bent, nb
 // entries) and walk it whenever it holds 32; `final` also walks the rest.
+// (The queues are given by their 32-bit shared addresses.)
 // Not inlined: its registers do not weigh on the scan loop (it runs once per
 // few rounds).
 template <int Kind>
 __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t cta_lo, uint64_t cta_round0,
-                                                uint32_t ctg_bytes, const uint32_t *dpos, const uint32_t *dkey,
-                                                uint32_t n, uint32_t *bpos, uint32_t *bent, uint32_t nb, bool final,
+                                                uint32_t ctg_bytes, uint32_t dpos, uint32_t dkey,
+                                                uint32_t n, uint32_t bpos, uint32_t bent, uint32_t nb, bool final,
                                                 uint2 *hits, uint32_t n_hits) {
     const ScanArgs &a = *ap;
     const Smem s = Kind == 1 ? Smem{} : make_smem(a);  // (see walk_batch)
@@ -869,7 +903,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
     __syncwarp();
     if (!two_level<Kind>(a)) {  // direct: walk every queued start
         for (uint32_t j0 = 0; j0 < n; j0 += 32)
-            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, dpos + j0, nullptr, min(32u, n - j0), hits,
+            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, dpos + 4u * j0, 0u, min(32u, n - j0), hits,
                                       n_hits, rows);
         __syncwarp();
         return FlushOut{n_hits, 0u, (uint32_t)rows};
@@ -878,33 +912,33 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
         const uint32_t j = j0 + lane;
         uint32_t p = 0, ent = kNone;
         if (j < n) {
-            p = dpos[j];
+            p = lds32q(dpos + 4u * j);
             const uint64_t gp = cta_lo + p;
             const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
-            ent = probe_start<Kind>(a, gt, Kind == 1 ? dkey[j] : 0u);
+            ent = probe_start<Kind>(a, gt, Kind == 1 ? lds32q(dkey + 4u * j) : 0u);
         }
         const uint32_t kb = __ballot_sync(0xffffffffu, ent != kNone);
         if (ent != kNone) {
             const uint32_t idx = nb + __popc(kb & ((1u << lane) - 1u));
             PFAC_CHECK(idx < kWalkQ);
-            bpos[idx] = p;
-            if (Kind != 1) bent[idx] = ent;
+            sts32(bpos + 4u * idx, p);
+            if (Kind != 1) sts32(bent + 4u * idx, ent);
         }
         nb += __popc(kb);
         if (nb >= 32) {  // walk the first 32, keep the rest (< 32) at the front
             __syncwarp();
-            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, 32u,
+            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? 0u : bent, 32u,
                                       hits, n_hits, rows);
             uint32_t rp = 0, re = 0;
             const bool mv = (uint32_t)lane + 32u < nb;
             if (mv) {
-                rp = bpos[lane + 32];
-                if (Kind != 1) re = bent[lane + 32];
+                rp = lds32q(bpos + 4u * (lane + 32));
+                if (Kind != 1) re = lds32q(bent + 4u * (lane + 32));
             }
             __syncwarp();
             if (mv) {
-                bpos[lane] = rp;
-                if (Kind != 1) bent[lane] = re;
+                sts32(bpos + 4u * lane, rp);
+                if (Kind != 1) sts32(bent + 4u * lane, re);
             }
             nb -= 32;
             __syncwarp();
@@ -912,7 +946,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
     }
     if (final && nb) {
         __syncwarp();
-        n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? nullptr : bent, nb, hits,
+        n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? 0u : bent, nb, hits,
                                   n_hits, rows);
         nb = 0;
     }
@@ -933,9 +967,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t *s_node = reinterpret_cast<uint32_t *>(smem + a.off_node);
     uint8_t *s_label = smem + a.off_label;
     constexpr WarpLayout WL = warp_layout(Kind, kSlots);
-    uint8_t *const wsm = smem + a.off_warps + (uint32_t)warp * WL.bytes;  // this warp's region
-    uint8_t *ring = wsm + WL.ring;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(wsm + WL.bars);
+    if (smem_u32(smem) != kSmemBase) __trap();  // (see kSmemBase)
+    // this warp's region: its 32-bit shared address
+    const uint32_t wss = kSmemBase + a.off_warps + (uint32_t)warp * WL.bytes;
     unsigned long long *s_wtot = reinterpret_cast<unsigned long long *>(smem + a.off_warp);  // [kWarps + 2]
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
 
@@ -963,7 +997,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         if (nb_t) bulk_g2s(smem + a.off_tails, a.t.tails, nb_t, sbar, pl);
         if (nb_tb) bulk_g2s(smem + a.off_tbytes, a.t.tail_bytes, nb_tb, sbar, pl);
     }
-    if (lane < kSlots) mbar_init(&bars[lane], 1);
+    if (lane < kSlots)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(wss + WL.bars + 8u * lane), "r"(1) : "memory");
     uint32_t *s_next = reinterpret_cast<uint32_t *>(s_wtot + kWarps + 1);  // round counter of the CTA (phase 1;
                                                                             // then s_wtot[kWarps + 1])
     if (tid == 32) *s_next = 0u;
@@ -986,8 +1021,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // kind 1: (word mask, copy term) in the (sWmul, stride) slots of filter32
     const uint32_t sWmul = kWordSwz ? (fbytes - 1u) & ~3u : 1u << (32u - sW);  // (hash * sWmul) >> 32 == hash >> sW
     const uint32_t stride = kWordSwz ? (lane_copy * fbytes) | (lane_copy * 4u) : rep * unit;
-    const uint32_t base_lane = smem_u32(smem) + (kWordSwz ? 0u : lane_copy * unit);
-    const bool imm1024 = kWordSwz && smem_u32(smem) == 1024u;  // the filter's base fits the LDS immediate
+    const uint32_t base_lane = kSmemBase + (kWordSwz ? 0u : lane_copy * unit);
+    static_assert(kSmemBase == 1024u, "filter32's immediate");  // word kinds: the base is the LDS immediate
 
     const uint64_t policy = evict_first_policy();
     // starts < lim are valid: inside [0, n_starts) and their d-gram fits
@@ -1030,7 +1065,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         } else {
             r = 0;
             if (lane == 0) {
-                asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(s_next)) : "memory");
+                asm volatile("atom.shared.add.u32 %0, [%1], 1;"
+                             : "=r"(r)
+                             : "r"(kSmemBase + a.off_warp + 8u * (kWarps + 1))
+                             : "memory");
             }
             r = n_ctg + __shfl_sync(0xffffffffu, r, 0);
             if (r >= n_local) {  // the CTA's range is done: a pool round, if any is left
@@ -1058,14 +1096,12 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // bytes, zero-filled past `readable`, or everything when the text pointer
     // is not 16-byte aligned), all loads issued before the stores.
     auto issue = [&](uint32_t r, uint32_t slot) {
-        uint8_t *dst = ring + slot * kSlotBytes;
+        const uint32_t dst = wss + WL.ring + slot * kSlotBytes, bar = wss + WL.bars + 8u * slot;
         if (r < n_fast) {  // the whole slot is readable and aligned: one bulk copy
             if (lane == 0) {
-                const uint32_t ws = smem_u32(wsm), bar = ws + WL.bars + 8u * slot;
                 fence_proxy_async_smem();  // prior generic accesses of the slot precede the async write
                 mbar_arrive_expect_tx_s(bar, kSlotBytes);
-                bulk_g2s_s(ws + WL.ring + slot * kSlotBytes, a.text + cta_lo + (uint64_t)r * kRound, kSlotBytes, bar,
-                           policy);
+                bulk_g2s_s(dst, a.text + cta_lo + (uint64_t)r * kRound, kSlotBytes, bar, policy);
             }
             return;
         }
@@ -1084,7 +1120,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const uint32_t o = o0 + lane + 32 * q;
-                    if (o < (uint32_t)kSlotBytes) dst[o] = (uint8_t)v[q];
+                    if (o < (uint32_t)kSlotBytes)
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + o), "r"(v[q]) : "memory");
                 }
             }
             __syncwarp();
@@ -1092,10 +1129,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         if (lane == 0) {
             if (nbulk) {
                 fence_proxy_async_smem();  // prior generic accesses of the slot precede the async write
-                mbar_arrive_expect_tx(&bars[slot], nbulk);
-                bulk_g2s(dst, a.text + lo, nbulk, &bars[slot], policy);
+                mbar_arrive_expect_tx_s(bar, nbulk);
+                bulk_g2s_s(dst, a.text + lo, nbulk, bar, policy);
             } else {
-                mbar_arrive(&bars[slot]);
+                mbar_arrive_s(bar);
             }
         }
     };
@@ -1192,37 +1229,35 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t dcount = 0;  // queued starts (warp-uniform)
     uint32_t nb = 0;      // walk-queue entries (two-level kinds; warp-uniform)
     constexpr uint32_t qcap = defer_cap(Kind);  // queue capacity
-    uint32_t *dpos = reinterpret_cast<uint32_t *>(wsm + WL.dpos);
-    uint32_t *dkey = reinterpret_cast<uint32_t *>(wsm + WL.dkey);  // kind 1
-    // walk queue: positions (+ entry words, kinds 3/4)
-    uint32_t *bpos = reinterpret_cast<uint32_t *>(wsm + WL.bpos);
-    uint32_t *bent = reinterpret_cast<uint32_t *>(wsm + WL.bent);
+    // (32-bit shared addresses of the queues)
+    const uint32_t dpos = wss + WL.dpos, dkey = wss + WL.dkey;  // probe queue (+ kind-1 keys)
+    const uint32_t bpos = wss + WL.bpos, bent = wss + WL.bent;  // walk queue: positions (+ entry words, kinds 3/4)
     uint32_t slot = 0, phase = 0;  // ring slot of the current round, its mbarrier parity
     for (;;) {
         const bool done = rid[0] == kNoRound;
         const uint32_t rel = rid[0] * (uint32_t)kRound;  // round start relative to cta_lo
         const uint64_t rbase = cta_lo + rel;
-        const uint8_t *p0 = ring + slot * kSlotBytes;
+        const uint32_t p0 = wss + WL.ring + slot * kSlotBytes;  // the round's slot
         uint32_t pending = 0;
         if (!done) {
             // refill the slot of the previous round with the next round taken
             __syncwarp();  // every lane's reads of that slot precede its refill
             rid[kSlots - 1] = take();
             if (rid[kSlots - 1] != kNoRound) issue(rid[kSlots - 1], slot == 0 ? kSlots - 1 : slot - 1);
-            mbar_wait_s(smem_u32(wsm) + WL.bars + 8u * slot, phase);
+            mbar_wait_s(wss + WL.bars + 8u * slot, phase);
 #ifdef PFAC_TIMING
             if (taken == kSlots) STAMP(6);  // the first round's text is in
 #endif
 #ifdef PFAC_STREAM_ONLY
-            if (p0[lane] == 0xFF && a.pos_base == ~0ull) n_hits++;  // keeps the loads
+            if (lds8q(p0 + lane) == 0xFF && a.pos_base == ~0ull) n_hits++;  // keeps the loads
 #else
             // ---- stage 1: filter over the lane's 32 starts (its 32 bytes: two
             // 16-byte loads; the 2-way bank conflict of the 32-byte stride costs
             // less than un-swizzling in registers)
             uint32_t wv[kWv];
             {
-                const uint4 h0 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane);
-                const uint4 h1 = *reinterpret_cast<const uint4 *>(p0 + lane * kPerLane + 16);
+                const uint4 h0 = lds128q(p0 + lane * kPerLane);
+                const uint4 h1 = lds128q(p0 + lane * kPerLane + 16);
                 wv[0] = h0.x;
                 wv[1] = h0.y;
                 wv[2] = h0.z;
@@ -1233,17 +1268,16 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 wv[7] = h1.w;
             }
             const uint32_t w8 = __shfl_down_sync(0xffffffffu, wv[0], 1);
-            wv[kWv - 1] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound) : w8;
+            wv[kWv - 1] = lane == 31 ? lds32q(p0 + kRound) : w8;
             uint32_t ext[3] = {0, 0, 0};  // kind 3: the next 12 bytes (the slot holds 16 past the round)
             if (Kind == 3 || Kind == 4) {
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const uint32_t e = __shfl_down_sync(0xffffffffu, wv[q + 1], 1);
-                    ext[q] = lane == 31 ? *reinterpret_cast<const uint32_t *>(p0 + kRound + 4 + 4 * q) : e;
+                    ext[q] = lane == 31 ? lds32q(p0 + kRound + 4 + 4 * q) : e;
                 }
             }
-            pending = imm1024 ? filter32<Kind, true>(a, wv, ext, sW, sWmul, stride, base_lane)
-                              : filter32<Kind, false>(a, wv, ext, sW, sWmul, stride, base_lane);
+            pending = filter32<Kind, kWordSwz>(a, wv, ext, sW, sWmul, stride, base_lane);
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
@@ -1263,10 +1297,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 for (uint32_t m = pending; m; m &= m - 1) {
                     const uint32_t k = __ffs(m) - 1;
                     const uint32_t off = lane * kPerLane + k;
-                    const uint32_t b0 = p0[off];
+                    const uint32_t b0 = lds8q(p0 + off);
                     uint32_t keep;
                     if (off + 1 < rl) {
-                        const uint32_t b1 = p0[off + 1];  // the slot holds 16 bytes past the round
+                        const uint32_t b1 = lds8q(p0 + off + 1);  // the slot holds 16 bytes past the round
                         keep = (s_pair[b0 * 8 + (b1 >> 5)] >> (b1 & 31)) & 1u;
                     } else {
                         keep = s.root[b0] != 0u;  // last readable byte: let the walk decide
@@ -1299,14 +1333,14 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     uint32_t e = dcount + ex;
                     for (uint32_t m = pending; m; m &= m - 1, ++e) {
                         PFAC_CHECK(e < qcap);
-                        dpos[e] = rel + lane * kPerLane + (__ffs(m) - 1);
+                        sts32(dpos + 4u * e, rel + lane * kPerLane + (__ffs(m) - 1));
                     }
                     if (Kind == 1 && a.use_kset) {
                         // the keys of the new entries, one per lane (the per-lane loop
                         // above only scatters offsets: it runs max-over-lanes times)
                         __syncwarp();
                         for (uint32_t j = dcount + (uint32_t)lane; j < dcount + tot; j += 32)
-                            dkey[j] = slot_key<Kind>(p0, dpos[j] - rel);
+                            sts32(dkey + 4u * j, slot_key<Kind>(p0, lds32q(dpos + 4u * j) - rel));
                     }
                     dcount += tot;
                     __syncwarp();
@@ -1316,8 +1350,8 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                         for (uint32_t m = pending; m; m &= m - 1, ++e) {
                             if (e >= c0 && e < c0 + qcap) {
                                 const uint32_t off = lane * kPerLane + (__ffs(m) - 1);
-                                dpos[e - c0] = rel + off;
-                                if (Kind == 1 && a.use_kset) dkey[e - c0] = slot_key<Kind>(p0, off);
+                                sts32(dpos + 4u * (e - c0), rel + off);
+                                if (Kind == 1 && a.use_kset) sts32(dkey + 4u * (e - c0), slot_key<Kind>(p0, off));
                             }
                         }
                         const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey,
@@ -1331,7 +1365,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             }
         } else if (dcount != 0 || nb != 0) {  // the warp's rounds are done: decide everything left
 #if defined(PFAC_EXP) && PFAC_EXP == 2
-            if (dpos[0] == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
+            if (lds32q(dpos) == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
             const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey, dcount, bpos,
                                                      bent, nb, true, hits, n_hits);
@@ -1565,7 +1599,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     if (lbase + 4 * q + b < a.readable) x |= (uint32_t)__ldg(a.text + lbase + 4 * q + b) << (8 * b);
                 if (q < kWv) wv[q] = x; else ext[q - kWv] = x;
             }
-            uint32_t surv = filter32<Kind, false>(a, wv, ext, sW, sWmul, stride, base_lane);
+            uint32_t surv = filter32<Kind, kWordSwz>(a, wv, ext, sW, sWmul, stride, base_lane);
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
                 surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
