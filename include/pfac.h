@@ -116,8 +116,14 @@ typedef enum {
     PFAC_PLACE_AUTO = 0,    /* planner's choice (below) */
     PFAC_PLACE_GLOBAL = 1,  /* no trie level staged: root table + level-1 bitmaps only, the rest via L1/L2 */
     PFAC_PLACE_SMEM = 2,    /* the whole trie, else its BFS prefix (upper levels), in shared memory */
-    PFAC_PLACE_BIG_L1 = 3   /* no trie level staged, 2-slot text ring, one filter copy: the
+    PFAC_PLACE_BIG_L1 = 3,  /* no trie level staged, 2-slot text ring, one filter copy: the
                                largest L1 carve-out for the nodes the walks visit */
+    PFAC_PLACE_CLUSTER = 4  /* thread-block clusters of pfac_plan_options.cluster CTAs: the node
+                               records of the trie's BFS prefix are spread over the cluster's shared
+                               memories (CTA q holds a power-of-two slice) and walks read them through
+                               distributed shared memory (ld.shared::cluster); 2-slot ring, one filter
+                               copy.  Filter kinds 1, 3 and 4 (the tries larger than one SM's shared
+                               memory); LIMIT for the others.  The grid is the co-resident clusters. */
 } pfac_placement;
 
 /* Scan-plan options (pfac_match_device_ex, pfac_plan_query).  NULL = the
@@ -138,7 +144,8 @@ typedef struct {
                                      window for this launch (sets the device's persisting-L2 limit
                                      to min(image, 64 MiB) on first use) */
     uint32_t form;                /* pfac_form (PFAC_FORM_MERGED_DAG needs a trie built with merge_suffixes) */
-    uint32_t reserved[5];         /* must be 0 */
+    uint32_t cluster;             /* CTAs per cluster for PFAC_PLACE_CLUSTER: 2, 4 or 8 (0: 2) */
+    uint32_t reserved[4];         /* must be 0 */
 } pfac_plan_options;
 
 /* Fill *o with the defaults (struct_bytes set, every choice automatic). */
@@ -152,6 +159,8 @@ typedef struct {
     uint32_t grid, warps_per_cta, hit_cap, stage2;
     uint32_t entry, kset, pool_rounds, placement;
     uint64_t rounds_per_cta, main_rounds;
+    uint32_t cluster;    /* CTAs per cluster (1: no cluster) */
+    uint32_t dsm_nodes;  /* nodes [0, dsm_nodes) read from the cluster's shared memories (PFAC_PLACE_CLUSTER) */
 } pfac_plan_info;
 
 /* Host-side result of pfac_match: library-allocated, free with pfac_matches_free.

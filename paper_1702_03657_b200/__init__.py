@@ -62,17 +62,18 @@ class PlanOptions(C.Structure):
     _fields_ = [("struct_bytes", C.c_uint32), ("placement", C.c_uint32), ("hot_bytes_cap", C.c_uint32),
                 ("max_filter_rep_log2", C.c_int32), ("ring_slots", C.c_int32), ("ctg64", C.c_int32),
                 ("pool64", C.c_int32), ("stage2", C.c_int32), ("entry", C.c_int32), ("l2_persist", C.c_uint32),
-                ("form", C.c_uint32), ("reserved", C.c_uint32 * 5)]
+                ("form", C.c_uint32), ("cluster", C.c_uint32), ("reserved", C.c_uint32 * 4)]
 
 
 class _PlanInfo(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "filter_kind", "ring_slots", "filter_copies", "smem_bytes", "hot_nodes", "image_nodes", "hot_edges",
         "terms_in_smem", "grid", "warps_per_cta", "hit_cap", "stage2", "entry", "kset", "pool_rounds",
-        "placement")] + [("rounds_per_cta", C.c_uint64), ("main_rounds", C.c_uint64)]
+        "placement")] + [("rounds_per_cta", C.c_uint64), ("main_rounds", C.c_uint64), ("cluster", C.c_uint32),
+                         ("dsm_nodes", C.c_uint32)]
 
 
-PLACEMENTS = {"auto": 0, "global": 1, "smem": 2, "big_l1": 3}
+PLACEMENTS = {"auto": 0, "global": 1, "smem": 2, "big_l1": 3, "cluster": 4}
 
 
 def build_options(**kw) -> BuildOptions:

@@ -144,6 +144,10 @@ struct ScanArgs {
                                     // (the rest, the range's end, is handed out dynamically)
     uint32_t use_pair;              // the 2-gram prefix table is staged and tested
     uint32_t use_entry;            // kind 4: walks enter through the depth-8 entry table
+    // cluster placement (PFAC_PLACE_CLUSTER): node records [0, dsm_nodes) in
+    // the cluster's shared memories, CTA rank q holding [q << dsm_log2,
+    // (q + 1) << dsm_log2) at off_dsm (0 = no cluster tier)
+    uint32_t dsm_nodes, dsm_log2, off_dsm;
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -513,6 +517,7 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
 // Fig. 3: 256-bit child bitmap + offset, child = offset + rank of c among the
 // set bits); deeper nodes use the CSR label list of the image; tail and chain
 // starts compare their path's bytes at once.
+template <bool kDsm>
 __device__ __forceinline__ void node_load(const ScanArgs &a, const Smem &s, uint32_t v, uint32_t &w, uint32_t &wn,
                                           uint32_t &ax, uint32_t &ax2) {
     // the node's word, the next node's word (its edge end) and its aux word:
@@ -524,6 +529,14 @@ __device__ __forceinline__ void node_load(const ScanArgs &a, const Smem &s, uint
         wn = s.node[v + 1];
         ax = s.aux[v];
         ax2 = kNone;
+    } else if (kDsm && v < a.dsm_nodes) {  // cluster placement: the record from its owner CTA's shared memory
+        extern __shared__ __align__(128) uint8_t smem_base[];
+        const uint32_t la = smem_u32(smem_base) + a.off_dsm + 16u * (v & ((1u << a.dsm_log2) - 1u));
+        uint32_t ra;
+        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(v >> a.dsm_log2));
+        asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w), "=r"(wn), "=r"(ax), "=r"(ax2)
+                     : "r"(ra));
     } else {
         PFAC_CHECK(v < a.t.n_nodes);
         const uint4 r = __ldg(a.t.rec + v);
@@ -537,7 +550,8 @@ __device__ __forceinline__ void node_load(const ScanArgs &a, const Smem &s, uint
 // kWide: 5..8-child nodes are matched from their aux word and record word
 // (walk-heavy kinds: C3 -4%; kind 1, whose walks are rare, keeps the smaller
 // code: C4 +1.6% with it)
-template <bool kWide, class Text>
+// kDsm: the cluster kernels (node records of the cluster tier via DSMEM)
+template <bool kWide, bool kDsm, class Text>
 __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint32_t r0, uint32_t v0 = 0,
                          uint32_t d0 = 1) {
     // (v0, d0): enter at image node v0 of depth d0 whose path the start's
@@ -545,7 +559,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
     uint32_t v = v0 ? v0 : s.root[tx.at(r0)];
     if (v == 0) return kNone;
     uint32_t w, wn, ax, ax2;
-    node_load(a, s, v, w, wn, ax, ax2);
+    node_load<kDsm>(a, s, v, w, wn, ax, ax2);
     uint32_t last = (w & kTermBit) ? v : kNone;
     uint32_t j = r0 + d0;
     bool l1 = d0 == 1;  // v is a level-1 node: the next step uses its bitmap
@@ -564,7 +578,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
         }
         l1 = false;
         v = nv;
-        node_load(a, s, v, w, wn, ax, ax2);
+        node_load<kDsm>(a, s, v, w, wn, ax, ax2);
         if (w & kTermBit) last = v;
     }
     return term_of(last);
@@ -844,7 +858,7 @@ __device__ __forceinline__ uint32_t probe_start(const ScanArgs &a, const GlobalT
 // to the warp's hit list in the same (position) order and their pid counts
 // added to the lane's block rows or their round's count.  Returns the new hit
 // count.
-template <int Kind>
+template <int Kind, bool kCl>
 __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s_in, uint64_t cta_lo,
                                                uint64_t cta_round0, uint32_t ctg_bytes, uint32_t bpos,
                                                uint32_t bent, uint32_t m, uint2 *hits, uint32_t n_hits,
@@ -859,8 +873,8 @@ __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s_
         const uint32_t ent = bent ? lds32q(bent + 4u * lane) : 0u;
         const uint64_t gp = cta_lo + p;
         const GlobalText gt{a.text + gp, clamp32(a.readable - gp), a.aligned};
-        tn = ent ? walk<Kind != 1>(a, s, gt, 0u, ent & ((1u << kEntShift) - 1u), ent >> kEntShift)
-                 : walk<Kind != 1>(a, s, gt, 0u);
+        tn = ent ? walk<Kind != 1, kCl>(a, s, gt, 0u, ent & ((1u << kEntShift) - 1u), ent >> kEntShift)
+                 : walk<Kind != 1, kCl>(a, s, gt, 0u);
         if (tn != kNone) {
             PFAC_CHECK(tn < a.t.n_terminals);
             const uint32_t cnt = s.out_ptr[tn + 1] - s.out_ptr[tn];
@@ -891,7 +905,7 @@ struct FlushOut {
 // (The queues are given by their 32-bit shared addresses.)
 // Not inlined: its registers do not weigh on the scan loop (it runs once per
 // few rounds).
-template <int Kind>
+template <int Kind, bool kCl>
 __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t cta_lo, uint64_t cta_round0,
                                                 uint32_t ctg_bytes, uint32_t dpos, uint32_t dkey,
                                                 uint32_t n, uint32_t bpos, uint32_t bent, uint32_t nb, bool final,
@@ -903,7 +917,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
     __syncwarp();
     if (!two_level<Kind>(a)) {  // direct: walk every queued start
         for (uint32_t j0 = 0; j0 < n; j0 += 32)
-            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, dpos + 4u * j0, 0u, min(32u, n - j0), hits,
+            n_hits = walk_batch<Kind, kCl>(a, s, cta_lo, cta_round0, ctg_bytes, dpos + 4u * j0, 0u, min(32u, n - j0), hits,
                                       n_hits, rows);
         __syncwarp();
         return FlushOut{n_hits, 0u, (uint32_t)rows};
@@ -927,7 +941,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
         nb += __popc(kb);
         if (nb >= 32) {  // walk the first 32, keep the rest (< 32) at the front
             __syncwarp();
-            n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? 0u : bent, 32u,
+            n_hits = walk_batch<Kind, kCl>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? 0u : bent, 32u,
                                       hits, n_hits, rows);
             uint32_t rp = 0, re = 0;
             const bool mv = (uint32_t)lane + 32u < nb;
@@ -946,7 +960,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
     }
     if (final && nb) {
         __syncwarp();
-        n_hits = walk_batch<Kind>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? 0u : bent, nb, hits,
+        n_hits = walk_batch<Kind, kCl>(a, s, cta_lo, cta_round0, ctg_bytes, bpos, Kind == 1 ? 0u : bent, nb, hits,
                                   n_hits, rows);
         nb = 0;
     }
@@ -954,7 +968,13 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
     return FlushOut{n_hits, nb, (uint32_t)rows};
 }
 
-template <int Kind, int kSlots>
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// kCl: launched in thread-block clusters (PFAC_PLACE_CLUSTER): the shared
+// window address carries the CTA's rank bits, so it is read, not assumed
+template <int Kind, int kSlots, bool kCl = false>
 __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a) {
     // the shared round pool (cross-CTA balance) is planned only for kinds
     // whose tries may live outside shared memory; the pair-filter kernel
@@ -967,9 +987,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint32_t *s_node = reinterpret_cast<uint32_t *>(smem + a.off_node);
     uint8_t *s_label = smem + a.off_label;
     constexpr WarpLayout WL = warp_layout(Kind, kSlots);
-    if (smem_u32(smem) != kSmemBase) __trap();  // (see kSmemBase)
+    if (!kCl && smem_u32(smem) != kSmemBase) __trap();  // (see kSmemBase)
+    const uint32_t sb = kCl ? smem_u32(smem) : kSmemBase;
     // this warp's region: its 32-bit shared address
-    const uint32_t wss = kSmemBase + a.off_warps + (uint32_t)warp * WL.bytes;
+    const uint32_t wss = sb + a.off_warps + (uint32_t)warp * WL.bytes;
     unsigned long long *s_wtot = reinterpret_cast<unsigned long long *>(smem + a.off_warp);  // [kWarps + 2]
     uint32_t *s_bm = reinterpret_cast<uint32_t *>(smem + a.off_bm);
 
@@ -986,7 +1007,16 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         const uint32_t nb_t = 16 * a.hot_tails, nb_tb = align16(a.hot_tail_bytes);
         const uint32_t nb_f = a.rep_log2 == 0 ? align16(4 * a.filter_words) : 0u;  // one copy: a bulk copy too
         const uint32_t nb_pair = a.use_pair ? 8192u : 0u;
-        mbar_arrive_expect_tx(sbar, 1024 + nb_pair + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb + nb_f);
+        // cluster placement: this CTA's slice of the node records
+        uint32_t nb_dsm = 0, dsm0 = 0;
+        if (kCl && a.dsm_nodes) {
+            uint32_t q;
+            asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(q));
+            dsm0 = q << a.dsm_log2;
+            nb_dsm = dsm0 < a.dsm_nodes ? 16u * min(1u << a.dsm_log2, a.dsm_nodes - dsm0) : 0u;
+        }
+        mbar_arrive_expect_tx(sbar, 1024 + nb_pair + 2 * nb_node + nb_label + nb_l1 + nb_t + nb_tb + nb_f + nb_dsm);
+        if (nb_dsm) bulk_g2s(smem + a.off_dsm, a.t.rec + dsm0, nb_dsm, sbar, pl);
         if (nb_pair) bulk_g2s(smem + a.off_pair, a.t.pair, nb_pair, sbar, pl);
         if (nb_f) bulk_g2s(s_filter, a.t.filter, nb_f, sbar, pl);
         bulk_g2s(s_root, a.t.root, 1024, sbar, pl);
@@ -1021,7 +1051,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // kind 1: (word mask, copy term) in the (sWmul, stride) slots of filter32
     const uint32_t sWmul = kWordSwz ? (fbytes - 1u) & ~3u : 1u << (32u - sW);  // (hash * sWmul) >> 32 == hash >> sW
     const uint32_t stride = kWordSwz ? (lane_copy * fbytes) | (lane_copy * 4u) : rep * unit;
-    const uint32_t base_lane = kSmemBase + (kWordSwz ? 0u : lane_copy * unit);
+    const uint32_t base_lane = sb + (kWordSwz ? 0u : lane_copy * unit);
     static_assert(kSmemBase == 1024u, "filter32's immediate");  // word kinds: the base is the LDS immediate
 
     const uint64_t policy = evict_first_policy();
@@ -1067,7 +1097,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             if (lane == 0) {
                 asm volatile("atom.shared.add.u32 %0, [%1], 1;"
                              : "=r"(r)
-                             : "r"(kSmemBase + a.off_warp + 8u * (kWarps + 1))
+                             : "r"(sb + a.off_warp + 8u * (kWarps + 1))
                              : "memory");
             }
             r = n_ctg + __shfl_sync(0xffffffffu, r, 0);
@@ -1208,6 +1238,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     mbar_wait(sbar, 0);
     STAMP(5);
     __syncthreads();
+    if (kCl) cluster_sync_all();  // every CTA's record slice is resident before the first remote read
     // 2-gram prefix table: word (b0, q) bit j <=> the walk from a start with
     // bytes (b0, 32q + j) gets past level 1 (or b0's node already is a
     // terminal / tail start, where every b1 is kept)
@@ -1277,7 +1308,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     ext[q] = lane == 31 ? lds32q(p0 + kRound + 4 + 4 * q) : e;
                 }
             }
-            pending = filter32<Kind, kWordSwz>(a, wv, ext, sW, sWmul, stride, base_lane);
+            pending = filter32<Kind, kWordSwz && !kCl>(a, wv, ext, sW, sWmul, stride, base_lane);
             const uint64_t lbase = rbase + (uint64_t)lane * kPerLane;
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
@@ -1322,7 +1353,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             }
             if (tot) {
                 if (dcount + tot > qcap) {  // decide the queued starts first
-                    const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey,
+                    const FlushOut fo = flush_deferred<Kind, kCl>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey,
                                                              dcount, bpos, bent, nb, false, hits, n_hits);
                     n_hits = fo.n_hits;
                     nb = fo.nb;
@@ -1354,7 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                                 if (Kind == 1 && a.use_kset) sts32(dkey + 4u * (e - c0), slot_key<Kind>(p0, off));
                             }
                         }
-                        const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey,
+                        const FlushOut fo = flush_deferred<Kind, kCl>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey,
                                                                  min(qcap, tot - c0), bpos, bent, nb, false, hits,
                                                                  n_hits);
                         n_hits = fo.n_hits;
@@ -1367,7 +1398,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 #if defined(PFAC_EXP) && PFAC_EXP == 2
             if (lds32q(dpos) == 0xFFFFFFFFu && a.pos_base == ~0ull) n_hits++;  // experiment: no walks
 #else
-            const FlushOut fo = flush_deferred<Kind>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey, dcount, bpos,
+            const FlushOut fo = flush_deferred<Kind, kCl>(&a, cta_lo, cta_round0, n_ctg * kRound, dpos, dkey, dcount, bpos,
                                                      bent, nb, true, hits, n_hits);
             n_hits = fo.n_hits;
             nb = fo.nb;
@@ -1599,7 +1630,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     if (lbase + 4 * q + b < a.readable) x |= (uint32_t)__ldg(a.text + lbase + 4 * q + b) << (8 * b);
                 if (q < kWv) wv[q] = x; else ext[q - kWv] = x;
             }
-            uint32_t surv = filter32<Kind, kWordSwz>(a, wv, ext, sW, sWmul, stride, base_lane);
+            uint32_t surv = filter32<Kind, kWordSwz && !kCl>(a, wv, ext, sW, sWmul, stride, base_lane);
             if (lbase + kPerLane > lim) {
                 const uint32_t nvalid = lbase >= lim ? 0u : (uint32_t)(lim - lbase);
                 surv &= nvalid >= 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
@@ -1608,7 +1639,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             uint32_t cc = 0, hm = 0;
             for (uint32_t m = surv; m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
-                const uint32_t ti = walk<Kind != 1>(a, s, gt, (uint32_t)k);
+                const uint32_t ti = walk<Kind != 1, kCl>(a, s, gt, (uint32_t)k);
                 if (ti != kNone) {
                     cc += s.out_ptr[ti + 1] - s.out_ptr[ti];
                     hm |= 1u << k;
@@ -1618,7 +1649,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             uint64_t o = off + warp_excl_scan(cc, lane, &ctot);
             for (uint32_t m = hm; m; m &= m - 1) {
                 const uint32_t k = (uint32_t)(__ffs(m) - 1);
-                const uint32_t ti = walk<Kind != 1>(a, s, gt, k);
+                const uint32_t ti = walk<Kind != 1, kCl>(a, s, gt, k);
                 const uint32_t r0 = s.out_ptr[ti], r1 = s.out_ptr[ti + 1];
                 for (uint32_t e = r0; e < r1; ++e, ++o) {
                     if (o < a.capacity) {
@@ -1630,12 +1661,19 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             contig_off += ctot;
         }
     }
+    if (kCl) cluster_sync_all();  // no CTA leaves while the others may still read its slice
     STAMP(4);
 }
 
 // Kernel instance for a filter kind and ring depth (2 slots only where the
 // filter can exceed 64 KiB: kinds 1 and 3).
-const void *kernel_for(uint32_t kind, uint32_t slots) {
+const void *kernel_for(uint32_t kind, uint32_t slots, bool cluster = false) {
+    if (cluster)  // (2-slot ring; the kinds whose tries outgrow one SM)
+        return slots != 2    ? nullptr
+               : kind == 1 ? (const void *)pfac_scan_kernel<1, 2, true>
+               : kind == 3 ? (const void *)pfac_scan_kernel<3, 2, true>
+               : kind == 4 ? (const void *)pfac_scan_kernel<4, 2, true>
+                           : nullptr;
     if (slots == 2)
         return kind == 1   ? (const void *)pfac_scan_kernel<1, 2>
                : kind == 2 ? (const void *)pfac_scan_kernel<2, 2>
@@ -1675,8 +1713,10 @@ int device_info(int device, DeviceInfo &out, std::string &err) {
             e = cudaDeviceGetAttribute(&di.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         for (uint32_t kind = 0; kind < 5 && e == cudaSuccess; ++kind)
             for (uint32_t slots = 2; slots <= 3 && e == cudaSuccess; ++slots)
-                if (const void *fn = kernel_for(kind, slots))
-                    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, di.max_smem_optin);
+                for (int cl = 0; cl < 2 && e == cudaSuccess; ++cl)
+                    if (const void *fn = kernel_for(kind, slots, cl != 0))
+                        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 di.max_smem_optin);
         if (e != cudaSuccess) {
             err = std::string("device query: ") + cudaGetErrorString(e);
             return kStatusCuda;
@@ -1714,7 +1754,9 @@ Geometry geometry(uint64_t n_starts, int sms) {
     g.hit_cap = (uint32_t)cap;
     g.off_owner = kWsFixed + 8 * g.n_rounds;
     g.off_hits = g.off_owner + ((4 * g.n_rounds + 15) & ~15ull);
-    g.ws_bytes = g.off_hits + 8ull * g.warps * g.hit_cap;
+    // hit lists for the grid rounded up to 8 CTAs (a cluster plan's grid, a
+    // multiple of its cluster size <= 8, may exceed a tiny scan's grid)
+    g.ws_bytes = g.off_hits + 8ull * ((g.grid + 7) & ~7ull) * kWarps * g.hit_cap;
     return g;
 }
 
@@ -1722,13 +1764,15 @@ Geometry geometry(uint64_t n_starts, int sms) {
 struct Plan {
     ScanArgs a;  // layout and policy fields (the per-call pointers are set by launch_scan)
     uint32_t slots;
+    uint32_t cluster;  // CTAs per cluster (1: a plain cooperative launch)
     size_t smem;
     Geometry geo;
     pfac_plan_info info;
 };
 
 int check_plan_options(const pfac_plan_options &o, std::string &err) {
-    bool ok = o.struct_bytes >= sizeof(pfac_plan_options) && o.placement <= PFAC_PLACE_BIG_L1 &&
+    bool ok = o.struct_bytes >= sizeof(pfac_plan_options) && o.placement <= PFAC_PLACE_CLUSTER &&
+              (o.cluster == 0 || o.cluster == 2 || o.cluster == 4 || o.cluster == 8) &&
               o.max_filter_rep_log2 >= -1 && o.max_filter_rep_log2 <= 5 &&
               (o.ring_slots == -1 || o.ring_slots == 2 || o.ring_slots == 3) && o.ctg64 >= -1 && o.ctg64 <= 64 &&
               o.pool64 >= -1 && o.pool64 <= 32 && o.stage2 >= -1 && o.stage2 <= 1 && o.entry >= -1 &&
@@ -1747,6 +1791,40 @@ int check_plan_options(const pfac_plan_options &o, std::string &err) {
 int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di, uint64_t n_starts,
               const pfac_plan_options &o, Plan &p, std::string &err) {
     p.geo = geometry(n_starts, di.sms);
+    const bool cl = o.placement == PFAC_PLACE_CLUSTER;
+    const uint32_t csize = cl ? (o.cluster ? o.cluster : 2u) : 1u;
+    if (cl) {
+        // the kinds whose tries outgrow one SM's shared memory; the grid is
+        // the co-resident clusters (cooperative: every CTA resident)
+        const void *fn = kernel_for(t.kind, 2, true);
+        if (!fn) {
+            err = "pfac scan plan: cluster placement is for filter kinds 1, 3 and 4";
+            return kStatusLimit;
+        }
+        cudaLaunchConfig_t qc = {};
+        qc.gridDim = dim3(csize);
+        qc.blockDim = dim3(kThreads);
+        qc.dynamicSmemBytes = (size_t)di.max_smem_optin;  // (one CTA per SM at any plan size)
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = csize;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int nc = 0;
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, fn, &qc);
+        if (e != cudaSuccess || nc < 1) {
+            err = std::string("pfac scan plan: no co-resident cluster of this size: ") + cudaGetErrorString(e);
+            return kStatusLimit;
+        }
+        uint64_t g = std::min<uint64_t>((uint64_t)nc * csize, (uint64_t)di.sms) / csize * csize;
+        g = std::min<uint64_t>(g, (p.geo.grid + csize - 1) / csize * csize);  // (<= the workspace's 8-CTA rounding)
+        if (g < csize) g = csize;
+        p.geo.grid = g;
+        p.geo.warps = g * kWarps;
+        p.geo.rounds_per_cta = std::max<uint64_t>(1, (p.geo.n_rounds + g - 1) / g);
+    }
     const Geometry &geo = p.geo;
     ScanArgs &a = p.a;
     std::memset(&a, 0, sizeof a);
@@ -1778,7 +1856,7 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     const uint64_t whole = hot_bytes(t.n_nodes - 1);
     bool big_l1 = (t.kind == 1 || t.kind == 3 || t.kind == 4) && whole > kSmallTrie && whole <= kBigL1Trie;
     if (o.placement == PFAC_PLACE_BIG_L1) big_l1 = true;
-    if (o.placement == PFAC_PLACE_GLOBAL || o.placement == PFAC_PLACE_SMEM) big_l1 = false;
+    if (o.placement == PFAC_PLACE_GLOBAL || o.placement == PFAC_PLACE_SMEM || cl) big_l1 = false;
     // the 2-gram test (and its 8 KiB table): not for DNA (the kernel has no
     // stage 2 for kind 3), and by default only where it is selective: at most
     // a quarter of all 2-grams begin a pattern path (C2 1.5%, C3 5.8%; C4's
@@ -1791,6 +1869,7 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     const bool use_pair = t.kind != 3 && (o.stage2 == 1 || (o.stage2 == -1 && pair_bits <= 65536u / 4));
     uint32_t slots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
     if (o.ring_slots > 0) slots = (uint32_t)o.ring_slots;
+    if (cl) slots = 2;  // (the cluster kernels' ring)
     // per-warp regions (ring, barriers, queues): the kernel's warp_layout
     // (queues deeper for DNA and 8-byte prefixes, whose walks are long:
     // measured C5 64 -4%, C3 96 -2.5%)
@@ -1814,7 +1893,7 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     // (the BFS prefix) in all that is left (measured: more hot levels beat a
     // larger L1 for the deeper ones).
     uint32_t budget = trie_budget;
-    if (big_l1 || o.placement == PFAC_PLACE_GLOBAL) budget = 64;  // root table and level-1 bitmaps only
+    if (big_l1 || cl || o.placement == PFAC_PLACE_GLOBAL) budget = 64;  // root table and level-1 bitmaps only
     if (o.hot_bytes_cap && o.hot_bytes_cap < budget) budget = o.hot_bytes_cap;
     uint32_t lo = 1, hi = t.n_nodes - 1;
     while (lo < hi) {
@@ -1833,7 +1912,7 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     uint32_t rep_log2 = rep0;
     while (rep_log2 < rep_cap && filter_words * 4 * (2u << rep_log2) <= (left < kFilterCap ? left : kFilterCap))
         rep_log2++;
-    if (big_l1) rep_log2 = 0;
+    if (big_l1 || cl) rep_log2 = 0;
     const uint32_t filter_bytes = filter_words * 4 << rep_log2;
 
     a.t = t;
@@ -1864,6 +1943,19 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     a.off_tbytes = off; off += align16(TBH);
     a.hot_tails = TH;
     a.hot_tail_bytes = TBH;
+    if (cl) {  // the cluster tier: a power-of-two slice of node records per CTA in what is left
+        a.off_dsm = align_up(off, 16);
+        const uint32_t avail = (uint32_t)di.max_smem_optin > a.off_dsm ? (uint32_t)di.max_smem_optin - a.off_dsm : 0u;
+        uint32_t lg = 0;
+        while ((16u << (lg + 1)) <= avail && ((uint64_t)csize << lg) < t.n_nodes) lg++;
+        if ((16u << lg) > avail) {
+            err = "pfac scan plan: no shared memory left for the cluster tier";
+            return kStatusLimit;
+        }
+        a.dsm_log2 = lg;
+        a.dsm_nodes = (uint32_t)std::min<uint64_t>(t.n_nodes, (uint64_t)csize << lg);
+        off = a.off_dsm + (16u << lg);
+    }
     p.smem = off;
     if (p.smem > (size_t)di.max_smem_optin) {
         err = "pfac scan plan: the requested plan does not fit shared memory";
@@ -1914,7 +2006,12 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     f.entry = a.use_entry;
     f.kset = a.use_kset;
     f.pool_rounds = (uint32_t)(geo.n_rounds - a.n_main);
-    f.placement = big_l1 ? PFAC_PLACE_BIG_L1 : o.placement == PFAC_PLACE_GLOBAL ? PFAC_PLACE_GLOBAL : PFAC_PLACE_SMEM;
+    f.placement = cl       ? PFAC_PLACE_CLUSTER
+                  : big_l1 ? PFAC_PLACE_BIG_L1
+                  : o.placement == PFAC_PLACE_GLOBAL ? PFAC_PLACE_GLOBAL : PFAC_PLACE_SMEM;
+    f.cluster = csize;
+    f.dsm_nodes = a.dsm_nodes;
+    p.cluster = csize;
     f.rounds_per_cta = a.rounds_per_cta;
     f.main_rounds = a.n_main;
     return kStatusOk;
@@ -2038,28 +2135,35 @@ int launch_scan(const DevTrie &t, const uint8_t *host_image, int device, const u
     a.hits = reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(d_ws) + geo.off_hits);
     a.aligned = (reinterpret_cast<uintptr_t>(d_text) & 15) == 0;
     void *args[] = {&a};
-    const void *fn = kernel_for(t.kind, p.slots);
+    const void *fn = kernel_for(t.kind, p.slots, p.cluster > 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)geo.grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
     attr[0].val.cooperative = 1;
     cfg.numAttrs = 1;
+    if (p.cluster > 1) {
+        attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+        attr[cfg.numAttrs].val.clusterDim.x = p.cluster;
+        attr[cfg.numAttrs].val.clusterDim.y = 1;
+        attr[cfg.numAttrs].val.clusterDim.z = 1;
+        cfg.numAttrs++;
+    }
     if (o.l2_persist) {  // placement ablation: the device image as an L2 persisting window of this launch
         const ImageHeader &hh = *reinterpret_cast<const ImageHeader *>(host_image);
         const size_t win = std::min<size_t>((size_t)hh.image_bytes - hh.off_node, 64u << 20);
         static std::once_flag once;
         std::call_once(once, [&] { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 64u << 20); });
-        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[1].val.accessPolicyWindow.base_ptr = const_cast<uint32_t *>(t.node);
-        attr[1].val.accessPolicyWindow.num_bytes = win;
-        attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.numAttrs = 2;
+        cudaLaunchAttribute &w = attr[cfg.numAttrs++];
+        w.id = cudaLaunchAttributeAccessPolicyWindow;
+        w.val.accessPolicyWindow.base_ptr = const_cast<uint32_t *>(t.node);
+        w.val.accessPolicyWindow.num_bytes = win;
+        w.val.accessPolicyWindow.hitRatio = 1.0f;
+        w.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        w.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     }
     cfg.attrs = attr;
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);

@@ -507,6 +507,40 @@ def test_placement_variants_exact(cid, placement):
     assert_same(gpu_rows(t, text, offset=2, **placement), want, f"C{cid} {placement}")
 
 
+@pytest.mark.parametrize("cluster", [2, 4, 8])
+@pytest.mark.parametrize("cid", [3, 4, 5])
+def test_cluster_placement_exact(cid, cluster):
+    """The cluster/DSMEM tier of the placement ablation: node
+    records spread over the shared memories of a thread-block cluster, read
+    by the walks through distributed shared memory, give the oracle's rows
+    (a multi-round scan with a ragged tail, and a scan smaller than one
+    cluster's grid)."""
+    ps = gen.patterns(cid)
+    t = pf.Trie(ps)
+    for n in (16 << 20 | 333, 5000):
+        text = gen.text(cid, 1, n)
+        want = oracle.Trie(ps).match(text, engine="ac" if cid == 5 else "pfac")
+        p = t.plan(len(text), placement="cluster", cluster=cluster)
+        assert p["placement"] == pf.PLACEMENTS["cluster"] and p["cluster"] == cluster, p
+        assert p["dsm_nodes"] > 0 and p["grid"] % cluster == 0, p
+        assert_same(gpu_rows(t, text, offset=2, placement="cluster", cluster=cluster), want,
+                    f"C{cid} cluster {cluster} n={n}")
+
+
+def test_cluster_placement_limits():
+    """Cluster placement is for the filter kinds whose tries outgrow one SM
+    (1, 3, 4): the pair-filter kind is refused with LIMIT, a bad cluster size
+    with INVALID_ARG."""
+    t = pf.Trie(gen.patterns(2))
+    with pytest.raises(pf.PfacError) as e:
+        t.plan(1 << 20, placement="cluster")
+    assert e.value.status == 2
+    t4 = pf.Trie(gen.patterns(4))
+    with pytest.raises(pf.PfacError) as e:
+        t4.plan(1 << 20, placement="cluster", cluster=3)
+    assert e.value.status == 1
+
+
 # ------------------------------------- launch hygiene (ADVICE r1 fixes)
 def test_cuda_graph_replay():
     """The scan captured once in a CUDA graph and replayed many times gives

@@ -9,6 +9,9 @@ memory with row_ptr in shared memory (22 Gbps) on a GTX 1080 (PAPER.md:121-125,
   smem     - the whole trie, or its upper levels, in shared memory
   smem+L2p - smem plus the device image as an L2 persisting access window
   big_l1   - no trie level staged, 2-slot ring, one filter copy (largest L1)
+  cluster2/4/8 - thread-block clusters of 2/4/8 CTAs: node records of the
+             BFS prefix spread over the cluster's shared memories, read through
+             distributed shared memory (kinds 1, 3, 4; C2 reports n/a)
   auto     - the planner's choice
 Timing as bench.py (CUDA events, L2 flushed outside them).  One JSON line per
 (config, variant), with the plan the library reports."""
@@ -26,7 +29,8 @@ import paper_1702_03657_b200 as pf  # noqa: E402
 
 VARIANTS = {"global": {"placement": "global"}, "smem": {"placement": "smem"},
             "smem+L2p": {"placement": "smem", "l2_persist": 1}, "big_l1": {"placement": "big_l1"},
-            "auto": {}}
+            "cluster2": {"placement": "cluster", "cluster": 2}, "cluster4": {"placement": "cluster", "cluster": 4},
+            "cluster8": {"placement": "cluster", "cluster": 8}, "auto": {}}
 if os.environ.get("VARIANTS"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["VARIANTS"].split(",")}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -36,6 +40,11 @@ for cid in [int(c) for c in (sys.argv[1:] or ["2", "3", "4", "5"])]:
     trie = pf.Trie(gen.patterns(cid))
     reps = 100 if cid == 2 else 8
     for name, kw in VARIANTS.items():
+        try:
+            plan = trie.plan(n, **kw)
+        except pf.PfacError as e:
+            print(json.dumps({"config": f"C{cid}", "variant": name, "n": n, "unavailable": str(e)}), flush=True)
+            continue
         sc = pf.Scanner(trie, "cuda:0", capacity=n // 64 + 4096, **kw)
         for _ in range(3):
             flush.fill_(1)
@@ -51,8 +60,8 @@ for cid in [int(c) for c in (sys.argv[1:] or ["2", "3", "4", "5"])]:
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) / 1e3)
         t = float(np.median(ts))
-        plan = trie.plan(n, **kw)
         print(json.dumps({"config": f"C{cid}", "variant": name, "n": n, "us": t * 1e6, "gbps": 8 * n / t / 1e9,
                           "count": int(sc.count.item()),
                           "plan": {k: plan[k] for k in ("placement", "hot_nodes", "image_nodes", "filter_copies",
-                                                        "ring_slots", "smem_bytes")}}), flush=True)
+                                                        "ring_slots", "smem_bytes", "grid", "cluster",
+                                                        "dsm_nodes")}}), flush=True)
