@@ -315,21 +315,41 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, int lane, uint32_
 }
 
 // ------------------------------------------------------------ trie access
+// The staged tables as 32-bit shared addresses (read with ldt*: no generic
+// pointer, so no shared-window conversion per use); the terminal tables as
+// generic pointers (shared or global memory).
 struct Smem {
-    const uint32_t *root;       // level-1 table: child of the root per byte
-    const uint32_t *bm;         // level-1 bitmapped nodes, 10 words each (see below)
-    const uint32_t *node;       // node words [0, H]
-    const uint32_t *aux;        // aux words [0, H]
-    const uint8_t *label;       // labels [0, hot_edges)
-    const uint4 *tails;         // tail records [0, hot_tails)
-    const uint8_t *tail_bytes;  // their bytes [0, hot_tail_bytes)
+    uint32_t root;              // level-1 table: child of the root per byte
+    uint32_t bm;                // level-1 bitmapped nodes, 10 words each (see below)
+    uint32_t node;              // node words [0, H]
+    uint32_t aux;               // aux words [0, H]
+    uint32_t label;             // labels [0, hot_edges)
+    uint32_t tails;             // tail records [0, hot_tails), 16 bytes each
+    uint32_t tail_bytes;        // their bytes [0, hot_tail_bytes)
     const uint32_t *out_ptr;    // pid-list offsets by terminal index (smem or global)
     const uint32_t *term_node;  // kept terminal node ids (smem or global)
 };
+// Loads from the staged (immutable after staging) tables: plain asm, so the
+// compiler may schedule and merge them freely.
+__device__ __forceinline__ uint32_t ldt32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldt8(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint4 ldt128(uint32_t addr) {
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 
 __device__ __forceinline__ uint32_t label_at(const ScanArgs &a, const Smem &s, uint32_t e) {
     PFAC_CHECK(e < a.t.n_edges);
-    return e < a.hot_edges ? (uint32_t)s.label[e] : (uint32_t)__ldg(a.t.label + e);
+    return e < a.hot_edges ? ldt8(s.label + e) : (uint32_t)__ldg(a.t.label + e);
 }
 
 // Text of a walk read from global memory (L1/L2): `g` = text + start,
@@ -353,9 +373,10 @@ struct GlobalText {
     }
     // Do the L text bytes from r equal the words pw (L <= end - r checked by
     // the caller)?  The fast path slides over the aligned text words, one load
-    // per 4 bytes; the pattern words come from shared (kHot) or global memory.
+    // per 4 bytes; the pattern words come from shared (kHot: shared address
+    // ps) or global memory (pw).
     template <bool kHot>
-    __device__ __forceinline__ bool equal(uint32_t r, const uint32_t *pw, uint32_t L) const {
+    __device__ __forceinline__ bool equal(uint32_t r, const uint32_t *pw, uint32_t ps, uint32_t L) const {
         const uintptr_t ad = reinterpret_cast<uintptr_t>(g + r);
         if (aligned && r + L + 8 <= end) {
             const uint32_t *w = reinterpret_cast<const uint32_t *>(ad & ~(uintptr_t)3);
@@ -365,7 +386,7 @@ struct GlobalText {
                 const uint32_t a1 = __ldg(w + (k >> 2) + 1);
                 const uint32_t n = L - k;
                 const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
-                const uint32_t pk = kHot ? pw[k >> 2] : __ldg(pw + (k >> 2));
+                const uint32_t pk = kHot ? ldt32(ps + k) : __ldg(pw + (k >> 2));
                 if ((__funnelshift_r(a0, a1, sh) ^ pk) & m) return false;
                 a0 = a1;
             }
@@ -374,7 +395,7 @@ struct GlobalText {
         for (uint32_t k = 0; k < L; k += 4) {
             const uint32_t n = L - k;
             const uint32_t m = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
-            const uint32_t pk = kHot ? pw[k >> 2] : __ldg(pw + (k >> 2));
+            const uint32_t pk = kHot ? ldt32(ps + k) : __ldg(pw + (k >> 2));
             if ((at4(r + k) ^ pk) & m) return false;
         }
         return true;
@@ -412,7 +433,7 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
     const bool hot = v < a.hot_nodes;  // hot records + bytes are in shared memory
     const uint32_t idx = ax;  // aux word: the record's index (= rank among the record nodes)
     PFAC_CHECK(idx < a.t.n_records && (!hot || idx < a.hot_tails));
-    const uint4 rec = hot ? s.tails[idx] : __ldg(a.t.tails + idx);
+    const uint4 rec = hot ? ldt128(s.tails + 16u * idx) : __ldg(a.t.tails + idx);
     PFAC_CHECK(rec.z == kVerify ? (uint64_t)rec.x + rec.y <= a.t.n_records
                                 : (uint64_t)rec.x + rec.y <= a.t.n_tail_bytes && (!hot || rec.x + rec.y <= a.hot_tail_bytes + 3));
     if (rec.z == kVerify) {
@@ -425,15 +446,16 @@ __device__ __forceinline__ uint32_t jump(const ScanArgs &a, const Smem &s, const
             const uint4 cr = __ldg(a.t.tails + c);
             PFAC_CHECK((uint64_t)cr.x + cr.y <= a.t.n_tail_bytes && cr.z < a.t.n_terminals);
             if ((uint64_t)j + cr.y > (uint64_t)tx.end) continue;
-            if (tx.template equal<false>(j, reinterpret_cast<const uint32_t *>(a.t.tail_bytes + cr.x), cr.y))
+            if (tx.template equal<false>(j, reinterpret_cast<const uint32_t *>(a.t.tail_bytes + cr.x), 0u, cr.y))
                 return cr.z;
         }
         return term_of(last);
     }
     if ((uint64_t)j + rec.y > (uint64_t)tx.end) return term_of(last);
     // (separate loops: no shared/global select per word)
-    const bool eq = hot ? tx.template equal<true>(j, reinterpret_cast<const uint32_t *>(s.tail_bytes + rec.x), rec.y)
-                        : tx.template equal<false>(j, reinterpret_cast<const uint32_t *>(a.t.tail_bytes + rec.x), rec.y);
+    const bool eq = hot ? tx.template equal<true>(j, nullptr, s.tail_bytes + rec.x, rec.y)
+                        : tx.template equal<false>(j, reinterpret_cast<const uint32_t *>(a.t.tail_bytes + rec.x), 0u,
+                                                   rec.y);
     if (!eq) return term_of(last);
     if (rec.z != kNone) return rec.z;  // tail
     nv = rec.w;                         // chain
@@ -449,10 +471,10 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
     uint32_t nv = kNone;
     if (l1) {  // level 1 -> 2 through the bitmap
         PFAC_CHECK(v >= 1 && v <= a.t.n_level1);
-        const uint32_t *bm = s.bm + (v - 1) * 10;
-        const uint32_t word = bm[c >> 5];
+        const uint32_t bm = s.bm + 40u * (v - 1);
+        const uint32_t word = ldt32(bm + 4u * (c >> 5));
         if (!((word >> (c & 31)) & 1u)) return kNone;
-        const uint32_t pre = (bm[8 + (c >> 7)] >> (8 * ((c >> 5) & 3))) & 0xFFu;
+        const uint32_t pre = (ldt32(bm + 32u + 4u * (c >> 7)) >> (8 * ((c >> 5) & 3))) & 0xFFu;
         nv = (w & kEdgeMask) + pre + __popc(word & ((1u << (c & 31)) - 1u)) + 1;
     } else {
         const uint32_t lo0 = w & kEdgeMask;
@@ -481,7 +503,7 @@ __device__ __forceinline__ uint32_t child_of(const ScanArgs &a, const Smem &s, u
 #pragma unroll 1
             for (uint32_t q = 0; q < nw; ++q) {
                 const uint32_t e0 = base + 4 * q;
-                const uint32_t wq = hotl ? *reinterpret_cast<const uint32_t *>(s.label + e0)
+                const uint32_t wq = hotl ? ldt32(s.label + e0)
                                          : __ldg(reinterpret_cast<const uint32_t *>(a.t.label + e0));
                 uint32_t oor = 0;  // 0xFF in the bytes outside [lo0, hi0)
                 if (e0 < lo0) oor = (1u << (8 * (lo0 - e0))) - 1u;
@@ -525,9 +547,9 @@ __device__ __forceinline__ void node_load(const ScanArgs &a, const Smem &s, uint
     // (whose last word holds labels 4..7 of a node with 5..8 children; ax2 =
     // kNone for a staged node: its labels are read from shared memory)
     if (v < a.hot_nodes) {
-        w = s.node[v];
-        wn = s.node[v + 1];
-        ax = s.aux[v];
+        w = ldt32(s.node + 4u * v);
+        wn = ldt32(s.node + 4u * v + 4u);
+        ax = ldt32(s.aux + 4u * v);
         ax2 = kNone;
     } else if (kDsm && v < a.dsm_nodes) {  // cluster placement: the record from its owner CTA's shared memory
         extern __shared__ __align__(128) uint8_t smem_base[];
@@ -556,7 +578,7 @@ __device__ uint32_t walk(const ScanArgs &a, const Smem &s, const Text &tx, uint3
                          uint32_t d0 = 1) {
     // (v0, d0): enter at image node v0 of depth d0 whose path the start's
     // first d0 bytes spell (the depth-8 entry table); else from the root
-    uint32_t v = v0 ? v0 : s.root[tx.at(r0)];
+    uint32_t v = v0 ? v0 : ldt32(s.root + 4u * tx.at(r0));
     if (v == 0) return kNone;
     uint32_t w, wn, ax, ax2;
     node_load<kDsm>(a, s, v, w, wn, ax, ax2);
@@ -792,19 +814,21 @@ __device__ __forceinline__ uint2 entry_find(const ScanArgs &a, uint32_t x0, uint
 }
 
 // The shared-memory views of the trie tables (the kernel's layout, ScanArgs).
+template <bool kCl>
 __device__ __forceinline__ Smem make_smem(const ScanArgs &a) {
     extern __shared__ __align__(128) uint8_t smem_base[];
     Smem s;
     // terminal tables: shared-memory copies when staged (generic pointers)
     s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem_base + a.off_terms) : a.t.out_ptr;
     s.term_node = a.off_terms ? s.out_ptr + a.t.n_terminals + 1 : a.t.term_node;
-    s.root = reinterpret_cast<const uint32_t *>(smem_base + a.off_root);
-    s.bm = reinterpret_cast<const uint32_t *>(smem_base + a.off_bm);
-    s.node = reinterpret_cast<const uint32_t *>(smem_base + a.off_node);
-    s.aux = reinterpret_cast<const uint32_t *>(smem_base + a.off_aux);
-    s.label = smem_base + a.off_label;
-    s.tails = reinterpret_cast<const uint4 *>(smem_base + a.off_tails);
-    s.tail_bytes = smem_base + a.off_tbytes;
+    const uint32_t sb = kCl ? smem_u32(smem_base) : kSmemBase;  // (see kSmemBase)
+    s.root = sb + a.off_root;
+    s.bm = sb + a.off_bm;
+    s.node = sb + a.off_node;
+    s.aux = sb + a.off_aux;
+    s.label = sb + a.off_label;
+    s.tails = sb + a.off_tails;
+    s.tail_bytes = sb + a.off_tbytes;
     return s;
 }
 
@@ -866,7 +890,7 @@ __device__ __forceinline__ uint32_t walk_batch(const ScanArgs &a, const Smem &s_
     const int lane = threadIdx.x & 31;
     // kind 1 builds its shared-memory views here (its walks are rare: C4
     // -4.5%); the walk-heavy kinds take them from the flush (C3 -17%)
-    const Smem s = Kind == 1 ? make_smem(a) : s_in;
+    const Smem s = Kind == 1 ? make_smem<kCl>(a) : s_in;
     uint32_t p = 0, tn = kNone;
     if ((uint32_t)lane < m) {
         p = lds32q(bpos + 4u * lane);
@@ -911,7 +935,7 @@ __device__ __forceinline__ FlushOut flush_deferred(const ScanArgs *ap, uint64_t 
                                                 uint32_t n, uint32_t bpos, uint32_t bent, uint32_t nb, bool final,
                                                 uint2 *hits, uint32_t n_hits) {
     const ScanArgs &a = *ap;
-    const Smem s = Kind == 1 ? Smem{} : make_smem(a);  // (see walk_batch)
+    const Smem s = Kind == 1 ? Smem{} : make_smem<kCl>(a);  // (see walk_batch)
     const int lane = threadIdx.x & 31;
     unsigned long long rows = 0;
     __syncwarp();
@@ -1035,7 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();  // barriers initialised
     STAMP(11);
-    const Smem s = make_smem(a);
+    const Smem s = make_smem<kCl>(a);
     // filter addressing: kinds 0, 2, 4: copies interleaved at the unit the
     // kernel loads (8-byte block b of copy r at filter + 8*(b*rep + r); word
     // w of copy r at filter + 4*(w*rep + r)); kinds 1, 3: copy r at filter +
@@ -1242,7 +1266,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     // 2-gram prefix table: word (b0, q) bit j <=> the walk from a start with
     // bytes (b0, 32q + j) gets past level 1 (or b0's node already is a
     // terminal / tail start, where every b1 is kept)
-    const uint32_t *s_pair = reinterpret_cast<const uint32_t *>(smem + a.off_pair);  // (arrived with the tables)
+    const uint32_t s_pair = sb + a.off_pair;  // (shared address; arrived with the tables)
     STAMP(1);
 
     // ================================================= phase 1: scan
@@ -1332,9 +1356,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                     uint32_t keep;
                     if (off + 1 < rl) {
                         const uint32_t b1 = lds8q(p0 + off + 1);  // the slot holds 16 bytes past the round
-                        keep = (s_pair[b0 * 8 + (b1 >> 5)] >> (b1 & 31)) & 1u;
+                        keep = (ldt32(s_pair + 32u * b0 + 4u * (b1 >> 5)) >> (b1 & 31)) & 1u;
                     } else {
-                        keep = s.root[b0] != 0u;  // last readable byte: let the walk decide
+                        keep = ldt32(s.root + 4u * b0) != 0u;  // last readable byte: let the walk decide
                     }
                     km |= keep << k;
                 }
