@@ -172,6 +172,44 @@ def oracle_sample_gbps(otrie, cid, seconds, reps_cap=1000):
     return 8.0 * done / t_tot / 1e9, S, reps, t_tot
 
 
+def oracle_engines(otrie4, ps4, seconds=2.0):
+    """Context beside cpu_baseline (SURVEY §8(d) "oracle beside it"): both CPU
+    engines -- "CPU PFAC" (the paper's walk over the uncompressed bitmap trie)
+    and "CPU Aho-Corasick" (the textbook DFA, the best serial algorithm) -- on
+    16 MiB of C4 with every host thread, and single-threaded on C1 and on
+    4 MiB of C2.  Gbps over the sample; each timing repeats the match until
+    about `seconds` have passed."""
+    import gen
+    import oracle
+    cores = os.cpu_count()
+
+    def rate(ot, text, n, engine, threads):
+        ot.match(text[:1 << 16], readable_len=min(len(text), 1 << 16), lo=0, hi=min(n, 1 << 16), engine=engine,
+                 threads=threads)  # (untimed: lazy per-engine tables)
+        t_tot, done = 0.0, 0
+        while t_tot < seconds:
+            t0 = time.perf_counter()
+            ot.match(text, readable_len=len(text), lo=0, hi=n, engine=engine, threads=threads)
+            t_tot += time.perf_counter() - t0
+            done += n
+        return round(8.0 * done / t_tot / 1e9, 4)
+
+    out = {}
+    t4 = gen.text(4, 0, 16 << 20)
+    for eng in ("pfac", "ac"):
+        try:
+            out[f"C4_16MiB_{eng}_{cores}t"] = rate(otrie4, t4, len(t4), eng, cores)
+        except oracle.OracleError as e:  # C4's DFA (6.4 M states x 256) exceeds the oracle's size limit
+            out[f"C4_16MiB_{eng}_{cores}t"] = f"unavailable ({e})"
+    for cid, nbytes in ((1, None), (2, 4 << 20)):
+        ot = oracle.Trie(gen.patterns(cid))
+        tx = gen.text(cid, 0, nbytes or gen.config(cid)["text_len"])
+        for eng in ("pfac", "ac"):
+            out[f"C{cid}_{eng}_1t"] = rate(ot, tx, len(tx), eng, 1)
+    out["unit"] = "Gbps"
+    return out
+
+
 def run_reference(args, rank):
     """`--impl reference`: the oracle as it stands (oracle/, test
     infrastructure) on the box's host cores, same metric and config; each step
@@ -465,7 +503,8 @@ def main():
         g, S, reps, tt = oracle_sample_gbps(otrie, CONFIG_ID, args.cpu_seconds)
         cpu = {"value": g, "unit": "Gbps", "cores": os.cpu_count(), "kind": "oracle",
                "sample": f"{reps} pass(es) over the first {S} start positions of the C4 text "
-                         f"(PFAC bitmap-trie walk, {os.cpu_count()} threads, {tt:.1f} s)"}
+                         f"(PFAC bitmap-trie walk, {os.cpu_count()} threads, {tt:.1f} s)",
+               "engines": oracle_engines(otrie, ps)}
 
     variants = None  # the C4 launch with the trie cut at 8 levels (NEXT-1) and as the merged DAG (NEXT-2)
     if rank == 0 and world == 1 and not args.no_extras:
