@@ -371,6 +371,23 @@ struct GlobalText {
             if (r + b < end) x |= (uint32_t)__ldg(g + r + b) << (8 * b);
         return x;
     }
+    // bytes r..r+15 as four little-endian words (one load per word + one for
+    // the misalignment when the text is aligned and 20 bytes are readable)
+    __device__ __forceinline__ void at16(uint32_t r, uint32_t (&o)[4]) const {
+        const uintptr_t ad = reinterpret_cast<uintptr_t>(g + r);
+        if (aligned && r + 20 <= end) {
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(ad & ~(uintptr_t)3);
+            const uint32_t sh = 8 * (uint32_t)(ad & 3);
+            uint32_t x[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) x[q] = __ldg(w + q);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) o[q] = __funnelshift_r(x[q], x[q + 1], sh);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) o[q] = at4(r + 4 * q);
+        }
+    }
     // Do the L text bytes from r equal the words pw (L <= end - r checked by
     // the caller)?  The fast path slides over the aligned text words, one load
     // per 4 bytes; the pattern words come from shared (kHot: shared address
@@ -860,11 +877,12 @@ __device__ __forceinline__ uint32_t probe_start(const ScanArgs &a, const GlobalT
     if (Kind == 3) {  // enter at depth <= 16 when the 16 bytes are A/C/G/T (the key
                       // aliases other bytes, and no DNA pattern can cover those)
         if (gt.end < kDnaGram) return kNone;
-        uint32_t k = 0;
+        uint32_t k = 0, w16[4];
         bool acgt = true;
+        gt.at16(0, w16);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const uint32_t w = gt.at4(4 * q);
+            const uint32_t w = w16[q];
             const uint32_t c = (w >> 1) & 0x03030303u;  // the four 2-bit codes, one per byte
             const uint32_t sel = (c & 0xFu) | ((c >> 4) & 0xF0u) | ((c >> 8) & 0xF00u) | ((c >> 12) & 0xF000u);
             acgt &= __byte_perm(0x47544341u, 0u, sel) == w;  // code -> 'A','C','T','G'
