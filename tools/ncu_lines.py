@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Summarise an ncu report's source page per CUDA source line:
 warp-stall samples, warp instructions executed, top stall reasons.
-usage: python tools/ncu_lines.py report.ncu-rep [top_n]"""
+usage: python tools/ncu_lines.py report.ncu-rep [top_n] [scan.cu]
+(the optional source file supplies the text of scan.cu lines, when the
+report's copy is not the source the binary was built from)"""
 import csv
 import io
 import subprocess
@@ -9,6 +11,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+src = open(sys.argv[3]).read().splitlines() if len(sys.argv) > 3 else None
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 def num(x):
@@ -43,5 +46,8 @@ for f, d in rows[:top]:
     if s == 0:
         break
     st = sorted(((num(d.get(h)), h[6:]) for h in stalls), reverse=True)[:3]
+    text = d['Source'].strip()
+    if src and f == "scan.cu" and 0 < int(d['Line No']) <= len(src):
+        text = src[int(d['Line No']) - 1].strip()
     print(f"{100*s/tot:5.1f}% {f}:{d['Line No']:>4} inst={d.get('Instructions Executed','')} "
-          f"thr={d.get('Avg. Threads Executed','')} {st} | {d['Source'].strip()[:90]}")
+          f"thr={d.get('Avg. Threads Executed','')} {st} | {text[:90]}")
