@@ -7,30 +7,39 @@
 // algorithm also allows for coalesced memory access during the first memory
 // transfer, and early thread termination."
 //
-// B200 mapping (DESIGN.md "Kernels"):
-//  * one persistent CTA per SM (kWarps warps).  Shared memory holds, once per
-//    SM, the first-stage filter (replicated per bank group so lanes rarely
-//    conflict; at smem offset 0 so a byte offset is an address), the level-1
-//    table, the level-1 bitmapped nodes (Fig. 3), and the top H
-//    nodes of the breadth-first CSR trie (BFS order = level order, so the
-//    first H nodes are the hot upper levels; PAPER.md:89 kept row_ptr on chip
-//    for the same reason).
+// B200 mapping (DESIGN.md §6):
+//  * one persistent CTA per SM (kWarps warps, 64 registers).  Shared memory
+//    holds, once per SM, the first-stage filter at offset 0 (replicated with
+//    bank swizzles while it fits), one region per warp (text ring, its
+//    mbarriers, the probe and walk queues; compile-time offsets from one
+//    base), the level-1 table, the level-1 bitmapped nodes (PAPER.md:97
+//    Fig. 3), the 2-gram table where selective, and the top H nodes of the
+//    breadth-first CSR trie (BFS order = level order, so the first H nodes
+//    are the hot upper levels; PAPER.md:89 kept row_ptr on chip for the same
+//    reason).  The dynamic window starts at shared address kSmemBase (checked
+//    at entry), so queues, ring and tables are addressed as 32-bit constants
+//    plus offsets.  Cluster placement (PFAC_PLACE_CLUSTER, the kCl kernels)
+//    instead spreads the node records of the BFS prefix over a thread-block
+//    cluster, read through distributed shared memory.
 //  * phase 1 (scan): CTA b owns a contiguous range of 1024-start rounds; its
 //    warps own contiguous blocks of the range's first part and take the rest
-//    (the last quarter, or a plan's share) from a shared counter.  A per-warp ring of kSlots slots (1 KiB + 16-byte overhang) is
-//    filled by TMA bulk copies (cp.async.bulk + mbarrier, evict-first in L2)
-//    kSlots-1 rounds ahead.  Per round each lane tests its 32 consecutive
-//    starts against the filter (a clear bit means no pattern can start there:
-//    PFAC's early termination taken before the first trie access), then
-//    tests each survivor against the 2-gram prefix table (level-1 bitmapped
-//    nodes); the few kept are queued in position order and walked in
-//    full-warp batches to the first mismatch.  A start that passed a terminal
-//    is appended, in position order, to the warp's hit list (offset, terminal
-//    index), its pid count to the lane's rows (block) or the round's count.
+//    (a plan's share) from a shared counter; the text's last rounds form a
+//    cross-CTA pool.  A per-warp ring of kSlots slots (1 KiB + 16-byte
+//    overhang) is filled by TMA bulk copies (cp.async.bulk + mbarrier,
+//    evict-first in L2) kSlots-1 rounds ahead.  Per round each lane tests its
+//    32 consecutive starts against the filter (a clear bit means no pattern
+//    can start there: PFAC's early termination taken before the first trie
+//    access), then, where selective, each survivor against the 2-gram prefix
+//    table; the kept starts are queued in position order, probed in full-warp
+//    batches (exact key set, kind 1; depth-8/16 entry table, kinds 4/3) and
+//    the survivors walked 32 at a time to the first mismatch.  A start that
+//    passed a terminal is appended, in position order, to the warp's hit list
+//    (offset, terminal index), its pid count to the lane's rows (block) or the
+//    round's count.
 //  * phase 2 (offsets): CTA exclusive scan of the warp totals and the dynamic
-//    rounds' counts -> one grid
-//    barrier -> exclusive prefix over CTA totals.  Ranges are contiguous and
-//    ordered, so the concatenation is globally sorted by (pos, pid).
+//    rounds' counts -> a self-resetting grid barrier -> exclusive prefix over
+//    CTA totals (the pool's segments after a second barrier).  Ranges are
+//    contiguous and ordered, so the concatenation is sorted by (pos, pid).
 //  * phase 3 (emit): each warp expands its hit list into (pos, pid) rows (a
 //    segmented scan gives each row its index).  A warp whose list overflowed
 //    re-scans its rounds writing rows directly.
