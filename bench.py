@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-verify", action="store_true", help="skip rank 0's oracle count/digest check")
     ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C5 side lines (N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample (wall seconds)")
+    ap.add_argument("--ref-seconds", type=float, default=45.0,
+                    help="--impl reference: oracle seconds over all steps (each step a bounded sample)")
     return ap.parse_args()
 
 
@@ -222,7 +224,7 @@ def run_reference(args, rank):
     ps = gen.patterns(CONFIG_ID)
     otrie = oracle.Trie(ps)
     cores = os.cpu_count()
-    per_step = 45.0 / max(1, args.steps + args.warmup)
+    per_step = args.ref_seconds / max(1, args.steps + args.warmup)
     _, S, _, _ = oracle_sample_gbps(otrie, CONFIG_ID, per_step, reps_cap=1)
     text = gen.text(CONFIG_ID, 0, S + 4096)
     for _ in range(args.warmup):
