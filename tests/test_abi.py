@@ -263,3 +263,35 @@ def test_no_cpu_fallback():
     with pytest.raises(pf.PfacError) as e:
         t.match_host(b"ushers")
     assert e.value.status == 4
+
+
+def test_option_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of pfac_build_options / pfac_plan_options /
+    pfac_plan_info (argument marshalling only) have the header's size and
+    field offsets: compiled from include/pfac.h with the host C compiler."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no host C compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    structs = {"pfac_build_options": pf.BuildOptions, "pfac_plan_options": pf.PlanOptions,
+               "pfac_plan_info": pf._PlanInfo}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pfac.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines():
+        cname, f, v = line.split()
+        got[(cname, f)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
