@@ -47,6 +47,12 @@ WORKLOADS = {
     5: "C5: 50,000 DNA k-mers (k=16-32), 2 GiB slice of the 16 GiB genome-like text (its 1-GPU share at G=8)",
 }
 EXTRA_BYTES = {2: 64 << 20, 3: 1 << 30, 5: 2 << 30}
+# --config: the headline workload (4: the metric's config; 5: C5's whole
+# 16 GiB genome-like text, the SURVEY §8(e) 8-GPU configuration, strong
+# scaling of the 16 GiB over --gpus N)
+HEADLINE = {4: WORKLOADS[4],
+            5: "C5: 50,000 DNA k-mers (k=16-32), 16 GiB genome-like text (the 8-GPU configuration)"}
+ORACLE_ENGINE = {4: "pfac", 5: "ac"}  # C5: the AC engine (the bitmap-trie walk is ~4x slower on DNA)
 PAPER_CONTEXT = {"gbps": 22, "hw": "GTX 1080", "patterns": 1000, "text": "King James Bible", "cite": "PAPER.md:136"}
 
 
@@ -56,6 +62,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="pfac", choices=["pfac", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[4, 5],
+                    help="4: C4 4 GiB (default, the metric's config); 5: C5's whole 16 GiB")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true", help="skip rank 0's oracle count/digest check")
@@ -149,7 +157,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU oracle
-def oracle_sample_gbps(otrie, cid, seconds, reps_cap=1000):
+def oracle_sample_gbps(otrie, cid, seconds, reps_cap=1000, engine="pfac"):
     """The oracle as it stands (PFAC bitmap-trie walk, all host threads) on a
     bounded prefix of config cid's text: (Gbps, bytes per pass, passes)."""
     import gen
@@ -158,7 +166,7 @@ def oracle_sample_gbps(otrie, cid, seconds, reps_cap=1000):
     probe = 16 << 20
     text = gen.text(cid, 0, probe + 4096)
     t0 = time.perf_counter()
-    otrie.match(text[:probe + 127], readable_len=probe + 127, lo=0, hi=probe, engine="pfac", threads=cores)
+    otrie.match(text[:probe + 127], readable_len=probe + 127, lo=0, hi=probe, engine=engine, threads=cores)
     est = (time.perf_counter() - t0) / probe  # s per byte
     S = int(min(n - 4096, max(probe, seconds / max(est, 1e-12))))
     S -= S % 4096
@@ -167,19 +175,19 @@ def oracle_sample_gbps(otrie, cid, seconds, reps_cap=1000):
     done, t_tot, reps = 0, 0.0, 0
     while t_tot < seconds and reps < reps_cap:
         t0 = time.perf_counter()
-        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine="pfac", threads=cores)
+        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine=engine, threads=cores)
         t_tot += time.perf_counter() - t0
         done += S
         reps += 1
     return 8.0 * done / t_tot / 1e9, S, reps, t_tot
 
 
-def oracle_engines(otrie4, ps4, seconds=2.0):
+def oracle_engines(otrie_h, cid_h, seconds=2.0):
     """Context beside cpu_baseline (SURVEY §8(d) "oracle beside it"): both CPU
     engines -- "CPU PFAC" (the paper's walk over the uncompressed bitmap trie)
     and "CPU Aho-Corasick" (the textbook DFA, the best serial algorithm) -- on
-    16 MiB of C4 with every host thread, and single-threaded on C1 and on
-    4 MiB of C2.  Gbps over the sample; each timing repeats the match until
+    16 MiB of the headline config (otrie_h = its oracle trie) with every host
+    thread, and single-threaded on C1 and on 4 MiB of C2.  Gbps over the sample; each timing repeats the match until
     about `seconds` have passed."""
     import gen
     import oracle
@@ -197,12 +205,12 @@ def oracle_engines(otrie4, ps4, seconds=2.0):
         return round(8.0 * done / t_tot / 1e9, 4)
 
     out = {}
-    t4 = gen.text(4, 0, 16 << 20)
+    th = gen.text(cid_h, 0, 16 << 20)
     for eng in ("pfac", "ac"):
         try:
-            out[f"C4_16MiB_{eng}_{cores}t"] = rate(otrie4, t4, len(t4), eng, cores)
+            out[f"C{cid_h}_16MiB_{eng}_{cores}t"] = rate(otrie_h, th, len(th), eng, cores)
         except oracle.OracleError as e:  # C4's DFA (6.4 M states x 256) exceeds the oracle's size limit
-            out[f"C4_16MiB_{eng}_{cores}t"] = f"unavailable ({e})"
+            out[f"C{cid_h}_16MiB_{eng}_{cores}t"] = f"unavailable ({e})"
     for cid, nbytes in ((1, None), (2, 4 << 20)):
         ot = oracle.Trie(gen.patterns(cid))
         tx = gen.text(cid, 0, nbytes or gen.config(cid)["text_len"])
@@ -221,27 +229,30 @@ def run_reference(args, rank):
         return
     import gen
     import oracle
-    ps = gen.patterns(CONFIG_ID)
+    cid = args.config
+    eng = ORACLE_ENGINE[cid]
+    ps = gen.patterns(cid)
     otrie = oracle.Trie(ps)
     cores = os.cpu_count()
     per_step = args.ref_seconds / max(1, args.steps + args.warmup)
-    _, S, _, _ = oracle_sample_gbps(otrie, CONFIG_ID, per_step, reps_cap=1)
-    text = gen.text(CONFIG_ID, 0, S + 4096)
+    _, S, _, _ = oracle_sample_gbps(otrie, cid, per_step, reps_cap=1, engine=eng)
+    text = gen.text(cid, 0, S + 4096)
     for _ in range(args.warmup):
-        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine="pfac", threads=cores)
+        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine=eng, threads=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine="pfac", threads=cores)
+        otrie.match(text[:S + 127], readable_len=S + 127, lo=0, hi=S, engine=eng, threads=cores)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     gbps = 8.0 * S * len(times) / tot / 1e9
-    sample = f"first {S} start positions of the C4 text per step (PFAC bitmap-trie walk, {cores} threads)"
+    sample = (f"first {S} start positions of the C{cid} text per step "
+              f"({'PFAC bitmap-trie walk' if eng == 'pfac' else 'Aho-Corasick DFA'}, {cores} threads)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": gbps, "unit": "Gbps", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": WORKLOADS[CONFIG_ID], "text_bytes": S, "patterns": len(ps),
+        "config": {"workload": HEADLINE[cid], "text_bytes": S, "patterns": len(ps),
                    "parallelism": "cpu threads"},
         "cpu_baseline": {"value": gbps, "unit": "Gbps", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbps, "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -342,6 +353,8 @@ def extra_configs(dev, flush, peak, stream):
 # ---------------------------------------------------------------- main
 def main():
     args = parse()
+    global CONFIG_ID
+    CONFIG_ID = args.config
     rank, local_rank, world = dist_env()
     if args.impl == "reference":
         run_reference(args, rank)
@@ -465,7 +478,7 @@ def main():
             gp, gq = gpos.cpu().numpy().astype(np.uint64), gpid.cpu().numpy().astype(np.uint32)
         full = host.numpy() if world == 1 else gen.text(CONFIG_ID, 0, n_total)
         t0 = time.perf_counter()
-        wp, wq = otrie.match(full, engine="pfac", threads=os.cpu_count())
+        wp, wq = otrie.match(full, engine=ORACLE_ENGINE[CONFIG_ID], threads=os.cpu_count())
         verify = {"rows": int(len(gp)), "digest": digest(gp, gq), "oracle_rows": int(len(wp)),
                   "oracle_digest": digest(wp, wq),
                   "equal": bool(len(gp) == len(wp) and np.array_equal(gp, wp) and np.array_equal(gq, wq)),
@@ -502,14 +515,16 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         otrie = otrie or oracle.Trie(ps)
-        g, S, reps, tt = oracle_sample_gbps(otrie, CONFIG_ID, args.cpu_seconds)
+        eng = ORACLE_ENGINE[CONFIG_ID]
+        g, S, reps, tt = oracle_sample_gbps(otrie, CONFIG_ID, args.cpu_seconds, engine=eng)
         cpu = {"value": g, "unit": "Gbps", "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"{reps} pass(es) over the first {S} start positions of the C4 text "
-                         f"(PFAC bitmap-trie walk, {os.cpu_count()} threads, {tt:.1f} s)",
-               "engines": oracle_engines(otrie, ps)}
+               "sample": f"{reps} pass(es) over the first {S} start positions of the C{CONFIG_ID} text "
+                         f"({'PFAC bitmap-trie walk' if eng == 'pfac' else 'Aho-Corasick DFA'}, "
+                         f"{os.cpu_count()} threads, {tt:.1f} s)",
+               "engines": oracle_engines(otrie, CONFIG_ID)}
 
     variants = None  # the C4 launch with the trie cut at 8 levels (NEXT-1) and as the merged DAG (NEXT-2)
-    if rank == 0 and world == 1 and not args.no_extras:
+    if rank == 0 and world == 1 and not args.no_extras and CONFIG_ID == 4:
         variants = {}
         for name, bkw, pkw in [("truncated_depth8", {"truncate_depth": 8}, {}),
                                ("merged_dag", {"merge_suffixes": 1}, {"form": "merged_dag"})]:
@@ -532,10 +547,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "Gbps", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": WORKLOADS[CONFIG_ID], "text_bytes": int(n_total), "patterns": len(ps),
+            "config": {"workload": HEADLINE[CONFIG_ID], "text_bytes": int(n_total), "patterns": len(ps),
                        "parallelism": f"text-sharded x{world} (4 KiB-aligned starts, halo {st['max_len'] - 1} B)"
                                       + (", rank-0 gather in every step" if world > 1 else ""),
-                       "l2": "text 4 GiB > L2; also flushed before every step (256 MiB write, outside the events)"},
+                       "l2": f"text {n_total >> 30} GiB > L2; also flushed before every step (256 MiB write, outside the events)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "pfac_scan_kernel", "alg_bytes_per_launch": int(alg_bytes),
