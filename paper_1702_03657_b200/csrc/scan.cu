@@ -2028,7 +2028,11 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     // dynamically (measured: C3 -11% dynamic)
     // (kind 1, large sets of random-looking byte patterns: even work per
     // round, so every CTA range is static and only the pool balances: C4 -2%)
-    a.ctg64 = o.ctg64 >= 0 ? (uint32_t)o.ctg64 : (H >= t.n_nodes - 1 || t.kind == 1 ? 64u : 48u);
+    // (DNA, kind 3, with >= 128 rounds per warp: 60/64 static -- its walks per
+    // round vary less than C3's token text: C5 2 GiB -1.5%; at 55 rounds per
+    // warp (256 MiB) the dynamic quarter still pays: +5% with 60)
+    const bool dna_long = t.kind == 3 && geo.rounds_per_cta >= 128u * kWarps;
+    a.ctg64 = o.ctg64 >= 0 ? (uint32_t)o.ctg64 : (H >= t.n_nodes - 1 || t.kind == 1 ? 64u : dna_long ? 60u : 48u);
     // the shared pool: the text's last rounds, taken by any warp whose CTA's
     // range is done (cross-CTA balance where walks leave the SM: content
     // skew between ranges, e.g. C5's first ranges hold twice the matches);
