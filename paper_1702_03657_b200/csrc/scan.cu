@@ -2038,7 +2038,8 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     // skew between ranges, e.g. C5's first ranges hold twice the matches);
     // planned when start offsets from a CTA's first round fit 32 bits
     {
-        const uint64_t pool64 = o.pool64 >= 0 ? (uint64_t)o.pool64 : (a.ctg64 < 64 || t.kind == 1 ? 4u : 0u);
+        // (kind 1: 2/64, its rounds are even: C4 4 GiB -0.5% against 4/64)
+        const uint64_t pool64 = o.pool64 >= 0 ? (uint64_t)o.pool64 : t.kind == 1 ? 2u : a.ctg64 < 64 ? 4u : 0u;
         const uint64_t n_pool = geo.n_rounds * pool64 / 64;
         const bool pool = t.kind != 2 && n_pool >= geo.grid && geo.n_rounds * (uint64_t)kRound <= (1ull << 32);
         a.n_main = pool ? geo.n_rounds - n_pool : geo.n_rounds;
