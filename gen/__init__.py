@@ -23,6 +23,7 @@ CONFIG_NAMES = {
     3: "C3 10,000 Snort/ClamAV-shaped patterns len 8-64 / 1 GiB packets",
     4: "C4 100,000 byte patterns len 4-128 / 4 GiB",
     5: "C5 DNA 50,000 k-mers k=16-32 / 16 GiB",
+    6: "C4 ASCII variant: 100,000 printable patterns len 4-128 / 4 GiB printable text (reported, not gating)",
 }
 
 

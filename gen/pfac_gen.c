@@ -131,6 +131,10 @@ int pg_config_get(int id, pg_config *c) {
     case 5: /* DNA, 50,000 k-mers k=16..32, 16 GiB genome-like */
         c->text_len = 16ull << 30; c->n_patterns = 50000; c->min_len = 16; c->max_len = 32;
         return 0;
+    case 6: /* C4's ASCII variant (reported): 100,000 printable patterns len 4..128,
+               4 GiB printable text */
+        c->text_len = 4ull << 30; c->n_patterns = 100000; c->min_len = 4; c->max_len = 128;
+        return 0;
     default:
         return -1;
     }
@@ -314,7 +318,7 @@ static void bg_dna(uint64_t seed, uint64_t chunk, uint8_t *b) {
 }
 static void gen_background(const pg_config *c, uint64_t chunk, uint8_t *b) {
     switch (c->id) {
-    case 1: case 2: bg_printable(c->seed_text, chunk, b); break;
+    case 1: case 2: case 6: bg_printable(c->seed_text, chunk, b); break;
     case 3: bg_packets(c->seed_text, chunk, b); break;
     case 4: bg_uniform(c->seed_text, chunk, b); break;
     case 5: bg_dna(c->seed_text, chunk, b); break;
@@ -504,12 +508,12 @@ int pg_make_patterns(const pg_config *c, uint8_t **data, uint32_t **lens, uint32
     if (c->id == 1) {
         static const char *toy[4] = {"he", "she", "his", "hers"};
         for (int i = 0; i < 4; i++) ps_add(&ps, (const uint8_t *)toy[i], (uint32_t)strlen(toy[i]));
-    } else if (c->id == 2 || c->id == 4) {
+    } else if (c->id == 2 || c->id == 4 || c->id == 6) {
         uint32_t span = c->max_len - c->min_len + 1;
         while (ps.n < c->n_patterns) {
             uint32_t l = c->min_len + (uint32_t)mt_unif(&mt, span);
             for (uint32_t k = 0; k < l; k++)
-                p[k] = c->id == 2 ? (uint8_t)(0x20 + mt_unif(&mt, 95)) : (uint8_t)mt_unif(&mt, 256);
+                p[k] = c->id != 4 ? (uint8_t)(0x20 + mt_unif(&mt, 95)) : (uint8_t)mt_unif(&mt, 256);
             ps_add(&ps, p, l);
         }
     } else if (c->id == 3) {

@@ -1921,7 +1921,7 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
         const uint32_t *pair = reinterpret_cast<const uint32_t *>(host_image + hh.off_pair);
         for (uint32_t j = 0; j < 2048; j++) pair_bits += (uint32_t)__builtin_popcount(pair[j]);
     }
-    const bool use_pair = t.kind != 3 && (o.stage2 == 1 || (o.stage2 == -1 && pair_bits <= 65536u / 4));
+    bool use_pair = t.kind != 3 && (o.stage2 == 1 || (o.stage2 == -1 && pair_bits <= 65536u / 4));
     uint32_t slots = filter_words * 4 > 65536u || big_l1 ? 2u : (uint32_t)kSlotsMax;  // ring depth
     if (o.ring_slots > 0) slots = (uint32_t)o.ring_slots;
     if (cl) slots = 2;  // (the cluster kernels' ring)
@@ -1929,8 +1929,12 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     // (queues deeper for DNA and 8-byte prefixes, whose walks are long:
     // measured C5 64 -4%, C3 96 -2.5%)
     const uint32_t warp_bytes = warp_layout((int)t.kind, (int)slots).bytes;
-    const uint32_t fixed = kWarps * warp_bytes + 16 + 1024 + (use_pair ? 8192 : 0) + align16(40 * B) +
-                           8 * (kWarps + 2) + 512;
+    const uint32_t fixed0 = kWarps * warp_bytes + 16 + 1024 + align16(40 * B) + 8 * (kWarps + 2) + 512;
+    // an automatic 2-gram table that does not fit beside the filter and ring
+    // is dropped (e.g. C4's ASCII variant: 128 KiB filter, selective 2-grams)
+    if (use_pair && o.stage2 == -1 && (uint32_t)di.max_smem_optin < fixed0 + 8192 + filter_words * 4 + 64)
+        use_pair = false;
+    const uint32_t fixed = fixed0 + (use_pair ? 8192 : 0);
     if ((uint32_t)di.max_smem_optin < fixed + filter_words * 4 + 64) {
         err = "pfac scan plan: filter and text ring do not fit shared memory";
         return kStatusLimit;

@@ -6,20 +6,20 @@ import pytest
 import gen
 
 
-@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5, 6])
 def test_patterns_shape(cid):
     c = gen.config(cid)
     ps = gen.patterns(cid)
     assert len(ps) == c["n_patterns"]
     assert ps.lens.min() >= c["min_len"] and ps.lens.max() <= c["max_len"]
     assert len(set(ps.to_list())) == len(ps)                 # deduplicated by resampling
-    if cid == 2:
+    if cid in (2, 6):
         assert ps.data.min() >= 0x20 and ps.data.max() <= 0x7E
     if cid == 5:
         assert set(np.unique(ps.data).tolist()) <= set(b"ACGT")
 
 
-@pytest.mark.parametrize("cid", [2, 3, 4, 5])
+@pytest.mark.parametrize("cid", [2, 3, 4, 5, 6])
 def test_text_chunk_independence(cid):
     full = gen.text(cid, 0, 3 * gen.CHUNK)
     for a, n in [(0, 100), (gen.CHUNK - 7, 20), (gen.CHUNK + 12345, gen.CHUNK), (2 * gen.CHUNK, gen.CHUNK)]:
@@ -30,8 +30,9 @@ def test_text_chunk_independence(cid):
 
 
 def test_text_value_ranges():
-    t2 = gen.text(2, 0, gen.CHUNK)
-    assert t2.min() >= 0x20 and t2.max() <= 0x7E
+    for cid in (2, 6):
+        t2 = gen.text(cid, 0, gen.CHUNK)
+        assert t2.min() >= 0x20 and t2.max() <= 0x7E
     t5 = gen.text(5, 0, gen.CHUNK)
     assert set(np.unique(t5).tolist()) <= set(b"ACGT")
     freq = np.bincount(t5, minlength=256)[list(b"ACGT")] / t5.size
