@@ -47,8 +47,11 @@ WORKLOADS = {
     5: "C5: 50,000 DNA k-mers (k=16-32), 2 GiB slice of the 16 GiB genome-like text (its 1-GPU share at G=8)",
     6: "C4's ASCII variant (reported, not gating): 100,000 printable patterns (len 4-128), 1 GiB slice of its "
        "4 GiB printable text",
+    7: "C2's paper-shaped variant (reported): 1,000 substrings (len 4-32) of a Zipf(1.0) word text, 64 MiB",
+    8: "C2's dense variant (reported): every 64-byte slot planted, 64 MiB",
 }
-EXTRA_BYTES = {2: 64 << 20, 3: 1 << 30, 5: 2 << 30, 6: 1 << 30}
+EXTRA_BYTES = {2: 64 << 20, 3: 1 << 30, 5: 2 << 30, 6: 1 << 30, 7: 64 << 20, 8: 64 << 20}
+EXTRA_NAMES = {6: "C4ascii", 7: "C2paper", 8: "C2dense"}
 # --config: the headline workload (4: the metric's config; 5: C5's whole
 # 16 GiB genome-like text, the SURVEY §8(e) 8-GPU configuration, strong
 # scaling of the 16 GiB over --gpus N)
@@ -326,8 +329,8 @@ def byte_stages(ps):
 
 
 def extra_configs(dev, flush, peak, stream):
-    """C2, C3, C5 (1-GPU sizes) and C4's ASCII variant timed like the
-    headline: side lines only."""
+    """C2, C3, C5 (1-GPU sizes) and the reported variants (C4 ASCII, C2
+    paper-shaped and dense) timed like the headline: side lines only."""
     import torch
 
     import gen
@@ -341,9 +344,9 @@ def extra_configs(dev, flush, peak, stream):
         text = host.to(dev)
         sc = pf.Scanner(trie, dev, capacity=max(1 << 16, n // 256))
         time_launches(sc, text, flush, n, 3, stream)
-        med, mean = time_launches(sc, text, flush, n, 30 if cid == 2 else 10, stream)
+        med, mean = time_launches(sc, text, flush, n, 30 if n <= (64 << 20) else 10, stream)
         cnt = int(sc.count.item())
-        out["C4ascii" if cid == 6 else f"C{cid}"] = {"workload": WORKLOADS[cid], "text_bytes": n, "us_median": 1e6 * med,
+        out[EXTRA_NAMES.get(cid, f"C{cid}")] = {"workload": WORKLOADS[cid], "text_bytes": n, "us_median": 1e6 * med,
                           "gbps": 8.0 * n / med / 1e9, "hbm_frac": (n + 12 * cnt) / med / 1e9 / peak,
                           "matches": cnt,
                           "trie_image_vs_uncompressed": trie.nbytes("device_image") / trie.nbytes("uncompressed"),

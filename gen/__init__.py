@@ -24,6 +24,8 @@ CONFIG_NAMES = {
     4: "C4 100,000 byte patterns len 4-128 / 4 GiB",
     5: "C5 DNA 50,000 k-mers k=16-32 / 16 GiB",
     6: "C4 ASCII variant: 100,000 printable patterns len 4-128 / 4 GiB printable text (reported, not gating)",
+    7: "C2 paper-shaped variant: 1,000 substrings (len 4-32) of a Zipf(1.0) word text / 64 MiB (reported)",
+    8: "C2 dense variant: C2's distribution (its own seeds) with every 64-byte slot planted / 64 MiB (reported)",
 }
 
 

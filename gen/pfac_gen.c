@@ -135,6 +135,15 @@ int pg_config_get(int id, pg_config *c) {
                4 GiB printable text */
         c->text_len = 4ull << 30; c->n_patterns = 100000; c->min_len = 4; c->max_len = 128;
         return 0;
+    case 7: /* C2's paper-shaped variant (reported): 1,000 patterns len 4..32
+               MT-sampled as substrings of the first 4 MiB of a Zipf(1.0) word text (20 K
+               pseudo-words), 64 MiB of that text */
+        c->text_len = 64ull << 20; c->n_patterns = 1000; c->min_len = 4; c->max_len = 32;
+        return 0;
+    case 8: /* C2's dense variant (reported): C2 with every 64-byte slot planted */
+        c->text_len = 64ull << 20; c->n_patterns = 1000; c->min_len = 4; c->max_len = 32;
+        c->plant_slot = 64; c->plant_p_q20 = 1u << 20;
+        return 0;
     default:
         return -1;
     }
@@ -316,9 +325,51 @@ static void bg_dna(uint64_t seed, uint64_t chunk, uint8_t *b) {
         }
     }
 }
+/* ------------------------------------ C2 paper-shaped: Zipf word text */
+/* 20,000 pseudo-words (2..10 lowercase letters) drawn once from a fixed seed;
+ * a chunk is words drawn by Zipf(1.0) (rank k with weight 1/k, inverse CDF by
+ * binary search on a 2^32-scaled cumulative table), separated by single
+ * spaces; a word cut by the chunk end is cut. */
+#define ZW_N 20000
+static struct {
+    char w[ZW_N][11];
+    uint8_t len[ZW_N];
+    uint64_t cdf[ZW_N]; /* cumulative weight, scaled to 2^32 */
+} ZW;
+static pthread_once_t ZW_once = PTHREAD_ONCE_INIT;
+static void zw_init(void) {
+    uint64_t s = 0x5A17F00Dull;
+    double tot = 0, acc = 0;
+    for (int i = 0; i < ZW_N; i++) tot += 1.0 / (i + 1);
+    for (int i = 0; i < ZW_N; i++) {
+        int l = 2 + (int)sm_unif(&s, 9); /* 2..10 letters */
+        for (int k = 0; k < l; k++) ZW.w[i][k] = (char)('a' + sm_unif(&s, 26));
+        ZW.len[i] = (uint8_t)l;
+        acc += 1.0 / (i + 1);
+        ZW.cdf[i] = (uint64_t)(acc / tot * 4294967296.0);
+    }
+    ZW.cdf[ZW_N - 1] = 1ull << 32;
+}
+static void bg_zipf_words(uint64_t seed, uint64_t chunk, uint8_t *b) {
+    pthread_once(&ZW_once, zw_init);
+    uint64_t s = chunk_state(seed, chunk);
+    uint32_t o = 0;
+    while (o < PG_CHUNK) {
+        const uint64_t u = pg_splitmix64_next(&s) >> 32; /* uniform in [0, 2^32) */
+        int lo = 0, hi = ZW_N - 1;                        /* first rank with cdf > u */
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (ZW.cdf[mid] > u) hi = mid; else lo = mid + 1;
+        }
+        for (int k = 0; k < ZW.len[lo] && o < PG_CHUNK; k++) b[o++] = (uint8_t)ZW.w[lo][k];
+        if (o < PG_CHUNK) b[o++] = ' ';
+    }
+}
+
 static void gen_background(const pg_config *c, uint64_t chunk, uint8_t *b) {
     switch (c->id) {
-    case 1: case 2: case 6: bg_printable(c->seed_text, chunk, b); break;
+    case 1: case 2: case 6: case 8: bg_printable(c->seed_text, chunk, b); break;
+    case 7: bg_zipf_words(c->seed_text, chunk, b); break;
     case 3: bg_packets(c->seed_text, chunk, b); break;
     case 4: bg_uniform(c->seed_text, chunk, b); break;
     case 5: bg_dna(c->seed_text, chunk, b); break;
@@ -508,7 +559,7 @@ int pg_make_patterns(const pg_config *c, uint8_t **data, uint32_t **lens, uint32
     if (c->id == 1) {
         static const char *toy[4] = {"he", "she", "his", "hers"};
         for (int i = 0; i < 4; i++) ps_add(&ps, (const uint8_t *)toy[i], (uint32_t)strlen(toy[i]));
-    } else if (c->id == 2 || c->id == 4 || c->id == 6) {
+    } else if (c->id == 2 || c->id == 4 || c->id == 6 || c->id == 8) {
         uint32_t span = c->max_len - c->min_len + 1;
         while (ps.n < c->n_patterns) {
             uint32_t l = c->min_len + (uint32_t)mt_unif(&mt, span);
@@ -551,6 +602,18 @@ int pg_make_patterns(const pg_config *c, uint8_t **data, uint32_t **lens, uint32
                 for (int k = 0; k < C3V.len[t] && o + 2 < l; k++) p[o++] = (uint8_t)C3V.tok[t][k];
                 while (o < l) p[o++] = (uint8_t)mt_unif(&mt, 256);
             }
+            ps_add(&ps, p, l);
+        }
+    } else if (c->id == 7) {
+        /* substrings of the first 4 MiB of the text's background */
+        bgchunks = 4;
+        bgcache = (uint8_t *)malloc(bgchunks * PG_CHUNK);
+        if (!bgcache) return -1;
+        for (uint64_t ch = 0; ch < bgchunks; ch++) gen_background(c, ch, bgcache + ch * PG_CHUNK);
+        while (ps.n < c->n_patterns) {
+            uint32_t l = c->min_len + (uint32_t)mt_unif(&mt, c->max_len - c->min_len + 1);
+            uint64_t off = mt_unif(&mt, bgchunks * PG_CHUNK - l + 1);
+            memcpy(p, bgcache + off, l);
             ps_add(&ps, p, l);
         }
     } else if (c->id == 5) {

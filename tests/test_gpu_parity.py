@@ -242,7 +242,7 @@ def _full_size_exact(cid, n_bytes, engine):
     return len(pos)
 
 
-@pytest.mark.parametrize("cid", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("cid", [2, 3, 4, 5, 6, 7, 8])
 def test_configs_unaligned_exact(cid):
     """4 MiB of each config's text at a 16-byte-unaligned device address (the
     lane-copy ring path instead of TMA for every round), every filter kind
@@ -301,12 +301,12 @@ def test_full_c2_exact():
 
 
 @pytest.mark.parametrize("cid,n_bytes,engine", [(3, 1 << 30, "pfac"), (4, 4 << 30, "pfac"), (5, 2 << 30, "ac"),
-                                                (6, 1 << 30, "pfac")],
-                         ids=["C3-1GiB", "C4-4GiB", "C5-2GiB", "C4ascii-1GiB"])
+                                                (6, 1 << 30, "pfac"), (7, 64 << 20, "pfac"), (8, 64 << 20, "pfac")],
+                         ids=["C3-1GiB", "C4-4GiB", "C5-2GiB", "C4ascii-1GiB", "C2paper-64MiB", "C2dense-64MiB"])
 def test_full_size_exact(cid, n_bytes, engine):
     """C3 1 GiB, C4 4 GiB (the metric's config: 2^32 start positions in one
-    launch), C5 2 GiB (its per-GPU share at G=8), 1 GiB of C4's ASCII variant:
-    full-array exact parity.
+    launch), C5 2 GiB (its per-GPU share at G=8), 1 GiB of C4's ASCII variant
+    and C2's paper-shaped and dense variants: full-array exact parity.
     The oracle engine is the PFAC walk, or for C5 the textbook Aho-Corasick
     DFA (both engines are pinned in test_oracle.py)."""
     assert _full_size_exact(cid, n_bytes, engine) > 0
