@@ -1800,12 +1800,16 @@ Geometry geometry(uint64_t n_starts, int sms) {
     g.warps = g.grid * kWarps;
     g.rounds_per_cta = (g.n_rounds + g.grid - 1) / g.grid;
     if (g.rounds_per_cta < 1) g.rounds_per_cta = 1;
-    // hit records per warp: 1/16 of twice its average share of starts,
-    // between 64 and 4096 (a warp that finds more re-scans its rounds in
-    // phase 3 instead)
-    uint64_t cap = 2 * ((g.rounds_per_cta + kWarps - 1) / kWarps) * kRound / 16;
+    // hit records per warp: a quarter of its average share of starts (dense-
+    // match texts such as C2's paper-shaped variant, a word text with word
+    // patterns, hit a third of all positions: with 1/16 the hit lists
+    // overflowed into the re-scan path, 7.0 -> 2.75 ms), at least 64, and at
+    // most 4096 or what keeps all hit lists within 256 MiB (a warp that finds
+    // more re-scans its rounds in phase 3)
+    uint64_t cap = ((g.rounds_per_cta + kWarps - 1) / kWarps) * kRound / 4;
+    const uint64_t cap_max = std::max<uint64_t>(4096, (256ull << 20) / (8ull * g.warps));
     if (cap < 64) cap = 64;
-    if (cap > 4096) cap = 4096;
+    if (cap > cap_max) cap = cap_max;
     g.hit_cap = (uint32_t)cap;
     g.off_owner = kWsFixed + 8 * g.n_rounds;
     g.off_hits = g.off_owner + ((4 * g.n_rounds + 15) & ~15ull);
