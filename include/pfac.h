@@ -230,7 +230,10 @@ void pfac_matches_free(pfac_matches *m);
 
 /* --------------------------------------------------------- match, device */
 
-/* Workspace bytes pfac_match_device needs for n_starts start positions. */
+/* Workspace bytes pfac_match_device needs for n_starts start positions: a
+ * small fixed header, 12 B per 1024-start round, and the per-warp hit lists
+ * (sized for one hit per four starts, at most ~256 MiB; a warp that finds
+ * more re-scans its rounds, so the result never depends on this size). */
 pfac_status pfac_workspace_bytes(const pfac_trie *t, uint64_t n_starts, uint64_t *out);
 
 /* Stream-ordered scan on `device` (which must be the current device), all
