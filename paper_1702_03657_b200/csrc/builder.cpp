@@ -785,6 +785,7 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
         h.off_rank_term = o; o = align256(o + 4 * rank_term.size());
     }
     h.off_rec = o;  o = align256(o + 16 * NI);  // node records (image.h)
+    h.off_term_rk = o;  o = align256(o + 8 * ((NI + 31) / 32));  // kept-terminal rank (image.h, v22)
     h.n_dag_nodes = ND;
     h.n_dag_edges = ED;
     h.bytes_merged = bytes_merged;
@@ -838,6 +839,17 @@ int build_image(const uint8_t *const *pats, const uint32_t *lens, uint32_t m, co
         }
     }
     if (!kset.empty()) std::memcpy(p + h.off_kset, kset.data(), 4 * kset.size());
+    {   // kept-terminal rank {bits, rank} per 32 nodes
+        uint32_t *rk = reinterpret_cast<uint32_t *>(p + h.off_term_rk);
+        uint32_t acc = 0;
+        for (uint64_t w = 0; w < (NI + 31) / 32; w++) {
+            uint32_t bits = 0;
+            for (uint64_t b = 0; b < 32 && 32 * w + b < NI; b++) bits |= ((node_word[32 * w + b] >> 31) & 1u) << b;
+            rk[2 * w] = bits;
+            rk[2 * w + 1] = acc;
+            acc += (uint32_t)__builtin_popcount(bits);
+        }
+    }
     {   // node records {node[v], node[v+1], aux[v], 0}
         uint32_t *rec = reinterpret_cast<uint32_t *>(p + h.off_rec);
         for (uint64_t v = 0; v < NI; v++) {
@@ -973,6 +985,18 @@ int validate_image(const uint8_t *p, uint64_t size, std::string &err) {
         for (uint64_t v = 0; ok && v < N; v++)
             if (node[v] & kTermBit) ok = k < h.n_kept_terminals && tn[k++] == v;
         ok = ok && k == h.n_kept_terminals;
+        // kept-terminal rank: the terminal bits and their prefix counts
+        ok = ok && in(h.off_term_rk, 8 * ((N + 31) / 32));
+        if (ok) {
+            const uint32_t *rk = reinterpret_cast<const uint32_t *>(p + h.off_term_rk);
+            uint32_t acc2 = 0;
+            for (uint64_t w = 0; ok && w < (N + 31) / 32; w++) {
+                uint32_t want = 0;
+                for (uint64_t b = 0; b < 32 && 32 * w + b < N; b++) want |= ((node[32 * w + b] >> 31) & 1u) << b;
+                ok = rk[2 * w] == want && rk[2 * w + 1] == acc2;
+                acc2 += (uint32_t)__builtin_popcount(want);
+            }
+        }
         // node records: copies of the node and aux words
         ok = ok && in(h.off_rec, 16 * N);
         const uint32_t *rc = reinterpret_cast<const uint32_t *>(p + h.off_rec);

@@ -27,6 +27,11 @@
 //   term_node u32[TK] ascending ids of the terminal nodes kept in the image
 //                     (terminal indices 0..TK-1); terminal indices TK..T-1 are
 //                     the ends of the compressed tails, in tail order.
+//   term_rk uint2[ceil(N/32)] {bits, rank} per 32 nodes: bit v & 31 = node v
+//                     has the terminal bit; rank = kept terminals before node
+//                     32 * (v / 32).  A kept terminal's index = rank + popc(bits
+//                     below v): one 8-byte load instead of a binary search of
+//                     term_node (dense-match texts end most walks on one; v22).
 //   out_ptr u32[T+1]  offsets into out_pid, by terminal index.
 //   out_pid u32[..]   per terminal t, the ascending union of the pattern ids
 //                     ending on the root->t path.  A walk passes every ancestor
@@ -163,7 +168,7 @@
 
 namespace pfac {
 
-constexpr uint32_t kVersion = 21;
+constexpr uint32_t kVersion = 22;
 constexpr uint32_t kTermBit = 0x80000000u;
 constexpr uint32_t kTailBit = 0x40000000u;
 constexpr uint32_t kEdgeMask = 0x3FFFFFFFu;
@@ -201,7 +206,8 @@ struct ImageHeader {
     uint64_t bytes_merged, bytes_merged_crs;               // 36 B x DAG nodes; its N x 9 CRS words x 4
     uint64_t pipe_depth, bytes_pipe_trunc, bytes_pipe_merged, bytes_pipe_crs;  // the paper's pipeline (below)
     uint64_t off_rec;                  // node records uint4[N] (below)
-    uint8_t pad[512 - 256 - 64 - 112];
+    uint64_t off_term_rk;              // kept-terminal rank uint2[ceil(N/32)] (below; v22)
+    uint8_t pad[512 - 256 - 64 - 120];
 };
 static_assert(sizeof(ImageHeader) == 512, "header must be 512 bytes");
 

@@ -63,6 +63,7 @@ struct DevTrie {
     const uint4 *rec;     // per node: {node[v], node[v+1], aux[v], 0} (image.h)
     const uint8_t *label;
     const uint32_t *term_node;
+    const uint2 *term_rk;  // kept-terminal rank {bits, rank} per 32 nodes (image v22)
     const uint32_t *out_ptr;
     const uint32_t *out_pid;
     const uint32_t *root;

@@ -143,7 +143,7 @@ struct ScanArgs {
     uint32_t off_root, off_node, off_label, off_warps, off_sbar, off_warp, off_bm, off_pair, off_aux;
     uint32_t off_tails, off_tbytes;
     uint32_t hot_tails, hot_tail_bytes;  // records (and their bytes) of the record nodes < H
-    uint32_t off_terms;             // out_ptr[T+1] + term_node[TK] in smem (0 = in global memory)
+    uint32_t off_terms;             // out_ptr[T+1] in smem (0 = in global memory)
     uint32_t n_level1;              // B: the root's children are nodes [1, B]
     uint32_t hot_nodes;             // H: node words [0, H] resident
     uint32_t hot_edges;             // row_ptr[H]: labels [0, hot_edges) resident
@@ -336,7 +336,6 @@ struct Smem {
     uint32_t tails;             // tail records [0, hot_tails), 16 bytes each
     uint32_t tail_bytes;        // their bytes [0, hot_tail_bytes)
     const uint32_t *out_ptr;    // pid-list offsets by terminal index (smem or global)
-    const uint32_t *term_node;  // kept terminal node ids (smem or global)
 };
 // Loads from the staged (immutable after staging) tables: plain asm, so the
 // compiler may schedule and merge them freely.
@@ -433,18 +432,14 @@ struct GlobalText {
 // [1, B]) uses the paper's bitmapped node (Fig. 3: 256-bit child
 // bitmap + offset, child = offset + rank of c among the set bits); deeper
 // nodes use the CSR label list of the image.
-// Terminal index of kept terminal node v: binary search in term_node (shared
-// memory when staged, else global; plain loads through a generic pointer).
-__device__ __forceinline__ uint32_t term_index(const uint32_t *term_node, uint32_t n, uint32_t v) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (term_node[mid] < v) lo = mid + 1; else hi = mid;
-    }
-    return lo;
+// Terminal index of kept terminal node v from the rank structure (image
+// v22): one 8-byte load, no search
+__device__ __forceinline__ uint32_t term_rank(const uint2 *rk, uint32_t v) {
+    const uint2 r = __ldg(rk + (v >> 5));
+    return r.y + __popc(r.x & ((1u << (v & 31)) - 1u));
 }
-// terminal index of node `last` (kNone stays kNone); needs `a` and `s` in scope
-#define term_of(last_) ((last_) == kNone ? kNone : term_index(s.term_node, a.t.n_kept_terminals, (last_)))
+// terminal index of node `last` (kNone stays kNone); needs `a` in scope
+#define term_of(last_) ((last_) == kNone ? kNone : term_rank(a.t.term_rk, (last_)))
 
 // Jump at a tail or chain start v (node word bit 30) with the next text
 // byte at offset j: its record holds the L bytes of the single path below v.
@@ -850,7 +845,6 @@ __device__ __forceinline__ Smem make_smem(const ScanArgs &a) {
     Smem s;
     // terminal tables: shared-memory copies when staged (generic pointers)
     s.out_ptr = a.off_terms ? reinterpret_cast<const uint32_t *>(smem_base + a.off_terms) : a.t.out_ptr;
-    s.term_node = a.off_terms ? s.out_ptr + a.t.n_terminals + 1 : a.t.term_node;
     const uint32_t sb = kCl ? smem_u32(smem_base) : kSmemBase;  // (see kSmemBase)
     s.root = sb + a.off_root;
     s.bm = sb + a.off_bm;
@@ -1274,7 +1268,6 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             uint32_t *so = reinterpret_cast<uint32_t *>(smem + a.off_terms);
             const uint32_t n_op = a.t.n_terminals + 1;
             for (uint32_t j = tid; j < n_op; j += kThreads) so[j] = __ldg(a.t.out_ptr + j);
-            for (uint32_t j = tid; j < a.t.n_kept_terminals; j += kThreads) so[n_op + j] = __ldg(a.t.term_node + j);
         }
     }
     STAMP(8);
@@ -1994,9 +1987,9 @@ int make_plan(const DevTrie &t, const uint8_t *host_image, const DeviceInfo &di,
     a.off_aux = off;    off += align16(4 * (H + 1));
     a.off_label = off;  off += align16(EH);
     {   // terminal tables in smem when small and they fit what is left
-        const uint32_t tb = align16(4 * (uint32_t)(hh.n_terminals + 1 + hh.n_kept_terminals));
+        const uint32_t tb = align16(4 * (uint32_t)(hh.n_terminals + 1));
         a.off_terms = 0;
-        if (hh.n_terminals + 1 + hh.n_kept_terminals < 8192 &&
+        if (hh.n_terminals + 1 < 8192 &&
             off + tb + 16 * TH + align16(TBH) <= (uint32_t)di.max_smem_optin) {
             a.off_terms = off;
             off += tb;
@@ -2094,6 +2087,7 @@ DevTrie make_dev_trie(const ImageHeader &h, const uint8_t *d) {
     t.rec = reinterpret_cast<const uint4 *>(d + h.off_rec);
     t.label = d + h.off_label;
     t.term_node = reinterpret_cast<const uint32_t *>(d + h.off_term_node);
+    t.term_rk = reinterpret_cast<const uint2 *>(d + h.off_term_rk);
     t.out_ptr = reinterpret_cast<const uint32_t *>(d + h.off_out_ptr);
     t.out_pid = reinterpret_cast<const uint32_t *>(d + h.off_out_pid);
     t.root = reinterpret_cast<const uint32_t *>(d + h.off_root);

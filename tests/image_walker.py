@@ -10,7 +10,7 @@ TERM = 0x80000000
 TAIL = 0x40000000
 MASK = 0x3FFFFFFF
 
-_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II Q II Q QQQQQQQ QQ QQQQ Q")
+_HDR = struct.Struct("<8sII Q QQQQ IIII IIII QQQQQQQ QQQQ QQQQQQ QQ QQ Q II Q Q II Q II Q QQQQQQQ QQ QQQQ Q Q")
 VERIFY = 0xFFFFFFFE
 
 
@@ -25,7 +25,7 @@ def parse(image: bytes) -> dict:
             "off_entry", "entry_log2", "entry_pad", "n_cand", "trunc_depth", "trunc_pad", "bytes_truncated",
             "n_dag_nodes", "n_dag_edges", "off_dag_node", "off_dag_label", "off_dag_child", "off_dag_skip",
             "off_rank_term", "bytes_merged", "bytes_merged_crs", "pipe_depth", "bytes_pipe_trunc",
-            "bytes_pipe_merged", "bytes_pipe_crs", "off_rec"]
+            "bytes_pipe_merged", "bytes_pipe_crs", "off_rec", "off_term_rk"]
     h = dict(zip(keys, f))
     buf = np.frombuffer(image, np.uint8)
     N, E, T = h["n_nodes"], h["n_edges"], h["n_terminals"]
@@ -49,6 +49,7 @@ def parse(image: bytes) -> dict:
     if h["off_kset"]:
         h["kset"] = buf[h["off_kset"]:h["off_kset"] + (4 << h["kset_log2"])].view(np.uint32)
     h["rec"] = buf[h["off_rec"]:h["off_rec"] + 16 * N].view(np.uint32).reshape(-1, 4)
+    h["term_rk"] = buf[h["off_term_rk"]:h["off_term_rk"] + 8 * ((N + 31) // 32)].view(np.uint32).reshape(-1, 2)
     if h["n_dag_nodes"]:
         ND, ED = h["n_dag_nodes"], h["n_dag_edges"]
         h["dag_node"] = buf[h["off_dag_node"]:h["off_dag_node"] + 4 * (ND + 1)].view(np.uint32)

@@ -295,3 +295,19 @@ def test_option_struct_layouts_match_header(tmp_path):
         assert got[(cname, "size")] == C.sizeof(py), cname
         for f, _ in py._fields_:
             assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_terminal_rank_matches_term_node(cid):
+    """Image v22's kept-terminal rank (bits + per-32-node prefix counts) gives
+    every kept terminal node its index in the ascending term_node list (the
+    definition), and no other node has the terminal bit."""
+    h = image_walker.parse(pf.Trie(gen.patterns(cid)).image())
+    rk = h["term_rk"].astype(np.uint64)
+    tn = h["term_node"].astype(np.int64)
+    v = tn
+    below = rk[v >> 5, 0] & ((np.uint64(1) << (v & 31).astype(np.uint64)) - np.uint64(1))
+    popc = np.array([bin(int(x)).count("1") for x in below], np.uint64)
+    assert np.array_equal(rk[v >> 5, 1] + popc, np.arange(len(tn), dtype=np.uint64))
+    bits = np.unpackbits(h["term_rk"][:, 0].astype("<u4").view(np.uint8), bitorder="little")[: h["n_nodes"]]
+    assert np.array_equal(np.nonzero(bits)[0], tn)

@@ -101,6 +101,8 @@ CORRUPTIONS = {
     "level1_prefix": lambda b, h: _u32(b, h["off_level1"] + 4 * 8, int(h["level1"][0][8]) ^ 0x0100),
     "tail_rank": lambda b, h: _u32(b, h["off_tail_rank"] + 4, int(h["tail_rank"][1]) + 1),
     "tail_bits": lambda b, h: _u32(b, h["off_tail_bits"], int(h["tail_bits"][0]) ^ 1),
+    "term_rank": lambda b, h: _u32(b, h["off_term_rk"] + 12, int(h["term_rk"][1][1]) + 1),
+    "term_bits": lambda b, h: _u32(b, h["off_term_rk"], int(h["term_rk"][0][0]) ^ 2),
 }
 
 
