@@ -3,6 +3,7 @@
 #include "pfac.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // host ranges for timeline profilers (no-ops when none is attached)
 
 #include <algorithm>
 #include <cstdlib>
@@ -22,6 +23,14 @@ using namespace pfac;
 // streaming pipeline's streams, events, text buffers (chunk + halo each),
 // pinned staging buffers (pageable input), workspace, per-chunk outputs.
 constexpr int kStreamBufs = 3;
+// A host range on the NVTX timeline (nsys / ncu --nvtx) for one API call.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 struct HostCtx {
     std::mutex mu;  // one pfac_match at a time per handle and device
     cudaStream_t copy = nullptr, comp = nullptr;
@@ -333,6 +342,7 @@ pfac_status pfac_match_device_ex(const pfac_trie *t, int device, const uint8_t *
                                  uint64_t n_starts, uint64_t pos_base, uint64_t *d_pos, uint32_t *d_pid,
                                  uint64_t capacity, uint64_t *d_count, void *d_workspace, uint64_t workspace_bytes,
                                  const pfac_plan_options *opt, pfac_stream stream) {
+    const NvtxRange range("pfac_match_device");
     if (!t || !d_count || (n_starts && !d_text) || (capacity && (!d_pos || !d_pid)))
         return fail(kStatusInvalid, "pfac_match_device: NULL argument");
     if (n_starts > readable_len) return fail(kStatusInvalid, "pfac_match_device: n_starts > readable_len");
@@ -382,6 +392,7 @@ pfac_status pfac_plan_query(const pfac_trie *t, int device, uint64_t n_starts, c
 }
 
 pfac_status pfac_match(const pfac_trie *t, const uint8_t *text, uint64_t len, pfac_matches *out) {
+    const NvtxRange range("pfac_match");
     if (!t || !out || (len && !text)) return fail(kStatusInvalid, "pfac_match: NULL argument");
     out->count = 0;
     out->pos = nullptr;
